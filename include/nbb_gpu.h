@@ -1,0 +1,192 @@
+/*
+ * nbb_gpu.h — C ABI of the B200-native λ(ω) / bounding-box launch engine.
+ *
+ * Drop-in boundary for the reference's workload entry points
+ * (/root/reference/proj/include/nbb/dispatch.hpp). The reference's operator API
+ * is `launch(const DispatchConfig&, const Kernel&)` with a host std::function
+ * kernel (dispatch.hpp:100-108); a host closure cannot run on the device, so the
+ * boundary sits one level up, at the three workloads the reference ships
+ * (SURVEY.md §8(b)):
+ *
+ *   reference (C++, dispatch.hpp)                         replaced by (this header)
+ *   -----------------------------------------------------------------------------
+ *   DispatchConfig::validate()          dispatch.cpp:50-114  nbb_gpu_validate
+ *   launch_block_count(config)          dispatch.cpp:475-479 nbb_gpu_launch_block_count
+ *   run_single_write(config)            dispatch.cpp:481-488 nbb_gpu_single_write
+ *   run_reduction(config, grid)         dispatch.cpp:490-515 nbb_gpu_reduction
+ *   run_ca(config, initial, steps, rule) dispatch.cpp:517-557 nbb_gpu_ca
+ *   work_quotient(bb, lambda, weighted) dispatch.cpp:559-572 nbb_gpu_work_quotient
+ *   WorkReport::csv_header/csv_row      dispatch.cpp:116-127 nbb_gpu_csv_header / nbb_gpu_report_csv_row
+ *   random_member_grid(spec,r,seed,mod) dispatch.cpp:133-149 nbb_gpu_random_member_grid
+ *   lambda_map over a whole orthotope   block_map.cpp:77-111 nbb_gpu_lambda_coords
+ *
+ * plus device-resident variants (`*_dev`) that take device pointers and a
+ * cudaStream_t (as void*) so that no PCIe traffic sits inside a timed region.
+ *
+ * All buffers are plain pointers + sizes; no torch types. Grids are the
+ * reference's dense row-major embedding (index = y*n + x, n = 2^r) of int64
+ * cells (dispatch.hpp:74-79). Every entry point returns an nbb_status; on
+ * failure nbb_gpu_last_error() holds a thread-local message that mirrors the
+ * reference's exception text. There is no CPU fallback: without a CUDA device
+ * every compute entry point returns NBB_ERR_CUDA.
+ */
+#ifndef NBB_GPU_H
+#define NBB_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NBB_GPU_ABI_VERSION 1
+#define NBB_MAX_REPLICAS 9
+
+/* Status codes; the C++ shim (nbb_gpu.hpp) rethrows the matching std:: type. */
+typedef enum nbb_status {
+    NBB_OK = 0,
+    NBB_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument            */
+    NBB_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range                */
+    NBB_ERR_RESOURCE = 3,         /* nbb::ResourceError / bad_alloc   */
+    NBB_ERR_CUDA = 4,             /* CUDA runtime failure / no device */
+    NBB_ERR_NCCL = 5,             /* collective failure               */
+    NBB_ERR_DOMAIN = 6,           /* std::domain_error                */
+    NBB_ERR_OVERFLOW = 7,         /* std::overflow_error              */
+    NBB_ERR_RUNTIME = 8           /* std::runtime_error               */
+} nbb_status;
+
+/* MapMode (dispatch.hpp:16) */
+enum { NBB_MODE_BB = 0, NBB_MODE_LAMBDA = 1 };
+/* IntraBlockStrategy (block_map.hpp:46-50), same enumerator order */
+enum { NBB_STRATEGY_UNROLL = 0, NBB_STRATEGY_LUT = 1, NBB_STRATEGY_SUBBOX = 2 };
+/* LambdaBackend (dispatch.hpp:17) */
+enum { NBB_BACKEND_DIRECT = 0, NBB_BACKEND_MMA1 = 1, NBB_BACKEND_MMA2 = 2, NBB_BACKEND_MMA3 = 3 };
+/* Device kernel family (new; not in the reference):
+ *  AUTO    — fastest implementation of the requested (mode, strategy, backend)
+ *  PERCELL — the paper's one-thread-per-cell blocks of rho x rho threads
+ *  TILE    — warp-per-tile, 32-byte-sector vectorised payload (subbox/direct only) */
+enum { NBB_KERNEL_AUTO = 0, NBB_KERNEL_PERCELL = 1, NBB_KERNEL_TILE = 2 };
+
+/* FractalSpec (fractal.hpp:53-102). Only the gasket runs on the GPU path. */
+typedef struct nbb_spec {
+    char name[32];
+    int32_t k;                       /* replica count  */
+    int32_t s;                       /* scale factor   */
+    int32_t offset_x[NBB_MAX_REPLICAS];
+    int32_t offset_y[NBB_MAX_REPLICAS];
+} nbb_spec;
+
+/* DispatchConfig (dispatch.hpp:25-38) extended with device-side knobs. */
+typedef struct nbb_config {
+    nbb_spec spec;
+    int32_t r;          /* scale level, n = s^r                                */
+    int32_t rho;        /* block edge, one of 1,2,4,8,16,32                     */
+    int32_t mode;       /* NBB_MODE_*                                          */
+    int32_t strategy;   /* NBB_STRATEGY_*                                      */
+    int32_t backend;    /* NBB_BACKEND_*                                       */
+    int32_t workers;    /* reference: host threads; here: devices (>= 1)        */
+    int32_t timing;     /* nonzero: fill report.micros from CUDA events         */
+    int32_t cell_width; /* device cell bytes: 8 (int64, drop-in) or 1 (uint8)   */
+    int32_t kernel;     /* NBB_KERNEL_*                                        */
+    int32_t device;     /* CUDA device ordinal of the first worker              */
+    uint64_t max_cells; /* membership-raster budget (reference kEnumerateBudget) */
+} nbb_config;
+
+/* WorkReport (dispatch.hpp:44-61) */
+typedef struct nbb_report {
+    char spec_name[32];
+    int32_t r;
+    int32_t rho;
+    int32_t mode;
+    int32_t strategy;
+    int32_t backend;
+    int32_t map_levels;
+    uint64_t blocks_launched;
+    uint64_t threads_launched;
+    uint64_t threads_active;
+    uint64_t threads_wasted;
+    uint64_t map_ops;
+    uint64_t micros;
+} nbb_report;
+
+/* ---- library / config helpers ------------------------------------------ */
+int nbb_gpu_abi_version(void);
+const char* nbb_gpu_last_error(void);
+/* gasket, r=0, rho=1, lambda, subbox, direct, workers=1, cell_width=8, 2^24 budget */
+void nbb_config_init(nbb_config* cfg);
+/* FractalSpec::sierpinski/vicsek/carpet (fractal.cpp:80-91) */
+void nbb_spec_sierpinski(nbb_spec* spec);
+void nbb_spec_vicsek(nbb_spec* spec);
+void nbb_spec_carpet(nbb_spec* spec);
+/* Number of CUDA devices visible (0 when none). */
+int nbb_gpu_device_count(int32_t* count);
+
+/* ---- host logic (no device needed) --------------------------------------- */
+int nbb_gpu_validate(const nbb_config* cfg);
+int nbb_gpu_launch_block_count(const nbb_config* cfg, uint64_t* blocks);
+/* Closed-form WorkReport of one launch; micros = 0. */
+int nbb_gpu_plan_report(const nbb_config* cfg, nbb_report* report);
+int nbb_gpu_work_quotient(const nbb_report* bb, const nbb_report* lambda, int32_t weighted,
+                          double* quotient);
+const char* nbb_gpu_csv_header(void);
+/* Writes WorkReport::csv_row() into buf (NUL-terminated); len >= 256 suffices. */
+int nbb_gpu_report_csv_row(const nbb_report* report, char* buf, size_t len);
+/* random_member_grid (dispatch.cpp:133-149), bit-identical, O(3^r) host loop.
+ * out_grid: n*n int64, fully written (non-members 0). */
+int nbb_gpu_random_member_grid(const nbb_spec* spec, int32_t r, uint64_t seed, uint64_t modulus,
+                               uint64_t max_cells, int64_t* out_grid);
+/* Member values only, in row-major member order (length 3^r): the same stream
+ * random_member_grid assigns, without the n*n embedding. */
+int nbb_gpu_random_member_values(const nbb_spec* spec, int32_t r, uint64_t seed,
+                                 uint64_t modulus, int64_t* out_values);
+
+/* ---- workloads on host buffers (drop-in) -------------------------------- */
+/* run_single_write: out_grid (n*n int64) receives the whole result grid. */
+int nbb_gpu_single_write(const nbb_config* cfg, int64_t* out_grid, nbb_report* report);
+/* run_reduction: grid (n*n int64) at level grid_level (must equal cfg->r). */
+int nbb_gpu_reduction(const nbb_config* cfg, const int64_t* grid, int32_t grid_level,
+                      int64_t* value, nbb_report* report);
+/* run_ca: `steps` double-buffered steps; per_step receives `steps` reports
+ * (may be NULL). out_grid may alias initial. */
+int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_level,
+               int32_t steps, uint16_t birth, uint16_t survive, int64_t* out_grid,
+               nbb_report* per_step);
+/* λ(ω) for every ω of the level-`level` orthotope, ordinal-major
+ * (xy[2*o], xy[2*o+1], o = ωy*W + ωx). Uses cfg->backend (direct or mma1/mma2). */
+int nbb_gpu_lambda_coords(const nbb_config* cfg, int32_t level, int64_t* xy);
+
+/* ---- device-resident variants (pointers are device pointers) -------------- */
+/* stream: cudaStream_t or NULL for the legacy default stream. */
+int nbb_gpu_single_write_dev(const nbb_config* cfg, void* d_grid, void* stream,
+                             nbb_report* report);
+/* *d_value (device int64) receives the sum; no host synchronisation. */
+int nbb_gpu_reduction_dev(const nbb_config* cfg, const void* d_grid, void* d_value,
+                          void* stream, nbb_report* report);
+/* One CA step d_src -> d_dst. Non-member cells of d_dst must already be 0
+ * (true after nbb_gpu_sanitize_dev / a zeroed allocation); they stay 0. */
+int nbb_gpu_ca_step_dev(const nbb_config* cfg, const void* d_src, void* d_dst, uint16_t birth,
+                        uint16_t survive, void* stream, nbb_report* report);
+/* Zero every non-member cell of a device grid of cfg->cell_width cells. */
+int nbb_gpu_sanitize_dev(const nbb_config* cfg, void* d_grid, void* stream);
+/* int64 grid -> uint8 alive grid (cell != 0) and back (0/1 -> int64). */
+int nbb_gpu_pack_alive_dev(const nbb_config* cfg, const void* d_grid64, void* d_grid8,
+                           void* stream);
+int nbb_gpu_unpack_alive_dev(const nbb_config* cfg, const void* d_grid8, void* d_grid64,
+                             void* stream);
+/* Scatter member values given in row-major member order into a zeroed
+ * embedded device grid (inverse of the host generator's order). */
+int nbb_gpu_scatter_members_dev(const nbb_config* cfg, const void* d_values, void* d_grid,
+                                void* stream);
+/* λ map of the whole level-`level` orthotope into device memory.
+ * coord_bytes = 4 (int32 pairs) or 8 (int64 pairs). */
+int nbb_gpu_lambda_coords_dev(const nbb_config* cfg, int32_t level, void* d_xy,
+                              int32_t coord_bytes, void* stream);
+/* Free the device buffers cached by the host-buffer entry points. */
+int nbb_gpu_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NBB_GPU_H */

@@ -1,0 +1,732 @@
+// nbb_capi.cu — the C ABI of include/nbb_gpu.h: validation, planning, device
+// buffers, and dispatch to the sm_100a kernels.
+//
+// Kernel selection (NBB_KERNEL_AUTO):
+//   tile kernel (tile_kernels.cuh) when the launch is BB, or λ with the subbox
+//   strategy and direct backend, and the tile holds whole 32-byte sectors
+//   (int64: ρ ∈ {8,16,32}; uint8: ρ = 32); otherwise the per-cell kernel
+//   (percell_kernels.cuh), which covers every (strategy, backend) the reference
+//   accepts. Both produce identical grids; WorkReports are the reference's
+//   closed-form counters of the logical launch (nbb_host.cpp).
+// There is no CPU fallback: without a CUDA device every compute call fails with
+// NBB_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "nbb_gpu.h"
+#include "nbb_host.hpp"
+#include "percell_kernels.cuh"
+#include "tile_kernels.cuh"
+#include "util_kernels.cuh"
+
+using namespace nbbgpu;
+using nbbhost::Error;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+int fail(const Error& e) { return fail(e.code, e.msg); }
+
+#define NBB_CUDA(call)                                                                          \
+    do {                                                                                        \
+        cudaError_t _e = (call);                                                                \
+        if (_e != cudaSuccess) {                                                                \
+            return fail(NBB_ERR_CUDA, std::string("CUDA error ") + cudaGetErrorName(_e) + ": " + \
+                                          cudaGetErrorString(_e) + " (" #call ")");             \
+        }                                                                                       \
+    } while (0)
+
+#define NBB_TRY(...)                      \
+    do {                                  \
+        const Error _e = (__VA_ARGS__);   \
+        if (!_e.ok()) return fail(_e);    \
+    } while (0)
+
+#define NBB_CHECK(...)                    \
+    do {                                  \
+        const int _rc = (__VA_ARGS__);    \
+        if (_rc != NBB_OK) return _rc;    \
+    } while (0)
+
+// ---- per-device context ------------------------------------------------------
+struct DeviceCtx {
+    bool ready = false;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    unsigned long long* partials = nullptr;  // 4096 slots + 1 result
+    void* bufs[3] = {nullptr, nullptr, nullptr};
+    size_t buf_bytes[3] = {0, 0, 0};
+    int16_t* lut[6] = {};                    // LocalCellTable per edge 2^i
+};
+
+std::mutex g_mutex;
+std::vector<DeviceCtx> g_ctx;
+
+int ensure_device(int device, DeviceCtx** out) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        return fail(NBB_ERR_CUDA, std::string("no CUDA device available (") +
+                                      (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices") +
+                                      "); the GPU path has no CPU fallback");
+    }
+    if (device < 0 || device >= count)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "device " + std::to_string(device) + " out of range");
+    std::lock_guard<std::mutex> lock(g_mutex);
+    if ((int)g_ctx.size() < count) g_ctx.resize(count);
+    DeviceCtx& c = g_ctx[device];
+    NBB_CUDA(cudaSetDevice(device));
+    if (!c.ready) {
+        cudaDeviceProp prop;
+        NBB_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10) {
+            return fail(NBB_ERR_CUDA, std::string("device ") + prop.name +
+                                          " is not sm_100 (this library is built for sm_100a only)");
+        }
+        c.sms = prop.multiProcessorCount;
+        uint32_t tab[729];
+        for (uint32_t v = 0; v < 729; ++v) tab[v] = xy6_arith(v);
+        NBB_CUDA(cudaMemcpyToSymbol(c_xy729, tab, sizeof(tab)));
+        NBB_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        NBB_CUDA(cudaMalloc(&c.partials, 4097 * sizeof(unsigned long long)));
+        c.ready = true;
+    }
+    *out = &c;
+    return NBB_OK;
+}
+
+int device_buffer(DeviceCtx& c, int slot, size_t bytes, void** out) {
+    if (c.buf_bytes[slot] < bytes) {
+        if (c.bufs[slot]) NBB_CUDA(cudaFree(c.bufs[slot]));
+        c.bufs[slot] = nullptr;
+        c.buf_bytes[slot] = 0;
+        cudaError_t e = cudaMalloc(&c.bufs[slot], bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(NBB_ERR_RESOURCE, "device allocation of " + std::to_string(bytes) +
+                                              " bytes failed: " + cudaGetErrorString(e));
+        }
+        c.buf_bytes[slot] = bytes;
+    }
+    *out = c.bufs[slot];
+    return NBB_OK;
+}
+
+int local_table(DeviceCtx& c, const nbb_spec& s, int edge, const int16_t** out) {
+    int l = 0;
+    while ((1 << l) < edge) ++l;
+    if (!c.lut[l]) {
+        std::vector<int16_t> h((size_t)edge * edge * 2);
+        nbbhost::local_cell_table(s, edge, h.data());
+        NBB_CUDA(cudaMalloc(&c.lut[l], h.size() * sizeof(int16_t)));
+        NBB_CUDA(cudaMemcpy(c.lut[l], h.data(), h.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
+    }
+    *out = c.lut[l];
+    return NBB_OK;
+}
+
+// ---- timing ---------------------------------------------------------------------
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t s = nullptr;
+    bool on = false;
+    Timer(bool enable, cudaStream_t st) : s(st), on(enable) {
+        if (on) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, s);
+        }
+    }
+    uint64_t stop_micros() {
+        if (!on) return 0;
+        cudaEventRecord(b, s);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        return (uint64_t)(ms * 1000.0f);
+    }
+    ~Timer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+};
+
+// ---- launch helpers -----------------------------------------------------------------
+struct Launch {
+    const nbb_config* cfg;
+    nbbhost::Plan plan;
+    int op;
+    cudaStream_t stream;
+    DeviceCtx* ctx;
+};
+
+bool tile_supported(const nbb_config& c, int op, int cell_width) {
+    if (c.kernel == NBB_KERNEL_PERCELL) return false;
+    if (c.mode == NBB_MODE_LAMBDA &&
+        (c.strategy != NBB_STRATEGY_SUBBOX || c.backend != NBB_BACKEND_DIRECT))
+        return false;
+    if (c.r > 17) return false;
+    if (cell_width == 8) return c.rho == 8 || c.rho == 16 || c.rho == 32;
+    return c.rho == 32 && op != OP_RD;
+}
+
+// rule masks travel in TileArgs; thin wrapper so CA can set them.
+template <typename Cell, int RHO, int OP, bool BB>
+int run_tile_rule(const Launch& L, const void* src, void* dst, unsigned long long* sum,
+                  uint32_t birth, uint32_t survive, uint32_t tile_begin, uint32_t tiles) {
+    auto kern = tile_kernel<Cell, RHO, OP, BB>;
+    static int occ = 0;
+    if (occ == 0) {
+        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0));
+        if (occ < 1) occ = 1;
+    }
+    TileArgs a;
+    a.src = src;
+    a.dst = dst;
+    a.sum = sum;
+    a.n = L.plan.n;
+    a.tile_begin = tile_begin;
+    a.tiles = tiles;
+    a.gw = (uint32_t)L.plan.gw;
+    nbbhost::fastdiv_magic(a.gw, &a.div_gw.m, &a.div_gw.s);
+    a.div_gw.d = a.gw;
+    a.birth = birth;
+    a.survive = survive;
+    constexpr int TPW = 32 / RHO;
+    const uint64_t units = (tiles + TPW - 1) / TPW;
+    const uint64_t want = (units + 7) / 8;
+    const uint64_t cap = (uint64_t)L.ctx->sms * (uint64_t)occ;
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min(want, cap));
+    if (tiles == 0) return NBB_OK;
+    kern<<<blocks, 256, 0, L.stream>>>(a);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+template <typename Cell, int OP, bool BB>
+int dispatch_tile_rho(const Launch& L, const void* src, void* dst, unsigned long long* sum,
+                      uint32_t birth, uint32_t survive, uint32_t tile_begin, uint32_t tiles) {
+    if (sizeof(Cell) == 1) {
+        if constexpr (OP != OP_RD) {
+            return run_tile_rule<unsigned char, 32, OP, BB>(L, src, dst, sum, birth, survive,
+                                                            tile_begin, tiles);
+        }
+        return fail(NBB_ERR_INVALID_ARGUMENT, "reduction needs int64 cells");
+    }
+    switch (L.cfg->rho) {
+        case 8: return run_tile_rule<long long, 8, OP, BB>(L, src, dst, sum, birth, survive, tile_begin, tiles);
+        case 16: return run_tile_rule<long long, 16, OP, BB>(L, src, dst, sum, birth, survive, tile_begin, tiles);
+        case 32: return run_tile_rule<long long, 32, OP, BB>(L, src, dst, sum, birth, survive, tile_begin, tiles);
+    }
+    return fail(NBB_ERR_INVALID_ARGUMENT, "tile kernel needs rho in {8, 16, 32}");
+}
+
+template <typename Cell, int OP>
+int launch_tile(const Launch& L, const void* src, void* dst, unsigned long long* sum,
+                uint32_t birth, uint32_t survive) {
+    const uint32_t tiles = (uint32_t)L.plan.blocks();
+    // workers > 1: contiguous ordinal chunks (dispatch.cpp:419-427), run in order
+    const uint32_t workers = (uint32_t)std::max(1, L.cfg->workers);
+    const uint32_t chunk = (tiles + workers - 1) / workers;
+    for (uint32_t w = 0; w < workers; ++w) {
+        const uint32_t begin = w * chunk;
+        if (begin >= tiles) break;
+        const uint32_t count = std::min(chunk, tiles - begin);
+        int rc = L.cfg->mode == NBB_MODE_BB
+                     ? dispatch_tile_rho<Cell, OP, true>(L, src, dst, sum, birth, survive, begin, count)
+                     : dispatch_tile_rho<Cell, OP, false>(L, src, dst, sum, birth, survive, begin, count);
+        if (rc != NBB_OK) return rc;
+    }
+    return NBB_OK;
+}
+
+template <typename Cell, int OP, bool BB, int STRATEGY, int BACKEND>
+int run_percell(const Launch& L, const PercellArgs& a) {
+    const uint64_t B = a.total_blocks;
+    if (B == 0) return NBB_OK;
+    const unsigned threads = (unsigned)std::max(32, a.edge * a.edge);
+    const uint64_t X = std::min<uint64_t>(B, 65536);
+    const uint64_t Y = std::min<uint64_t>((B + X - 1) / X, 65535);
+    const uint64_t Z = (B + X * Y - 1) / (X * Y);
+    dim3 grid((unsigned)X, (unsigned)Y, (unsigned)Z);
+    percell_kernel<Cell, OP, BB, STRATEGY, BACKEND><<<grid, threads, 0, L.stream>>>(a);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+template <typename Cell, int OP>
+int launch_percell(const Launch& L, const void* src, void* dst, uint32_t birth, uint32_t survive) {
+    const nbb_config& c = *L.cfg;
+    PercellArgs a;
+    a.src = src;
+    a.dst = dst;
+    a.partials = L.ctx->partials;
+    a.n = L.plan.n;
+    a.total_blocks = L.plan.blocks();
+    a.gw = (uint64_t)L.plan.gw;
+    a.edge = L.plan.edge;
+    a.map_level = L.plan.map_level;
+    a.local_level = L.plan.local_level;
+    a.local_w = (int)L.plan.local_w;
+    a.local_members = (int)L.plan.local_members;
+    a.sub_w = L.plan.sub_w;
+    a.sub_h = L.plan.sub_h;
+    a.lut = nullptr;
+    a.birth = birth;
+    a.survive = survive;
+    if (c.mode == NBB_MODE_LAMBDA && c.strategy == NBB_STRATEGY_LUT)
+        NBB_CHECK(local_table(*L.ctx, c.spec, L.plan.edge, &a.lut));
+    if (c.mode == NBB_MODE_BB)
+        return run_percell<Cell, OP, true, NBB_STRATEGY_SUBBOX, NBB_BACKEND_DIRECT>(L, a);
+#define NBB_PC_BACKENDS(ST)                                                                   \
+    switch (c.backend) {                                                                      \
+        case NBB_BACKEND_DIRECT: return run_percell<Cell, OP, false, ST, NBB_BACKEND_DIRECT>(L, a); \
+        case NBB_BACKEND_MMA1: return run_percell<Cell, OP, false, ST, NBB_BACKEND_MMA1>(L, a); \
+        case NBB_BACKEND_MMA2: return run_percell<Cell, OP, false, ST, NBB_BACKEND_MMA2>(L, a); \
+    }
+    switch (c.strategy) {
+        case NBB_STRATEGY_SUBBOX:
+            if (c.backend == NBB_BACKEND_MMA3)
+                return run_percell<Cell, OP, false, NBB_STRATEGY_SUBBOX, NBB_BACKEND_MMA3>(L, a);
+            NBB_PC_BACKENDS(NBB_STRATEGY_SUBBOX)
+            break;
+        case NBB_STRATEGY_UNROLL:
+            NBB_PC_BACKENDS(NBB_STRATEGY_UNROLL)
+            break;
+        case NBB_STRATEGY_LUT:
+            NBB_PC_BACKENDS(NBB_STRATEGY_LUT)
+            break;
+    }
+#undef NBB_PC_BACKENDS
+    return fail(NBB_ERR_INVALID_ARGUMENT, "unsupported strategy/backend combination");
+}
+
+// one workload launch (SW / RD / CA step) on device buffers
+int launch_op(const Launch& L, int op, const void* src, void* dst, unsigned long long* d_sum,
+              uint32_t birth, uint32_t survive) {
+    const nbb_config& c = *L.cfg;
+    const int cw = op == OP_RD ? 8 : c.cell_width;
+    const bool tile = tile_supported(c, op, cw);
+    if (c.kernel == NBB_KERNEL_TILE && !tile)
+        return fail(NBB_ERR_INVALID_ARGUMENT,
+                    "tile kernel needs bb or lambda/subbox/direct, rho in {8,16,32} (int64) or "
+                    "rho = 32 (uint8), r <= 17");
+    if (op == OP_RD) {
+        if (tile) {
+            NBB_CUDA(cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), L.stream));
+            return launch_tile<long long, OP_RD>(L, src, nullptr, d_sum, 0, 0);
+        }
+        NBB_CUDA(cudaMemsetAsync(L.ctx->partials, 0, 4096 * sizeof(unsigned long long), L.stream));
+        NBB_CHECK(launch_percell<long long, OP_RD>(L, src, nullptr, 0, 0));
+        reduce_partials_kernel<<<1, 1024, 0, L.stream>>>(L.ctx->partials, 4096, d_sum);
+        NBB_CUDA(cudaGetLastError());
+        return NBB_OK;
+    }
+    if (cw == 8) {
+        if (tile) {
+            return op == OP_SW ? launch_tile<long long, OP_SW>(L, src, dst, nullptr, 0, 0)
+                               : launch_tile<long long, OP_CA>(L, src, dst, nullptr, birth, survive);
+        }
+        return op == OP_SW ? launch_percell<long long, OP_SW>(L, src, dst, 0, 0)
+                           : launch_percell<long long, OP_CA>(L, src, dst, birth, survive);
+    }
+    if (tile) {
+        return op == OP_SW ? launch_tile<unsigned char, OP_SW>(L, src, dst, nullptr, 0, 0)
+                           : launch_tile<unsigned char, OP_CA>(L, src, dst, nullptr, birth, survive);
+    }
+    return op == OP_SW ? launch_percell<unsigned char, OP_SW>(L, src, dst, 0, 0)
+                       : launch_percell<unsigned char, OP_CA>(L, src, dst, birth, survive);
+}
+
+int prepare(const nbb_config* cfg, int op, Launch* L, bool need_budget) {
+    if (cfg == nullptr) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_TRY(nbbhost::validate(*cfg));
+    NBB_TRY(nbbhost::require_gasket(cfg->spec));
+    if (need_budget) NBB_TRY(nbbhost::member_mask_budget(cfg->spec, cfg->r, cfg->max_cells));
+    L->cfg = cfg;
+    L->op = op;
+    NBB_TRY(nbbhost::make_plan(*cfg, &L->plan));
+    if (L->plan.n > (int64_t(1) << 20))
+        return fail(NBB_ERR_RESOURCE, "embedding side " + std::to_string(L->plan.n) +
+                                          " exceeds the device path limit 2^20");
+    NBB_CHECK(ensure_device(cfg->device, &L->ctx));
+    return NBB_OK;
+}
+
+void fill_report(const nbb_config* cfg, nbb_report* r, uint64_t micros) {
+    if (!r) return;
+    nbbhost::plan_report(*cfg, r);
+    r->micros = cfg->timing ? micros : 0;
+}
+
+int sanitize(const Launch& L, void* d_grid, int cell_width, cudaStream_t s) {
+    const int blocks = L.ctx->sms * 8;
+    if (cell_width == 8)
+        sanitize_kernel<long long><<<blocks, 256, 0, s>>>((long long*)d_grid, L.plan.n, 0);
+    else
+        sanitize_kernel<unsigned char><<<blocks, 256, 0, s>>>((unsigned char*)d_grid, L.plan.n, 0);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+size_t grid_bytes(const Launch& L, int cw) { return (size_t)L.plan.n * (size_t)L.plan.n * cw; }
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+int nbb_gpu_abi_version(void) { return NBB_GPU_ABI_VERSION; }
+const char* nbb_gpu_last_error(void) { return g_last_error.c_str(); }
+
+void nbb_spec_sierpinski(nbb_spec* s) {
+    std::memset(s, 0, sizeof(*s));
+    std::strcpy(s->name, "sierpinski");
+    s->k = 3;
+    s->s = 2;
+    const int ox[] = {0, 0, 1}, oy[] = {0, 1, 1};
+    for (int i = 0; i < 3; ++i) {
+        s->offset_x[i] = ox[i];
+        s->offset_y[i] = oy[i];
+    }
+}
+
+void nbb_spec_vicsek(nbb_spec* s) {
+    std::memset(s, 0, sizeof(*s));
+    std::strcpy(s->name, "vicsek");
+    s->k = 5;
+    s->s = 3;
+    const int ox[] = {1, 1, 1, 0, 2}, oy[] = {1, 0, 2, 1, 1};
+    for (int i = 0; i < 5; ++i) {
+        s->offset_x[i] = ox[i];
+        s->offset_y[i] = oy[i];
+    }
+}
+
+void nbb_spec_carpet(nbb_spec* s) {
+    std::memset(s, 0, sizeof(*s));
+    std::strcpy(s->name, "carpet");
+    s->k = 8;
+    s->s = 3;
+    const int ox[] = {0, 1, 2, 0, 2, 0, 1, 2}, oy[] = {0, 0, 0, 1, 1, 2, 2, 2};
+    for (int i = 0; i < 8; ++i) {
+        s->offset_x[i] = ox[i];
+        s->offset_y[i] = oy[i];
+    }
+}
+
+void nbb_config_init(nbb_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    nbb_spec_sierpinski(&c->spec);
+    c->r = 0;
+    c->rho = 1;
+    c->mode = NBB_MODE_LAMBDA;
+    c->strategy = NBB_STRATEGY_SUBBOX;
+    c->backend = NBB_BACKEND_DIRECT;
+    c->workers = 1;
+    c->timing = 0;
+    c->cell_width = 8;
+    c->kernel = NBB_KERNEL_AUTO;
+    c->device = 0;
+    c->max_cells = (uint64_t)1 << 24;
+}
+
+int nbb_gpu_device_count(int32_t* count) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    *count = c;
+    return NBB_OK;
+}
+
+int nbb_gpu_validate(const nbb_config* cfg) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_TRY(nbbhost::validate(*cfg));
+    return NBB_OK;
+}
+
+int nbb_gpu_launch_block_count(const nbb_config* cfg, uint64_t* blocks) {
+    NBB_TRY(nbbhost::validate(*cfg));
+    nbbhost::Plan p;
+    NBB_TRY(nbbhost::make_plan(*cfg, &p));
+    *blocks = p.blocks();
+    return NBB_OK;
+}
+
+int nbb_gpu_plan_report(const nbb_config* cfg, nbb_report* report) {
+    NBB_TRY(nbbhost::plan_report(*cfg, report));
+    return NBB_OK;
+}
+
+int nbb_gpu_work_quotient(const nbb_report* bb, const nbb_report* lam, int32_t weighted, double* q) {
+    NBB_TRY(nbbhost::work_quotient(*bb, *lam, weighted != 0, q));
+    return NBB_OK;
+}
+
+const char* nbb_gpu_csv_header(void) { return nbbhost::csv_header(); }
+
+int nbb_gpu_report_csv_row(const nbb_report* report, char* buf, size_t len) {
+    const std::string row = nbbhost::csv_row(*report);
+    if (row.size() + 1 > len) return fail(NBB_ERR_INVALID_ARGUMENT, "csv buffer too small");
+    std::memcpy(buf, row.c_str(), row.size() + 1);
+    return NBB_OK;
+}
+
+int nbb_gpu_random_member_grid(const nbb_spec* spec, int32_t r, uint64_t seed, uint64_t modulus,
+                               uint64_t max_cells, int64_t* out_grid) {
+    NBB_TRY(nbbhost::random_member_grid(*spec, r, seed, modulus, max_cells, out_grid));
+    return NBB_OK;
+}
+
+int nbb_gpu_random_member_values(const nbb_spec* spec, int32_t r, uint64_t seed, uint64_t modulus,
+                                 int64_t* out_values) {
+    NBB_TRY(nbbhost::random_member_values(*spec, r, seed, modulus, out_values));
+    return NBB_OK;
+}
+
+// ---- device-resident workloads ---------------------------------------------------------
+int nbb_gpu_single_write_dev(const nbb_config* cfg, void* d_grid, void* stream, nbb_report* report) {
+    Launch L;
+    NBB_CHECK(prepare(cfg, OP_SW, &L, cfg && cfg->mode == NBB_MODE_BB));
+    L.stream = (cudaStream_t)stream;
+    Timer t(cfg->timing != 0, L.stream);
+    NBB_CHECK(launch_op(L, OP_SW, nullptr, d_grid, nullptr, 0, 0));
+    fill_report(cfg, report, t.stop_micros());
+    return NBB_OK;
+}
+
+int nbb_gpu_reduction_dev(const nbb_config* cfg, const void* d_grid, void* d_value, void* stream,
+                          nbb_report* report) {
+    Launch L;
+    NBB_CHECK(prepare(cfg, OP_RD, &L, cfg && cfg->mode == NBB_MODE_BB));
+    L.stream = (cudaStream_t)stream;
+    Timer t(cfg->timing != 0, L.stream);
+    NBB_CHECK(launch_op(L, OP_RD, d_grid, nullptr, (unsigned long long*)d_value, 0, 0));
+    fill_report(cfg, report, t.stop_micros());
+    return NBB_OK;
+}
+
+int nbb_gpu_ca_step_dev(const nbb_config* cfg, const void* d_src, void* d_dst, uint16_t birth,
+                        uint16_t survive, void* stream, nbb_report* report) {
+    Launch L;
+    NBB_CHECK(prepare(cfg, OP_CA, &L, true));
+    L.stream = (cudaStream_t)stream;
+    Timer t(cfg->timing != 0, L.stream);
+    NBB_CHECK(launch_op(L, OP_CA, d_src, d_dst, nullptr, birth, survive));
+    fill_report(cfg, report, t.stop_micros());
+    return NBB_OK;
+}
+
+int nbb_gpu_sanitize_dev(const nbb_config* cfg, void* d_grid, void* stream) {
+    Launch L;
+    NBB_CHECK(prepare(cfg, OP_CA, &L, false));
+    return sanitize(L, d_grid, cfg->cell_width, (cudaStream_t)stream);
+}
+
+int nbb_gpu_pack_alive_dev(const nbb_config* cfg, const void* d64, void* d8, void* stream) {
+    Launch L;
+    NBB_CHECK(prepare(cfg, OP_CA, &L, false));
+    pack_alive_kernel<<<L.ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>(
+        (const long long*)d64, (unsigned char*)d8, L.plan.n);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+int nbb_gpu_unpack_alive_dev(const nbb_config* cfg, const void* d8, void* d64, void* stream) {
+    Launch L;
+    NBB_CHECK(prepare(cfg, OP_CA, &L, false));
+    unpack_alive_kernel<<<L.ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>(
+        (const unsigned char*)d8, (long long*)d64, L.plan.n);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+int nbb_gpu_scatter_members_dev(const nbb_config* cfg, const void* d_values, void* d_grid,
+                                void* stream) {
+    Launch L;
+    NBB_CHECK(prepare(cfg, OP_CA, &L, false));
+    scatter_members_kernel<<<L.ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>(
+        (const long long*)d_values, (long long*)d_grid, L.plan.n);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+int nbb_gpu_lambda_coords_dev(const nbb_config* cfg, int32_t level, void* d_xy, int32_t coord_bytes,
+                              void* stream) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_TRY(nbbhost::require_gasket(cfg->spec));
+    if (level < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "lambda: negative level");
+    if (level > 17) return fail(NBB_ERR_RESOURCE, "lambda map kernel supports levels <= 17");
+    if (coord_bytes != 4 && coord_bytes != 8)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "coord_bytes must be 4 or 8");
+    const bool tc = cfg->backend == NBB_BACKEND_MMA1 || cfg->backend == NBB_BACKEND_MMA2;
+    if (tc && level > 16)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "variant 1 encodes at most 16 levels, r_b = " +
+                                                  std::to_string(level));
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    int64_t w, h;
+    NBB_TRY(nbbhost::orthotope_dims(cfg->spec, level, &w, &h));
+    const uint64_t total = (uint64_t)w * (uint64_t)h;
+    FastDiv f;
+    f.d = (uint32_t)w;
+    nbbhost::fastdiv_magic(f.d, &f.m, &f.s);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int blocks = ctx->sms * 8;
+    if (tc) {
+        if (coord_bytes == 4)
+            lambda_map_tc_kernel<int32_t><<<blocks, 256, 0, s>>>((int32_t*)d_xy, total, (uint32_t)w, f, level);
+        else
+            lambda_map_tc_kernel<long long><<<blocks, 256, 0, s>>>((long long*)d_xy, total, (uint32_t)w, f, level);
+    } else {
+        if (coord_bytes == 4)
+            lambda_map_kernel<int32_t><<<blocks, 256, 0, s>>>((int32_t*)d_xy, total, (uint32_t)w, f);
+        else
+            lambda_map_kernel<long long><<<blocks, 256, 0, s>>>((long long*)d_xy, total, (uint32_t)w, f);
+    }
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+// ---- workloads on host buffers (drop-in for run_single_write / run_reduction / run_ca) ----
+int nbb_gpu_single_write(const nbb_config* cfg, int64_t* out_grid, nbb_report* report) {
+    if (cfg && cfg->r < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "checked_pow: negative exponent");
+    Launch L;
+    NBB_CHECK(prepare(cfg, OP_SW, &L, cfg && cfg->mode == NBB_MODE_BB));
+    L.stream = L.ctx->stream;
+    nbb_config c8 = *cfg;
+    c8.cell_width = 8;  // the result Grid is int64
+    L.cfg = &c8;
+    void* d;
+    NBB_CHECK(device_buffer(*L.ctx, 0, grid_bytes(L, 8), &d));
+    NBB_CUDA(cudaMemsetAsync(d, 0, grid_bytes(L, 8), L.stream));
+    Timer t(cfg->timing != 0, L.stream);
+    NBB_CHECK(launch_op(L, OP_SW, nullptr, d, nullptr, 0, 0));
+    const uint64_t us = t.stop_micros();
+    NBB_CUDA(cudaMemcpyAsync(out_grid, d, grid_bytes(L, 8), cudaMemcpyDeviceToHost, L.stream));
+    NBB_CUDA(cudaStreamSynchronize(L.stream));
+    fill_report(cfg, report, us);
+    return NBB_OK;
+}
+
+int nbb_gpu_reduction(const nbb_config* cfg, const int64_t* grid, int32_t grid_level, int64_t* value,
+                      nbb_report* report) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_TRY(nbbhost::validate(*cfg));
+    if (grid_level != cfg->r)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "reduction: grid level " + std::to_string(grid_level) +
+                                                  " does not match the configured r = " +
+                                                  std::to_string(cfg->r));
+    Launch L;
+    NBB_CHECK(prepare(cfg, OP_RD, &L, cfg->mode == NBB_MODE_BB));
+    L.stream = L.ctx->stream;
+    void* d;
+    NBB_CHECK(device_buffer(*L.ctx, 0, grid_bytes(L, 8), &d));
+    NBB_CUDA(cudaMemcpyAsync(d, grid, grid_bytes(L, 8), cudaMemcpyHostToDevice, L.stream));
+    unsigned long long* d_sum = L.ctx->partials + 4096;
+    Timer t(cfg->timing != 0, L.stream);
+    NBB_CHECK(launch_op(L, OP_RD, d, nullptr, d_sum, 0, 0));
+    const uint64_t us = t.stop_micros();
+    unsigned long long v = 0;
+    NBB_CUDA(cudaMemcpyAsync(&v, d_sum, sizeof(v), cudaMemcpyDeviceToHost, L.stream));
+    NBB_CUDA(cudaStreamSynchronize(L.stream));
+    *value = (int64_t)v;
+    fill_report(cfg, report, us);
+    return NBB_OK;
+}
+
+int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_level, int32_t steps,
+               uint16_t birth, uint16_t survive, int64_t* out_grid, nbb_report* per_step) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_TRY(nbbhost::validate(*cfg));
+    if (initial_level != cfg->r)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "ca: grid level does not match the configured r");
+    if (steps < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "ca: negative step count");
+    Launch L;
+    NBB_CHECK(prepare(cfg, OP_CA, &L, true));
+    L.stream = L.ctx->stream;
+    const size_t b64 = grid_bytes(L, 8);
+    if (steps == 0) {  // the input comes back unchanged (App. B.4)
+        if (out_grid != initial) std::memmove(out_grid, initial, b64);
+        return NBB_OK;
+    }
+    const int cw = cfg->cell_width;
+    void *d64, *da, *db;
+    NBB_CHECK(device_buffer(*L.ctx, 0, b64, &d64));
+    NBB_CUDA(cudaMemcpyAsync(d64, initial, b64, cudaMemcpyHostToDevice, L.stream));
+    if (cw == 8) {
+        da = d64;
+        NBB_CHECK(device_buffer(*L.ctx, 1, b64, &db));
+        NBB_CHECK(sanitize(L, da, 8, L.stream));
+        NBB_CUDA(cudaMemsetAsync(db, 0, b64, L.stream));
+    } else {
+        const size_t b8 = grid_bytes(L, 1);
+        NBB_CHECK(device_buffer(*L.ctx, 1, b8, &da));
+        NBB_CHECK(device_buffer(*L.ctx, 2, b8, &db));
+        pack_alive_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)d64,
+                                                                (unsigned char*)da, L.plan.n);
+        NBB_CUDA(cudaGetLastError());
+        NBB_CUDA(cudaMemsetAsync(db, 0, b8, L.stream));
+    }
+    for (int s = 0; s < steps; ++s) {
+        Timer t(cfg->timing != 0, L.stream);
+        NBB_CHECK(launch_op(L, OP_CA, da, db, nullptr, birth, survive));
+        const uint64_t us = t.stop_micros();
+        if (per_step) fill_report(cfg, &per_step[s], us);
+        std::swap(da, db);
+    }
+    if (cw == 1) {
+        unpack_alive_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const unsigned char*)da,
+                                                                  (long long*)d64, L.plan.n);
+        NBB_CUDA(cudaGetLastError());
+        da = d64;
+    }
+    NBB_CUDA(cudaMemcpyAsync(out_grid, da, b64, cudaMemcpyDeviceToHost, L.stream));
+    NBB_CUDA(cudaStreamSynchronize(L.stream));
+    return NBB_OK;
+}
+
+int nbb_gpu_lambda_coords(const nbb_config* cfg, int32_t level, int64_t* xy) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    int64_t w, h;
+    NBB_TRY(nbbhost::orthotope_dims(cfg->spec, level < 0 ? 0 : level, &w, &h));
+    const size_t bytes = (size_t)w * (size_t)h * 16;
+    void* d;
+    NBB_CHECK(device_buffer(*ctx, 0, bytes, &d));
+    NBB_CHECK(nbb_gpu_lambda_coords_dev(cfg, level, d, 8, ctx->stream));
+    NBB_CUDA(cudaMemcpyAsync(xy, d, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    NBB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return NBB_OK;
+}
+
+int nbb_gpu_release(void) {
+    std::lock_guard<std::mutex> lock(g_mutex);
+    for (size_t d = 0; d < g_ctx.size(); ++d) {
+        DeviceCtx& c = g_ctx[d];
+        if (!c.ready) continue;
+        cudaSetDevice((int)d);
+        for (int i = 0; i < 3; ++i) {
+            if (c.bufs[i]) cudaFree(c.bufs[i]);
+            c.bufs[i] = nullptr;
+            c.buf_bytes[i] = 0;
+        }
+    }
+    return NBB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,389 @@
+// nbb_host.cpp — host-side logic of the engine; see nbb_host.hpp.
+#include "nbb_host.hpp"
+
+#include <cstring>
+#include <limits>
+#include <random>
+#include <sstream>
+#include <vector>
+
+namespace nbbhost {
+
+bool is_gasket(const nbb_spec& s) {
+    return s.k == 3 && s.s == 2 && s.offset_x[0] == 0 && s.offset_y[0] == 0 &&
+           s.offset_x[1] == 0 && s.offset_y[1] == 1 && s.offset_x[2] == 1 && s.offset_y[2] == 1;
+}
+
+Error require_gasket(const nbb_spec& s) {
+    if (!is_gasket(s)) {
+        return err(NBB_ERR_INVALID_ARGUMENT,
+                   std::string("fractal '") + s.name +
+                       "': the GPU path runs the sierpinski gasket only (k=3, s=2, offsets "
+                       "(0,0),(0,1),(1,1)); there is no CPU fallback");
+    }
+    return {};
+}
+
+Error checked_pow(uint64_t base, int exp, uint64_t* out) {
+    if (exp < 0) return err(NBB_ERR_INVALID_ARGUMENT, "checked_pow: negative exponent");
+    uint64_t r = 1;
+    for (int i = 0; i < exp; ++i) {
+        if (base != 0 && r > std::numeric_limits<uint64_t>::max() / base) {
+            return err(NBB_ERR_OVERFLOW, "checked_pow: " + std::to_string(base) + "^" +
+                                             std::to_string(exp) + " overflows 64 bits");
+        }
+        r *= base;
+    }
+    *out = r;
+    return {};
+}
+
+Error level_for_size(int64_t n, int s, int* level) {
+    if (s < 2) return err(NBB_ERR_INVALID_ARGUMENT, "level_for_size: scale factor must be >= 2");
+    if (n < 1) return err(NBB_ERR_INVALID_ARGUMENT, "level_for_size: side length must be >= 1");
+    int l = 0;
+    int64_t v = n;
+    while (v > 1) {
+        if (v % s != 0) {
+            return err(NBB_ERR_INVALID_ARGUMENT, "level_for_size: " + std::to_string(n) +
+                                                     " is not a power of " + std::to_string(s));
+        }
+        v /= s;
+        ++l;
+    }
+    *level = l;
+    return {};
+}
+
+Error side_length(const nbb_spec& s, int level, int64_t* n) {
+    uint64_t v;
+    Error e = checked_pow((uint64_t)s.s, level, &v);
+    if (!e.ok()) return e;
+    if (v > (uint64_t)std::numeric_limits<int64_t>::max())
+        return err(NBB_ERR_OVERFLOW, "side_length overflows int64");
+    *n = (int64_t)v;
+    return {};
+}
+
+Error orthotope_dims(const nbb_spec& s, int level, int64_t* w, int64_t* h) {
+    if (level < 0) return err(NBB_ERR_INVALID_ARGUMENT, "orthotope_dims: negative level");
+    uint64_t a, b;
+    Error e = checked_pow((uint64_t)s.k, (level + 1) / 2, &a);
+    if (!e.ok()) return e;
+    e = checked_pow((uint64_t)s.k, level / 2, &b);
+    if (!e.ok()) return e;
+    *w = (int64_t)a;
+    *h = (int64_t)b;
+    return {};
+}
+
+Error validate(const nbb_config& c) {
+    const int rho = c.rho;
+    if (!(rho == 1 || rho == 2 || rho == 4 || rho == 8 || rho == 16 || rho == 32))
+        return err(NBB_ERR_INVALID_ARGUMENT,
+                   "rho " + std::to_string(rho) + " is not one of 1, 2, 4, 8, 16, 32");
+    if (c.r < 0) return err(NBB_ERR_INVALID_ARGUMENT, "negative scale level");
+    if (c.workers < 1) return err(NBB_ERR_INVALID_ARGUMENT, "workers must be >= 1");
+    int64_t n;
+    Error e = side_length(c.spec, c.r, &n);
+    if (!e.ok()) return e;
+    if (n % rho != 0)
+        return err(NBB_ERR_INVALID_ARGUMENT,
+                   "rho " + std::to_string(rho) + " does not divide n = " + std::to_string(n));
+    if (c.cell_width != 8 && c.cell_width != 1)
+        return err(NBB_ERR_INVALID_ARGUMENT,
+                   "cell_width " + std::to_string(c.cell_width) + " is not 8 (int64) or 1 (uint8)");
+    if (c.mode == NBB_MODE_BB) {
+        if (c.backend != NBB_BACKEND_DIRECT)
+            return err(NBB_ERR_INVALID_ARGUMENT, "lambda backends apply to lambda mode only");
+        return {};
+    }
+    int r_t;
+    e = level_for_size(rho, c.spec.s, &r_t);
+    if (!e.ok()) return e;
+    if (r_t > c.r)
+        return err(NBB_ERR_INVALID_ARGUMENT, "block geometry: rho " + std::to_string(rho) +
+                                                 " exceeds the embedding side " + std::to_string(n));
+    const int r_b = c.r - r_t;
+    switch (c.backend) {
+        case NBB_BACKEND_DIRECT:
+            break;
+        case NBB_BACKEND_MMA1:
+            if (r_b > 16)
+                return err(NBB_ERR_INVALID_ARGUMENT,
+                           "variant 1 encodes at most 16 levels, r_b = " + std::to_string(r_b));
+            break;
+        case NBB_BACKEND_MMA2: {
+            if (rho < 2)
+                return err(NBB_ERR_INVALID_ARGUMENT, "variant 2 needs sub-blocks of edge rho/2 >= 1");
+            int sub_rt;
+            if (!level_for_size(rho / 2, c.spec.s, &sub_rt).ok())
+                return err(NBB_ERR_INVALID_ARGUMENT,
+                           "variant 2 sub-block edge " + std::to_string(rho / 2) +
+                               " is not a power of s = " + std::to_string(c.spec.s));
+            if (c.r - sub_rt > 16)
+                return err(NBB_ERR_INVALID_ARGUMENT, "variant 2 encodes at most 16 levels");
+            break;
+        }
+        case NBB_BACKEND_MMA3:
+            if (rho != 16)
+                return err(NBB_ERR_INVALID_ARGUMENT,
+                           "variant 3 runs at rho = 16 only, got " + std::to_string(rho));
+            if (c.strategy != NBB_STRATEGY_SUBBOX)
+                return err(NBB_ERR_INVALID_ARGUMENT,
+                           "variant 3 emits sub-box thread coordinates; use the subbox strategy");
+            if (r_b > 16) return err(NBB_ERR_INVALID_ARGUMENT, "variant 3 encodes at most 16 levels");
+            break;
+        default:
+            return err(NBB_ERR_INVALID_ARGUMENT, "unknown backend " + std::to_string(c.backend));
+    }
+    if (c.strategy < NBB_STRATEGY_UNROLL || c.strategy > NBB_STRATEGY_SUBBOX)
+        return err(NBB_ERR_INVALID_ARGUMENT, "unknown strategy " + std::to_string(c.strategy));
+    return {};
+}
+
+Error make_plan(const nbb_config& c, Plan* p) {
+    Plan plan;
+    Error e = side_length(c.spec, c.r, &plan.n);
+    if (!e.ok()) return e;
+    if (c.mode == NBB_MODE_BB) {
+        plan.gw = plan.gh = plan.n / c.rho;
+        plan.edge = c.rho;
+        *p = plan;
+        return {};
+    }
+    int r_t;
+    e = level_for_size(c.rho, c.spec.s, &r_t);
+    if (!e.ok()) return e;
+    if (c.backend == NBB_BACKEND_MMA2) {
+        int sub_rt;
+        e = level_for_size(c.rho / 2, c.spec.s, &sub_rt);
+        if (!e.ok()) return e;
+        const int r_sb = c.r - sub_rt;
+        int64_t w, h;
+        e = orthotope_dims(c.spec, r_sb, &w, &h);
+        if (!e.ok()) return e;
+        plan.gw = (w + 1) / 2 * 2;
+        plan.gh = (h + 1) / 2 * 2;
+        plan.sub_w = w;
+        plan.sub_h = h;
+        plan.edge = c.rho / 2;
+        plan.map_level = r_sb;
+        plan.local_level = sub_rt;
+    } else {
+        int64_t w, h;
+        e = orthotope_dims(c.spec, c.r - r_t, &w, &h);
+        if (!e.ok()) return e;
+        plan.gw = w;
+        plan.gh = h;
+        plan.edge = c.rho;
+        plan.map_level = c.r - r_t;
+        plan.local_level = r_t;
+    }
+    int64_t lw, lh;
+    e = orthotope_dims(c.spec, plan.local_level, &lw, &lh);
+    if (!e.ok()) return e;
+    plan.local_w = lw;
+    e = checked_pow((uint64_t)c.spec.k, plan.local_level, &plan.local_members);
+    if (!e.ok()) return e;
+    *p = plan;
+    return {};
+}
+
+Error plan_report(const nbb_config& c, nbb_report* r) {
+    Error e = validate(c);
+    if (!e.ok()) return e;
+    Plan p;
+    e = make_plan(c, &p);
+    if (!e.ok()) return e;
+    std::memset(r, 0, sizeof(*r));
+    std::strncpy(r->spec_name, c.spec.name, sizeof(r->spec_name) - 1);
+    r->r = c.r;
+    r->rho = c.rho;
+    r->mode = c.mode;
+    r->strategy = c.strategy;
+    r->backend = c.backend;
+    uint64_t members;
+    e = checked_pow((uint64_t)c.spec.k, c.r, &members);
+    if (!e.ok()) return e;
+    const uint64_t blocks = p.blocks();
+    const uint64_t edge2 = (uint64_t)p.edge * (uint64_t)p.edge;
+    r->blocks_launched = blocks;
+    r->threads_launched = blocks * edge2;
+    r->threads_active = members;
+    r->threads_wasted = r->threads_launched - members;
+    if (c.mode == NBB_MODE_BB) {
+        r->map_ops = r->threads_launched;  // one membership predicate per thread
+        r->map_levels = 0;
+        return {};
+    }
+    const uint64_t inrange =
+        c.backend == NBB_BACKEND_MMA2 ? (uint64_t)p.sub_w * (uint64_t)p.sub_h : blocks;
+    uint64_t ops = inrange * (uint64_t)p.map_level;
+    switch (c.strategy) {
+        case NBB_STRATEGY_SUBBOX: ops += inrange * edge2; break;
+        case NBB_STRATEGY_UNROLL: ops += members * (uint64_t)p.local_level; break;
+        case NBB_STRATEGY_LUT: ops += p.local_members * (uint64_t)p.local_level; break;
+    }
+    r->map_ops = ops;
+    r->map_levels = p.map_level;
+    return {};
+}
+
+Error member_mask_budget(const nbb_spec& s, int level, uint64_t max_cells) {
+    int64_t n;
+    Error e = side_length(s, level, &n);
+    if (!e.ok()) return e;
+    const uint64_t area = (uint64_t)n * (uint64_t)n;
+    if (area > max_cells)
+        return err(NBB_ERR_RESOURCE, "MemberMask: embedding of " + std::to_string(area) +
+                                         " cells exceeds the budget of " + std::to_string(max_cells));
+    return {};
+}
+
+static const char* mode_name(int m) { return m == NBB_MODE_BB ? "bb" : "lambda"; }
+static const char* strategy_name(int s) {
+    return s == NBB_STRATEGY_UNROLL ? "unroll" : s == NBB_STRATEGY_LUT ? "lut" : "subbox";
+}
+static const char* backend_name(int b) {
+    return b == NBB_BACKEND_MMA1 ? "mma1" : b == NBB_BACKEND_MMA2 ? "mma2" : b == NBB_BACKEND_MMA3 ? "mma3" : "direct";
+}
+
+std::string csv_row(const nbb_report& r) {
+    std::ostringstream out;
+    out << r.spec_name << ',' << r.r << ',' << r.rho << ',' << mode_name(r.mode) << ','
+        << strategy_name(r.strategy) << ',' << backend_name(r.backend) << ',' << r.blocks_launched
+        << ',' << r.threads_launched << ',' << r.threads_active << ',' << r.threads_wasted << ','
+        << r.map_ops << ',' << r.micros;
+    return out.str();
+}
+
+const char* csv_header() {
+    return "# spec,r,rho,mode,strategy,backend,blocks,threads,active,wasted,map_ops,micros";
+}
+
+Error work_quotient(const nbb_report& bb, const nbb_report& lam, bool weighted, double* q) {
+    if (bb.mode != NBB_MODE_BB || lam.mode != NBB_MODE_LAMBDA)
+        return err(NBB_ERR_INVALID_ARGUMENT, "work_quotient takes one bb report and one lambda report");
+    if (std::strncmp(bb.spec_name, lam.spec_name, sizeof(bb.spec_name)) != 0 || bb.r != lam.r ||
+        bb.rho != lam.rho)
+        return err(NBB_ERR_INVALID_ARGUMENT, "work_quotient: the reports describe different launches");
+    double denom = (double)lam.threads_launched;
+    if (weighted) denom *= (double)(lam.map_levels > 1 ? lam.map_levels : 1);
+    *q = (double)bb.threads_launched / denom;
+    return {};
+}
+
+static bool member_generic(const nbb_spec& s, int level, int64_t x, int64_t y, int64_t n) {
+    int64_t scale = n / s.s;
+    for (int mu = level; mu >= 1; --mu) {
+        const int cx = (int)(x / scale), cy = (int)(y / scale);
+        bool hit = false;
+        for (int i = 0; i < s.k; ++i) hit |= (s.offset_x[i] == cx && s.offset_y[i] == cy);
+        if (!hit) return false;
+        x -= cx * scale;
+        y -= cy * scale;
+        scale /= s.s;
+    }
+    return true;
+}
+
+Error random_member_values(const nbb_spec& s, int r, uint64_t seed, uint64_t modulus, int64_t* out) {
+    if (modulus == 0) return err(NBB_ERR_INVALID_ARGUMENT, "random_member_grid: modulus must be positive");
+    Error e = require_gasket(s);
+    if (!e.ok()) return e;
+    int64_t n;
+    e = side_length(s, r, &n);
+    if (!e.ok()) return e;
+    std::mt19937_64 rng(seed);
+    uint64_t k = 0;
+    for (int64_t y = 0; y < n; ++y) {
+        int64_t x = 0;
+        do {
+            out[k++] = (int64_t)(rng() % modulus);
+            x = (x - y) & y;
+        } while (x != 0);
+    }
+    return {};
+}
+
+Error random_member_grid(const nbb_spec& s, int r, uint64_t seed, uint64_t modulus,
+                         uint64_t max_cells, int64_t* grid) {
+    if (modulus == 0) return err(NBB_ERR_INVALID_ARGUMENT, "random_member_grid: modulus must be positive");
+    int64_t n;
+    Error e = side_length(s, r, &n);
+    if (!e.ok()) return e;
+    e = member_mask_budget(s, r, max_cells);
+    if (!e.ok()) return e;
+    std::memset(grid, 0, (size_t)n * (size_t)n * sizeof(int64_t));
+    std::mt19937_64 rng(seed);
+    if (is_gasket(s)) {
+        for (int64_t y = 0; y < n; ++y) {
+            int64_t x = 0;
+            do {
+                grid[y * n + x] = (int64_t)(rng() % modulus);
+                x = (x - y) & y;
+            } while (x != 0);
+        }
+        return {};
+    }
+    for (int64_t y = 0; y < n; ++y)
+        for (int64_t x = 0; x < n; ++x)
+            if (member_generic(s, r, x, y, n)) grid[y * n + x] = (int64_t)(rng() % modulus);
+    return {};
+}
+
+void local_cell_table(const nbb_spec& s, int edge, int16_t* out) {
+    int r_t = 0;
+    level_for_size(edge, s.s, &r_t);
+    uint64_t members = 1;
+    checked_pow((uint64_t)s.k, r_t, &members);
+    int64_t w, h;
+    orthotope_dims(s, r_t, &w, &h);
+    for (int64_t ty = 0; ty < edge; ++ty) {
+        for (int64_t tx = 0; tx < edge; ++tx) {
+            const uint64_t rank = (uint64_t)ty * (uint64_t)edge + (uint64_t)tx;
+            int16_t* e = out + 2 * (ty * edge + tx);
+            if (rank >= members) {
+                e[0] = e[1] = -1;
+                continue;
+            }
+            // λ at the local level (block_map.cpp:25-37, 77-111)
+            int64_t dx = (int64_t)(rank % (uint64_t)w), dy = (int64_t)(rank / (uint64_t)w);
+            int64_t px = 0, py = 0, scale = 1;
+            for (int mu = 1; mu <= r_t; ++mu) {
+                int beta;
+                if (mu % 2 == 1) {
+                    beta = (int)(dx % s.k);
+                    dx /= s.k;
+                } else {
+                    beta = (int)(dy % s.k);
+                    dy /= s.k;
+                }
+                px += s.offset_x[beta] * scale;
+                py += s.offset_y[beta] * scale;
+                scale *= s.s;
+            }
+            e[0] = (int16_t)px;
+            e[1] = (int16_t)py;
+        }
+    }
+}
+
+void fastdiv_magic(uint32_t d, uint32_t* m, uint32_t* s) {
+    if (d == 0) d = 1;
+    if ((d & (d - 1)) == 0) {
+        uint32_t l = 0;
+        while ((1u << l) < d) ++l;
+        *m = 0;
+        *s = l;
+        return;
+    }
+    uint32_t l = 0;
+    while ((2u << l) <= d) ++l;  // 2^l < d < 2^(l+1)
+    const unsigned __int128 num = (unsigned __int128)1 << (32 + l);
+    *m = (uint32_t)((num + d - 1) / d);
+    *s = l;
+}
+
+}  // namespace nbbhost

@@ -1,0 +1,69 @@
+// nbb_host.hpp — host-side logic of the engine (no CUDA): config validation,
+// launch planning, closed-form work counters, CSV rows, seeded grids.
+// Mirrors the reference's dispatch/fractal/block_map host code paths
+// (dispatch.cpp:50-197, 116-149, 559-572; fractal.cpp:12-45, 165-192) with the
+// same names, argument meaning and error text; errors are reported as
+// (nbb_status, message) instead of C++ exceptions so they cross the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include "nbb_gpu.h"
+
+namespace nbbhost {
+
+struct Error {
+    int code = NBB_OK;
+    std::string msg;
+    bool ok() const { return code == NBB_OK; }
+};
+
+inline Error err(int code, std::string msg) { return Error{code, std::move(msg)}; }
+
+bool is_gasket(const nbb_spec& s);
+Error require_gasket(const nbb_spec& s);
+Error checked_pow(uint64_t base, int exp, uint64_t* out);    // fractal.cpp:12-25
+Error level_for_size(int64_t n, int s, int* level);          // fractal.cpp:27-45
+Error side_length(const nbb_spec& s, int level, int64_t* n); // fractal.cpp:165-171
+Error orthotope_dims(const nbb_spec& s, int level, int64_t* w, int64_t* h); // :181-192
+
+// DispatchConfig::validate (dispatch.cpp:50-114)
+Error validate(const nbb_config& c);
+
+// make_plan (dispatch.cpp:153-197)
+struct Plan {
+    int64_t n = 1;
+    int64_t gw = 1, gh = 1;  // launch grid (blocks or mma2 sub-block slots)
+    int edge = 1;
+    int map_level = 0;
+    int local_level = 0;
+    int64_t local_w = 1;
+    uint64_t local_members = 1;
+    int64_t sub_w = -1, sub_h = -1;  // mma2 in-range bounds
+    uint64_t blocks() const { return (uint64_t)gw * (uint64_t)gh; }
+};
+Error make_plan(const nbb_config& c, Plan* p);
+
+// WorkReport of one launch in closed form
+Error plan_report(const nbb_config& c, nbb_report* r);
+
+// MemberMask budget (fractal.cpp:249-256): n^2 cells must fit max_cells
+Error member_mask_budget(const nbb_spec& s, int level, uint64_t max_cells);
+
+std::string csv_row(const nbb_report& r);                 // dispatch.cpp:120-127
+const char* csv_header();                                 // dispatch.cpp:116-118
+Error work_quotient(const nbb_report& bb, const nbb_report& lam, bool weighted, double* q);
+
+// random_member_grid (dispatch.cpp:133-149) — gasket rows enumerated as submasks.
+Error random_member_values(const nbb_spec& s, int r, uint64_t seed, uint64_t modulus, int64_t* out);
+Error random_member_grid(const nbb_spec& s, int r, uint64_t seed, uint64_t modulus,
+                         uint64_t max_cells, int64_t* grid);
+
+// LocalCellTable (block_map.cpp:197-206): edge*edge (x, y) int16 pairs, -1 = spare
+void local_cell_table(const nbb_spec& s, int edge, int16_t* out);
+
+// precomputed fast division magic (see common.cuh FastDiv), exact for x < 2^31
+void fastdiv_magic(uint32_t d, uint32_t* m, uint32_t* s);
+
+}  // namespace nbbhost

@@ -1,0 +1,282 @@
+// util_kernels.cuh — grid preparation kernels and the λ map-only kernels.
+//
+//  sanitize       : zero every non-member cell (establishes the invariant the CA
+//                   step relies on: non-member cells of both buffers are 0).
+//  pack / unpack  : int64 grid <-> uint8 alive grid (CA only reads cell != 0 and
+//                   writes 0/1, dispatch.cpp:542,548-549, so this is exact).
+//  scatter        : member values in row-major member order -> embedded grid, the
+//                   order random_member_grid fills (dispatch.cpp:141-147).
+//  lambda_map     : K0, λ(ω) of a whole orthotope (block_map.cpp:77-111), scalar
+//                   closed form with a shared-memory digit table, and K0-TC, the
+//                   paper's tensor-core encoding (§6.3, mma.cpp:49-77)
+//                   with ω along M so one m16n8k16 yields 16 coordinate pairs.
+#pragma once
+
+#include "common.cuh"
+#include "percell_kernels.cuh"
+
+namespace nbbgpu {
+
+// ---- sanitize ---------------------------------------------------------------
+template <typename Cell>
+__global__ void sanitize_kernel(Cell* grid, int64_t n, int logn) {
+    constexpr int CPS = 32 / (int)sizeof(Cell);
+    const uint64_t spr = (uint64_t)n / CPS > 0 ? (uint64_t)n / CPS : 1;  // sectors per row
+    const uint64_t total = (uint64_t)n * spr;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t nm1 = (uint32_t)(n - 1);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const uint32_t Y = (uint32_t)(i / spr);
+        const uint32_t X = (uint32_t)(i % spr) * CPS;
+        const uint32_t Yc = nm1 - Y;
+        if (n < CPS) {  // tiny grids: cell by cell
+            for (int64_t x = 0; x < n; ++x)
+                if (!gasket_member(x, Y, n)) grid[(int64_t)Y * n + x] = (Cell)0;
+            continue;
+        }
+        const uint32_t cm = CPS == 32 ? 0xFFFFFFFFu : ((1u << CPS) - 1u);
+        const uint32_t memb = ((X & Yc) == 0u) ? (submask_bits((~Yc) & (CPS - 1)) & cm) : 0u;
+        Cell* p = grid + (int64_t)Y * n + X;
+        if (memb == cm) continue;
+        Sector v;
+        if (memb == 0u) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v.w[k] = 0u;
+        } else {
+            v = ld_sector(p);
+            if (CPS == 4) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (!((memb >> c) & 1u)) v.w[2 * c] = v.w[2 * c + 1] = 0u;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t nib = (memb >> (4 * k)) & 0xFu;
+                    v.w[k] &= (nib * 0x00204081u & 0x01010101u) * 0xFFu;
+                }
+            }
+        }
+        stg_sector(p, v);
+    }
+    (void)logn;
+}
+
+// ---- int64 <-> uint8 --------------------------------------------------------
+// one thread per 32-cell run (one uint8 sector, eight int64 sectors)
+__global__ void pack_alive_kernel(const long long* g64, unsigned char* g8, int64_t n) {
+    const uint64_t runs_per_row = (uint64_t)(n >= 32 ? n / 32 : 1);
+    const uint64_t total = (uint64_t)n * runs_per_row;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t nm1 = (uint32_t)(n - 1);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const uint32_t Y = (uint32_t)(i / runs_per_row);
+        const uint32_t X = (uint32_t)(i % runs_per_row) * 32u;
+        if (n < 32) {
+            for (int64_t x = 0; x < n; ++x) {
+                const int64_t idx = (int64_t)Y * n + x;
+                g8[idx] = (gasket_member(x, Y, n) && g64[idx] != 0) ? 1 : 0;
+            }
+            continue;
+        }
+        const uint32_t Yc = nm1 - Y;
+        const uint32_t memb = ((X & Yc) == 0u) ? submask_bits((~Yc) & 31u) : 0u;
+        uint32_t bits = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t nib = (memb >> (4 * q)) & 0xFu;
+            if (nib) bits |= (alive4_i64(ldg_sector(g64 + (int64_t)Y * n + X + 4 * q)) & nib) << (4 * q);
+        }
+        stg_sector(g8 + (int64_t)Y * n + X, expand32_u8(bits));
+    }
+}
+
+__global__ void unpack_alive_kernel(const unsigned char* g8, long long* g64, int64_t n) {
+    const uint64_t runs_per_row = (uint64_t)(n >= 32 ? n / 32 : 1);
+    const uint64_t total = (uint64_t)n * runs_per_row;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t nm1 = (uint32_t)(n - 1);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const uint32_t Y = (uint32_t)(i / runs_per_row);
+        const uint32_t X = (uint32_t)(i % runs_per_row) * 32u;
+        if (n < 32) {
+            for (int64_t x = 0; x < n; ++x) {
+                const int64_t idx = (int64_t)Y * n + x;
+                g64[idx] = (gasket_member(x, Y, n) && g8[idx] != 0) ? 1 : 0;
+            }
+            continue;
+        }
+        const uint32_t Yc = nm1 - Y;
+        const uint32_t memb = ((X & Yc) == 0u) ? submask_bits((~Yc) & 31u) : 0u;
+        const uint32_t bits = memb ? (alive32_u8(ldg_sector(g8 + (int64_t)Y * n + X)) & memb) : 0u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            stg_sector(g64 + (int64_t)Y * n + X + 4 * q, expand4_i64((bits >> (4 * q)) & 0xFu));
+    }
+}
+
+// ---- member scatter ---------------------------------------------------------
+// Row y of the gasket holds 2^popc(y) members, x = pdep(j, y). The number of
+// members in rows < y is sum over set bits b of y of 2^popc(y >> (b+1)) * 3^b.
+__device__ __forceinline__ uint64_t members_before_row(uint32_t y) {
+    uint64_t s = 0, p3 = 1;
+    for (int b = 0; b < 32; ++b) {
+        if ((y >> b) & 1u) s += ((uint64_t)1 << __popc(y >> (b + 1))) * p3;
+        p3 *= 3u;
+        if ((y >> b) == 0u) break;
+    }
+    return s;
+}
+
+__device__ __forceinline__ uint32_t pdep32(uint32_t j, uint32_t m) {
+    uint32_t r = 0;
+    for (uint32_t bit = 1; m != 0u; m &= m - 1u, bit <<= 1)
+        if (j & bit) r |= m & (0u - m);
+    return r;
+}
+
+// one warp per row
+__global__ void scatter_members_kernel(const long long* values, long long* grid, int64_t n) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t y = warp; y < (uint32_t)n; y += nwarps) {
+        const uint64_t start = members_before_row(y);
+        const uint32_t cnt = 1u << __popc(y);
+        for (uint32_t j = (uint32_t)lane; j < cnt; j += 32u)
+            grid[(int64_t)y * n + pdep32(j, y)] = values[start + j];
+    }
+}
+
+// ---- K0: λ map of a whole orthotope (scalar closed form) ----------------------
+// 4 ordinals per thread; int32 pairs -> one 32-byte store, int64 pairs -> two.
+template <typename Coord>
+__global__ void lambda_map_kernel(Coord* xy, uint64_t total, uint32_t gw, FastDiv div_gw) {
+    __shared__ uint32_t s_tab[729];
+    for (int i = threadIdx.x; i < 729; i += blockDim.x) s_tab[i] = c_xy729[i];
+    __syncthreads();
+    const uint64_t quads = (total + 3) / 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += stride) {
+        const uint64_t o0 = q * 4;
+        uint32_t oy = fastdiv((uint32_t)o0, div_gw);
+        uint32_t ox = (uint32_t)o0 - oy * gw;
+        uint32_t Xy, Yy;
+        xy_from_table(s_tab, oy, Xy, Yy);
+        uint32_t lxs[4], lys[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (ox == gw) {  // carry into the next orthotope row
+                ox = 0;
+                ++oy;
+                xy_from_table(s_tab, oy, Xy, Yy);
+            }
+            uint32_t Xx, Yx;
+            xy_from_table(s_tab, ox, Xx, Yx);
+            lambda_from_xy(Xx, Yx, Xy, Yy, lxs[i], lys[i]);
+            ++ox;
+        }
+        if (o0 + 4 <= total) {
+            if (sizeof(Coord) == 4) {
+                Sector v;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    v.w[2 * i] = lxs[i];
+                    v.w[2 * i + 1] = lys[i];
+                }
+                stg_sector(xy + 2 * o0, v);
+            } else {
+                Sector v0, v1;
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    v0.w[4 * i] = lxs[i];
+                    v0.w[4 * i + 1] = 0u;
+                    v0.w[4 * i + 2] = lys[i];
+                    v0.w[4 * i + 3] = 0u;
+                    v1.w[4 * i] = lxs[i + 2];
+                    v1.w[4 * i + 1] = 0u;
+                    v1.w[4 * i + 2] = lys[i + 2];
+                    v1.w[4 * i + 3] = 0u;
+                }
+                stg_sector(xy + 2 * o0, v0);
+                stg_sector(xy + 2 * o0 + 4, v1);
+            }
+        } else {
+            for (uint64_t i = 0; o0 + i < total; ++i) {
+                xy[2 * (o0 + i)] = (Coord)lxs[i];
+                xy[2 * (o0 + i) + 1] = (Coord)lys[i];
+            }
+        }
+    }
+}
+
+// ---- K0-TC: tensor-core λ map --------------------------------------------------
+// D(16 ω x 8) += A_g(16 ω x 16) * B_g(16 x 8) over level groups g of 8 levels:
+// A_g[i][c] = τx(β_{8g+c+1}(ω_i)) for c < 8 and τy(β_{8g+c-7}(ω_i)) for c >= 8;
+// B_g[c][0] = 2^(8g+c) (c < 8), B_g[c][1] = 2^(8g+c-8) (c >= 8). D[i][0..1] = λ(ω_i).
+// All operands are 0/1 or powers of two <= 2^16 (exact in bf16) and the sums are
+// < 2^24 (exact in fp32), so the result is bit-identical to the scalar map.
+template <typename Coord>
+__global__ void lambda_map_tc_kernel(Coord* xy, uint64_t total, uint32_t gw, FastDiv div_gw,
+                                     int levels) {
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const int groups = (levels + 7) / 8;
+    // per-lane divisors 3^(4G+t) for the digits this lane encodes
+    uint32_t pw[3];
+#pragma unroll
+    for (int G = 0; G < 3; ++G) {
+        uint32_t p = 1;
+        for (int i = 0; i < 4 * G + t; ++i) p *= 3u;
+        pw[G] = p;
+    }
+    const uint64_t chunks = (total + 15) / 16;
+    for (uint64_t ch = warp; ch < chunks; ch += nwarps) {
+        const uint64_t base = ch * 16;
+        uint32_t ox[2], oy[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint64_t o = base + g + 8 * h;
+            if (o >= total) o = total - 1;
+            oy[h] = fastdiv((uint32_t)o, div_gw);
+            ox[h] = (uint32_t)o - oy[h] * gw;
+        }
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int G = 0; G < groups; ++G) {
+            const int mu1 = 8 * G + 2 * t + 1, mu2 = mu1 + 1;  // odd level -> ωx digit, even -> ωy
+            uint32_t a[4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t bx = (mu1 <= levels) ? (ox[h] / pw[G]) % 3u : 0u;
+                const uint32_t by = (mu2 <= levels) ? (oy[h] / pw[G]) % 3u : 0u;
+                // cols 2t, 2t+1: τx of levels mu1, mu2; cols 2t+8, 2t+9: τy of levels mu1, mu2
+                a[h] = pack_bf16((float)(bx / 2u), (float)(by / 2u));
+                a[h + 2] = pack_bf16((float)(bx - bx / 2u), (float)(by - by / 2u));
+            }
+            uint32_t b[2];
+            {
+                const int r0 = 2 * t, r1 = 2 * t + 1;  // rows of B held by this lane (k)
+                const float v0 = (g == 0) ? (float)(1u << (8 * G + r0)) : 0.f;
+                const float v1 = (g == 0) ? (float)(1u << (8 * G + r1)) : 0.f;
+                const float w0 = (g == 1) ? (float)(1u << (8 * G + r0)) : 0.f;
+                const float w1 = (g == 1) ? (float)(1u << (8 * G + r1)) : 0.f;
+                b[0] = pack_bf16(v0, v1);  // rows 2t, 2t+1 (τx part), column g
+                b[1] = pack_bf16(w0, w1);  // rows 2t+8, 2t+9 (τy part), column g
+            }
+            mma_bf16_16816(d, a, b, d);
+        }
+        if (t == 0) {  // lanes holding columns 0 and 1
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint64_t o = base + g + 8 * h;
+                if (o < total) {
+                    xy[2 * o] = (Coord)d[2 * h];
+                    xy[2 * o + 1] = (Coord)d[2 * h + 1];
+                }
+            }
+        }
+    }
+}
+
+}  // namespace nbbgpu

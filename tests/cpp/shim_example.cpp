@@ -1,0 +1,40 @@
+// Example reference-style program against the C++ shim (include/nbb_gpu.hpp).
+// Compiled by tests/test_capi.py (CPU: --host-only) and run on the GPU by
+// tests/test_gpu_parity.py::test_cpp_shim_on_gpu.
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+
+#include "nbb_gpu.hpp"
+
+int main(int argc, char** argv) {
+    namespace g = nbb::gpu;
+    const bool host_only = argc > 1 && std::strcmp(argv[1], "--host-only") == 0;
+    g::DispatchConfig cfg;
+    cfg.r = 8;
+    std::printf("%s\n", g::WorkReport::csv_header().c_str());
+    std::printf("%s\n", g::plan_report(cfg).csv_row().c_str());
+    try {
+        g::DispatchConfig bad = cfg;
+        bad.rho = 3;
+        bad.validate();
+        return 1;
+    } catch (const std::invalid_argument& e) {
+        std::printf("invalid_argument: %s\n", e.what());
+    }
+    if (host_only) return 0;
+
+    cfg.r = 10;
+    cfg.rho = 32;
+    const auto sw = g::run_single_write(cfg);
+    const long long sum = std::accumulate(sw.grid.values().begin(), sw.grid.values().end(), 0LL);
+    std::printf("sw sum %lld\n", sum);
+    const auto rd_grid = g::random_member_grid(cfg.spec, 10, 11, 100);
+    std::printf("rd %lld\n", (long long)g::run_reduction(cfg, rd_grid).value);
+    const auto ca_grid = g::random_member_grid(cfg.spec, 10, 11, 2);
+    const auto ca = g::run_ca(cfg, ca_grid, 10);
+    const long long pop = std::accumulate(ca.grid.values().begin(), ca.grid.values().end(), 0LL);
+    std::printf("ca pop %lld gen %llu reports %zu\n", pop, (unsigned long long)ca.grid.generation(),
+                ca.reports.size());
+    return (sum == 59049 && pop == 10398) ? 0 : 2;
+}

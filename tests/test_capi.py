@@ -1,0 +1,178 @@
+"""The product C ABI without a GPU: the library loads, exports every symbol
+include/nbb_gpu.h declares, its host logic (validation, counters, CSV, seeded grids)
+matches the reference's, and compute entry points fail loudly (no CPU fallback)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from _oracle import GASKET, ROOT, fnv1a64
+from paper_2004_13475_b200 import _abi
+from paper_2004_13475_b200 import nbb
+from paper_2004_13475_b200.nbb import (DispatchConfig, FractalSpec, IntraBlockStrategy,
+                                       InvalidArgument, LambdaBackend, MapMode)
+
+HEADER = os.path.join(ROOT, "include", "nbb_gpu.h")
+
+
+def _cfg(**kw):
+    c = DispatchConfig()
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(nbb_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _abi.load()
+    names = declared_symbols()
+    assert len(names) >= 25
+    for name in names:
+        assert hasattr(lib, name), name
+        assert name in _abi.SIGNATURES, f"{name} missing from _abi.SIGNATURES"
+    assert lib.nbb_gpu_abi_version() == 1
+
+
+def test_library_is_sm100a_and_native():
+    """The .so carries sm_100a SASS (cuobjdump) — no PTX-JIT-only or CPU build."""
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _abi.LIB_PATH],
+                         capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in out
+
+
+def test_config_init_defaults():
+    lib = _abi.load()
+    c = _abi.NbbConfig()
+    lib.nbb_config_init(ctypes.byref(c))
+    assert (c.spec.name, c.spec.k, c.spec.s) == (b"sierpinski", 3, 2)
+    assert (c.r, c.rho, c.mode, c.strategy, c.backend, c.workers, c.cell_width) == \
+        (0, 1, _abi.MODE_LAMBDA, _abi.STRATEGY_SUBBOX, _abi.BACKEND_DIRECT, 1, 8)
+    assert c.max_cells == 1 << 24
+
+
+def test_validation_matches_reference(golden):
+    for v in golden["validation"]:
+        spec = FractalSpec.builtin(v.get("spec", "sierpinski"))
+        c = _cfg(spec=spec, r=v["r"], rho=v["rho"], mode=MapMode(v["mode"]),
+                 strategy=IntraBlockStrategy(v["strategy"]), backend=LambdaBackend(v["backend"]),
+                 workers=v["workers"])
+        if v["rc"] == 0:
+            c.validate()
+        else:
+            with pytest.raises(InvalidArgument) as e:
+                c.validate()
+            assert str(e.value) == v["msg"]
+
+
+def test_counters_and_csv_match_reference(golden):
+    for row in golden["csv_rows"]:
+        c = _cfg(r=row["r"], rho=row["rho"], mode=MapMode(row["mode"]),
+                 strategy=IntraBlockStrategy(row["strategy"]), backend=LambdaBackend(row["backend"]))
+        rep = nbb.plan_report(c)
+        assert rep.csv_row() == row["csv"]
+        assert rep.map_levels == row["map_levels"]
+        assert nbb.launch_block_count(c) == rep.blocks_launched
+
+
+def test_csv_frozen_rows():
+    """test_dispatch.cpp:344-362 and test_cli.cpp:151-156."""
+    assert nbb.WorkReport.csv_header() == \
+        "# spec,r,rho,mode,strategy,backend,blocks,threads,active,wasted,map_ops,micros"
+    assert nbb.plan_report(_cfg(r=4, mode=MapMode.BoundingBox)).csv_row() == \
+        "sierpinski,4,1,bb,subbox,direct,256,256,81,175,256,0"
+    assert nbb.plan_report(_cfg(r=4)).csv_row() == "sierpinski,4,1,lambda,subbox,direct,81,81,81,0,405,0"
+    lut = nbb.plan_report(_cfg(r=4, rho=4, strategy=IntraBlockStrategy.SharedLookupTable))
+    assert lut.map_ops == 9 * 2 + 9 * 2 and lut.map_levels == 2
+    assert nbb.plan_report(_cfg(r=8, mode=MapMode.BoundingBox)).csv_row() == \
+        "sierpinski,8,1,bb,subbox,direct,65536,65536,6561,58975,65536,0"
+    assert nbb.plan_report(_cfg(r=8)).csv_row() == \
+        "sierpinski,8,1,lambda,subbox,direct,6561,6561,6561,0,59049,0"
+    v2 = nbb.plan_report(_cfg(r=4, rho=2, backend=LambdaBackend.MmaV2))
+    assert (v2.blocks_launched, v2.threads_launched, v2.threads_active, v2.threads_wasted) == \
+        (100, 100, 81, 19)
+
+
+def test_work_quotient():
+    bb8 = nbb.plan_report(_cfg(r=8, mode=MapMode.BoundingBox))
+    lam8 = nbb.plan_report(_cfg(r=8))
+    assert nbb.work_quotient(bb8, lam8) == pytest.approx(65536 / 6561)
+    assert nbb.work_quotient(bb8, lam8, True) == pytest.approx(65536 / 6561 / 8)
+    with pytest.raises(InvalidArgument):
+        nbb.work_quotient(lam8, bb8)
+    with pytest.raises(InvalidArgument):
+        nbb.work_quotient(bb8, nbb.plan_report(_cfg(r=6)))
+    bb0, lam0 = nbb.plan_report(_cfg(r=0, mode=MapMode.BoundingBox)), nbb.plan_report(_cfg(r=0))
+    assert nbb.work_quotient(bb0, lam0) == 1.0 and nbb.work_quotient(bb0, lam0, True) == 1.0
+
+
+def test_random_member_grid_matches_reference(golden):
+    for r in range(0, 13):
+        w = golden["workloads"][str(r)]
+        g = nbb.random_member_grid(GASKET, r, 1 + r, 100)
+        assert fnv1a64(g.values) == w["rd_grid_fnv"]
+        v = nbb.random_member_values(GASKET, r, 1 + r, 100)
+        n = 1 << r
+        yy, xx = np.mgrid[0:n, 0:n]
+        assert np.array_equal(g.values[(xx & (n - 1 - yy)) == 0], v)
+    with pytest.raises(InvalidArgument):
+        nbb.random_member_grid(GASKET, 3, 1, 0)
+    with pytest.raises(nbb.ResourceError):
+        nbb.random_member_grid(GASKET, 13, 1, 2)  # 2^26 cells > default 2^24 budget
+
+
+def test_string_conversions():
+    for s in ("bb", "lambda"):
+        assert nbb.to_string(nbb.mode_from_string(s)) == s
+    for s in ("unroll", "lut", "subbox"):
+        assert nbb.to_string(nbb.strategy_from_string(s)) == s
+    for s in ("direct", "mma1", "mma2", "mma3"):
+        assert nbb.to_string(nbb.backend_from_string(s)) == s
+    with pytest.raises(InvalidArgument):
+        nbb.strategy_from_string("fu")
+
+
+@pytest.mark.skipif(nbb.device_count() > 0, reason="a GPU is present")
+def test_compute_fails_loudly_without_gpu():
+    """No CPU fallback: every compute entry point reports NBB_ERR_CUDA."""
+    c = _cfg(r=4, rho=4)
+    with pytest.raises(nbb.CudaError):
+        nbb.run_single_write(c)
+    with pytest.raises(nbb.CudaError):
+        nbb.run_reduction(c, nbb.Grid(GASKET, 4))
+    with pytest.raises(nbb.CudaError):
+        nbb.run_ca(c, nbb.Grid(GASKET, 4), 1)
+    with pytest.raises(nbb.CudaError):
+        nbb.lambda_coords(c, 3)
+
+
+def test_invalid_config_rejected_before_device():
+    with pytest.raises(InvalidArgument, match="rho 3 is not one of"):
+        nbb.run_single_write(_cfg(r=4, rho=3))
+    with pytest.raises(InvalidArgument, match="does not match the configured"):
+        nbb.run_reduction(_cfg(r=3), nbb.Grid(GASKET, 2))
+    with pytest.raises(InvalidArgument, match="negative step count"):
+        nbb.run_ca(_cfg(r=2), nbb.Grid(GASKET, 2), -1)
+    with pytest.raises(InvalidArgument, match="sierpinski gasket only"):
+        nbb.run_single_write(_cfg(spec=FractalSpec.vicsek(), r=2))
+
+
+def test_cpp_shim_compiles():
+    """include/nbb_gpu.hpp (the reference-signature C++ shim) builds against the C ABI."""
+    src = os.path.join(ROOT, "tests", "cpp", "shim_example.cpp")
+    out = "/tmp/nbb_shim_example"
+    subprocess.run(["/usr/bin/g++", "-std=c++17", "-Wall", "-Wextra", "-Werror",
+                    f"-I{os.path.join(ROOT, 'include')}", src, "-o", out,
+                    f"-L{os.path.dirname(_abi.LIB_PATH)}", "-lnbbgpu",
+                    f"-Wl,-rpath,{os.path.dirname(_abi.LIB_PATH)}"], check=True)
+    # without a GPU the example must fail loudly (exit 3 = CUDA error via exception)
+    r = subprocess.run([out, "--host-only"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "sierpinski,8,1,lambda,subbox,direct,6561,6561,6561,0,59049,0" in r.stdout
