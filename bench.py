@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""Benchmark of the λ(ω) hot path on B200.
+
+Headline (BASELINE.json metric, config C3): one cellular-automaton step (B3/S23) of
+the Sierpinski gasket embedded at n = 2^16, int64 cells (the reference's Grid),
+launched over the compact λ(ω) orthotope with ρ = 32 — `value` = member-cell
+updates per second (3^16 per step) with the grid resident in HBM. Alongside: the
+same step through the bounding-box (BB) launch (paper-faithful per-cell BB and the
+sector-vectorised BB), the single-write and reduction workloads, the uint8-state
+variant, the HBM roofline of the dominant kernel, the reference CPU path timed on
+this host (`cpu_baseline`), and `e2e` = the same metric through the public C ABI
+call nbb_gpu_ca() with host buffers (H2D of the initial grid and D2H of the result
+inside the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun (one process per GPU): the tile ordinal range is split in
+contiguous chunks (dispatch.cpp:419-427) and CA halo cells cross ranks via NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "gasket cells/s at n=2^16: λ(ω) vs BB speedup, % of B200 HBM roofline"
+
+
+# ---------------------------------------------------------------------------------
+def layout_bytes_per_pass(r: int, cell_bytes: int) -> int:
+    """layout-minimum DRAM bytes of one pass over the member cells of the
+    embedded grid, 32-byte sectors: 32 * 2^g * 3^(r-g), 2^g = 32 / cell_bytes."""
+    g = {8: 2, 1: 5}[cell_bytes]
+    return 32 * (2 ** g) * 3 ** (r - g)
+
+
+def measured_peaks():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        if os.path.exists(p):
+            with open(p) as f:
+                d = json.load(f)
+            return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML samples of SM clock + throttle reasons while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------
+def reference_ca(r: int, rho: int, steps: int, seed: int, workers: int):
+    """The unmodified reference run_ca (oracle/_ref/libnbbref.so) on host cores."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+    from _oracle import ref_lib
+    from paper_2004_13475_b200 import _abi, nbb
+    ref = ref_lib()
+    spec = nbb.FractalSpec.sierpinski()
+    n = 1 << r
+    h = ref.ref_grid_create(ctypes.byref(spec.to_c()), r)
+    if not h:
+        raise MemoryError(ref.ref_last_error().decode())
+    try:
+        data = np.ctypeslib.as_array(ctypes.cast(ref.ref_grid_data(h), ctypes.POINTER(ctypes.c_int64)),
+                                     shape=(n * n,))
+        # input prep (not timed): our bit-identical O(3^r) generator writes the member cells
+        _abi.load().nbb_gpu_random_member_grid(ctypes.byref(spec.to_c()), r, seed, 2, n * n,
+                                              data.ctypes.data_as(ctypes.c_void_p))
+        cfg = nbb.DispatchConfig(r=r, rho=rho, mode=nbb.MapMode.Lambda, workers=workers,
+                                 timing=True, max_cells=n * n)
+        reps = (_abi.NbbReport * steps)()
+        secs = ctypes.c_double()
+        rc = ref.ref_ca_h(ctypes.byref(cfg.to_c()), h, steps, 8, 12, None, reps, ctypes.byref(secs))
+        if rc:
+            raise RuntimeError(ref.ref_last_error().decode())
+        micros = [reps[i].micros for i in range(steps)]
+        return secs.value, micros
+    finally:
+        ref.ref_grid_destroy(h)
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    r, rho = args.r, 32
+    steps = max(1, min(args.steps, args.ref_max_steps))
+    cores = os.cpu_count() or 1
+    secs, micros = reference_ca(r, rho, steps, 17, cores)
+    value = 3 ** r * steps / secs
+    line = {
+        "metric": METRIC, "value": value, "unit": "cells/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": steps, "warmup": 0, "ms_per_step": 1e3 * secs / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic: random_member_grid(gasket, 16, seed=17, modulus=2), B3/S23",
+        "config": config_block(r, rho),
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": cores, "kind": "reference",
+                         "sample": f"reference run_ca(r={r}, rho={rho}, lambda/subbox/direct, "
+                                   f"workers={cores}) for {steps} steps in one call; wall time of "
+                                   f"the call (incl. its MemberMask build and per-step fills); "
+                                   f"launch-only micros per step {micros}"},
+        "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(r, rho):
+    return {"workload": f"C3: gasket n=2^{r} cellular-automaton step (B3/S23), lambda(omega) launch, "
+                        f"rho={rho}, int64 embedded grid (reference Grid layout)",
+            "r": r, "n": 1 << r, "rho": rho, "mode": "lambda", "cells_per_step": 3 ** r,
+            "cell": "int64", "parallelism": "tile-range shards" ,
+            "l2": "no flush: each step touches 1.22 GB (> 126 MB L2)"}
+
+
+# ---------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--r", type=int, default=16)
+    ap.add_argument("--ref-max-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="only run a few λ/BB CA steps (for ncu); prints nothing")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    from paper_2004_13475_b200 import device as dev
+    from paper_2004_13475_b200 import nbb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    r, n = args.r, 1 << args.r
+    stream = torch.cuda.current_stream()
+    s = stream.cuda_stream
+    spec = nbb.FractalSpec.sierpinski()
+    members = 3 ** r
+
+    def cfg(**kw):
+        c = nbb.DispatchConfig(r=r, rho=32, max_cells=n * n, device=local)
+        for k, v in kw.items():
+            setattr(c, k, v)
+        return c
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- inputs: random_member_grid(gasket, r, 17, 2), generated bit-identically --------
+    a = torch.zeros((n, n), dtype=torch.int64, device="cuda")
+    vals = torch.from_numpy(nbb.random_member_values(spec, r, 17, 2)).cuda()
+    dev.scatter_members_dev(cfg(), vals.data_ptr(), a.data_ptr(), s)
+    del vals
+    b = torch.zeros_like(a)
+    torch.cuda.synchronize()
+
+    # shard of the tile range for this rank (weak: every rank owns one contiguous chunk)
+    from paper_2004_13475_b200 import shard
+    plan = shard.ShardPlan(r=r, rho=32, world=world, rank=rank)
+
+    def ca_runner(c, src, dst):
+        bufs = [src, dst]
+        state = {"i": 0}
+
+        def step():
+            i = state["i"]
+            if world > 1:
+                plan.exchange_halo(bufs[i & 1], dist)
+                dev.ca_step_dev(plan.local_config(c), bufs[i & 1].data_ptr(),
+                                bufs[(i + 1) & 1].data_ptr(), nbb.CaRule(), s)
+            else:
+                dev.ca_step_dev(c, bufs[i & 1].data_ptr(), bufs[(i + 1) & 1].data_ptr(),
+                                nbb.CaRule(), s)
+            state["i"] = i + 1
+        return step
+
+    def timed(step, K, W, sampler=None):
+        for _ in range(W):
+            step()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        if sampler:
+            sampler.__enter__()
+        e0.record(stream)
+        for _ in range(K):
+            step()
+        e1.record(stream)
+        e1.synchronize()
+        if sampler:
+            sampler.__exit__()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1)) / K  # ms per step
+
+    if args.profile:
+        for c in (cfg(), cfg(mode=nbb.MapMode.BoundingBox),
+                  cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell)):
+            run = ca_runner(c, a, b)
+            for _ in range(3):
+                run()
+        torch.cuda.synchronize()
+        return
+
+    K, W = args.steps, args.warmup
+    sampler = ClockSampler(local)
+    results = {}
+
+    # ---- headline: λ(ω) CA step, int64, ρ = 32 (tile kernel) -----------------------------
+    ms = timed(ca_runner(cfg(), a, b), K, W, sampler)
+    head_ms = ms
+    value = world * 0 + members * 1e3 / ms  # all ranks together update the 3^r cells per step
+    results["ca_lambda_tile_rho32_i64"] = ms
+
+    # the other CA launch shapes (each on its own timed loop; K shortened for slow BB)
+    variants = {
+        "ca_lambda_tile_rho16_i64": cfg(rho=16),
+        "ca_lambda_tile_rho8_i64": cfg(rho=8),
+        "ca_bb_tile_rho32_i64": cfg(mode=nbb.MapMode.BoundingBox),
+        "ca_bb_tile_rho16_i64": cfg(mode=nbb.MapMode.BoundingBox, rho=16),
+        "ca_bb_percell_rho32_i64": cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell),
+        "ca_bb_percell_rho16_i64": cfg(mode=nbb.MapMode.BoundingBox, rho=16,
+                                       kernel=nbb.KernelFamily.PerCell),
+        "ca_lambda_percell_rho32_i64": cfg(kernel=nbb.KernelFamily.PerCell),
+        "ca_lambda_percell_rho16_i64": cfg(rho=16, kernel=nbb.KernelFamily.PerCell),
+    }
+    if world == 1:
+        for name, c in variants.items():
+            kk = K if "tile" in name else max(5, K // 10)
+            results[name] = timed(ca_runner(c, a, b), kk, W)
+
+    # uint8 alive state (exact: CA only reads != 0 and writes 0/1)
+    if world == 1:
+        a8 = torch.zeros((n, n), dtype=torch.uint8, device="cuda")
+        b8 = torch.zeros_like(a8)
+        dev.pack_alive_dev(cfg(cell_width=1), a.data_ptr(), a8.data_ptr(), s)
+        results["ca_lambda_tile_rho32_u8"] = timed(ca_runner(cfg(cell_width=1), a8, b8), K, W)
+        results["ca_bb_tile_rho32_u8"] = timed(
+            ca_runner(cfg(cell_width=1, mode=nbb.MapMode.BoundingBox), a8, b8), K, W)
+        del a8, b8
+
+        # single write and reduction (C2 / C3-RD) on the same buffers
+        def sw(c):
+            return lambda: dev.single_write_dev(c, b.data_ptr(), s)
+        out = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+        def rd(c):
+            return lambda: dev.reduction_dev(c, a.data_ptr(), out.data_ptr(), s)
+        for name, c in {"sw_lambda_tile_rho32": cfg(), "sw_bb_tile_rho32": cfg(mode=nbb.MapMode.BoundingBox),
+                        "sw_bb_percell_rho32": cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell),
+                        "sw_lambda_percell_rho16": cfg(rho=16, kernel=nbb.KernelFamily.PerCell)}.items():
+            results[name] = timed(sw(c), K if "tile" in name else max(5, K // 10), W)
+        for name, c in {"rd_lambda_tile_rho32": cfg(), "rd_bb_tile_rho32": cfg(mode=nbb.MapMode.BoundingBox),
+                        "rd_bb_percell_rho32": cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell),
+                        "rd_lambda_percell_rho16": cfg(rho=16, kernel=nbb.KernelFamily.PerCell)}.items():
+            results[name] = timed(rd(c), K if "tile" in name else max(5, K // 10), W)
+
+    # ---- roofline of the dominant kernel ----------------------------------------------
+    peak, peak_kind = measured_peaks()
+    alg_bytes = 2 * layout_bytes_per_pass(r, 8)  # read src + write dst, per launch
+    achieved = alg_bytes / (head_ms * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        with open(tf) as f:
+            traffic = json.load(f).get("ca_lambda_tile_rho32_i64")
+
+    # ---- e2e through the public C ABI with pinned host buffers -------------------------
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        del b
+        torch.cuda.empty_cache()
+        hin = torch.empty((n, n), dtype=torch.int64, pin_memory=True)
+        hout = torch.empty((n, n), dtype=torch.int64, pin_memory=True)
+        lib = nbb._lib()
+        lib.nbb_gpu_random_member_grid(ctypes.byref(spec.to_c()), r, 17, 2, n * n,
+                                       ctypes.c_void_p(hin.data_ptr()))
+        del a
+        torch.cuda.empty_cache()
+        c = cfg()
+        cc = c.to_c()
+        ek = K
+        t0 = time.perf_counter()
+        rc = lib.nbb_gpu_ca(ctypes.byref(cc), ctypes.c_void_p(hin.data_ptr()), r, ek, 8, 12,
+                            ctypes.c_void_p(hout.data_ptr()), None)
+        t1 = time.perf_counter()
+        if rc:
+            raise RuntimeError(lib.nbb_gpu_last_error().decode())
+        e2e = {"value": members * ek / (t1 - t0), "unit": "cells/s",
+               "h2d_bytes_per_step": n * n * 8 // ek, "d2h_bytes_per_step": n * n * 8 // ek,
+               "call": f"nbb_gpu_ca(cfg, host_initial, steps={ek}, B3/S23, host_out) on pinned "
+                       f"host buffers; wall time of the call incl. H2D + D2H of the 32 GiB grid",
+               "seconds": t1 - t0}
+        del hin, hout
+        nbb.release()
+
+    # ---- CPU baseline: the reference on this host's cores (bounded sample) ------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            rs, steps_s = 15, 2
+            cores = os.cpu_count() or 1
+            secs, micros = reference_ca(rs, 32, steps_s, 16, cores)
+            cpu = {"value": 3 ** rs * steps_s / secs, "unit": "cells/s", "cores": cores,
+                   "kind": "reference",
+                   "sample": f"reference run_ca(r={rs}, rho=32, lambda, workers={cores}), {steps_s} "
+                             f"steps in one call, wall time incl. MemberMask build; launch-only "
+                             f"micros {micros}"}
+        except Exception as e:  # report, don't die
+            cpu = {"value": None, "unit": "cells/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    if rank != 0:
+        return
+    cells = lambda k: members * 1e3 / results[k] if k in results else None  # noqa: E731
+    best_bb = min((results[k] for k in results if k.startswith("ca_bb") and k.endswith("i64")),
+                  default=None)
+    best_bb_percell = min((results[k] for k in results if k.startswith("ca_bb_percell")), default=None)
+    line = {
+        "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": head_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic: random_member_grid(gasket, 16, seed=17, modulus=2) generated "
+                "bit-identically on device, B3/S23",
+        "config": config_block(r, 32),
+        "gpu_launches": K,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
+                     "kernel": "tile_kernel<int64, rho=32, CA, lambda>"},
+        "clocks": sampler.summary(),
+        "speedup_vs_bb": {
+            "ca_best_bb_over_lambda": (best_bb / head_ms) if best_bb else None,
+            "ca_paper_bb_percell_over_lambda": (best_bb_percell / head_ms) if best_bb_percell else None,
+        },
+        "workloads_ms": results,
+        "workloads_cells_per_s": {k: cells(k) for k in results},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -91,6 +91,11 @@ typedef struct nbb_config {
     int32_t kernel;     /* NBB_KERNEL_*                                        */
     int32_t device;     /* CUDA device ordinal of the first worker              */
     uint64_t max_cells; /* membership-raster budget (reference kEnumerateBudget) */
+    /* Shard: launch only block ordinals [shard_begin, shard_begin + shard_count)
+     * of the plan (0/0 = all). The multi-GPU path gives each rank one contiguous
+     * chunk, as the reference splits ordinals over workers (dispatch.cpp:419-427). */
+    uint64_t shard_begin;
+    uint64_t shard_count;
 } nbb_config;
 
 /* WorkReport (dispatch.hpp:44-61) */
@@ -182,6 +187,13 @@ int nbb_gpu_scatter_members_dev(const nbb_config* cfg, const void* d_values, voi
  * coord_bytes = 4 (int32 pairs) or 8 (int64 pairs). */
 int nbb_gpu_lambda_coords_dev(const nbb_config* cfg, int32_t level, void* d_xy,
                               int32_t coord_bytes, void* stream);
+/* Halo exchange helpers for sharded CA (multi-GPU): gather d_grid[idx[i]] into
+ * d_out[i] and scatter d_vals[i] into d_grid[idx[i]], count cells of
+ * cfg->cell_width bytes; idx are flat cell indices (y*n + x) in device memory. */
+int nbb_gpu_gather_cells_dev(const nbb_config* cfg, const void* d_grid, const int64_t* d_idx,
+                             int64_t count, void* d_out, void* stream);
+int nbb_gpu_scatter_cells_dev(const nbb_config* cfg, void* d_grid, const int64_t* d_idx,
+                              int64_t count, const void* d_vals, void* stream);
 /* Free the device buffers cached by the host-buffer entry points. */
 int nbb_gpu_release(void);
 

@@ -57,6 +57,8 @@ class NbbConfig(Structure):
         ("kernel", c_int32),
         ("device", c_int32),
         ("max_cells", c_uint64),
+        ("shard_begin", c_uint64),
+        ("shard_count", c_uint64),
     ]
 
 
@@ -112,6 +114,8 @@ SIGNATURES = {
     "nbb_gpu_unpack_alive_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p]),
     "nbb_gpu_scatter_members_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p]),
     "nbb_gpu_lambda_coords_dev": (c_int, [CP, c_int32, c_void_p, c_int32, c_void_p]),
+    "nbb_gpu_gather_cells_dev": (c_int, [CP, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "nbb_gpu_scatter_cells_dev": (c_int, [CP, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "nbb_gpu_release": (c_int, []),
 }
 

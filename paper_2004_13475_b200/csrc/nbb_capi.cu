@@ -232,17 +232,30 @@ int dispatch_tile_rho(const Launch& L, const void* src, void* dst, unsigned long
     return fail(NBB_ERR_INVALID_ARGUMENT, "tile kernel needs rho in {8, 16, 32}");
 }
 
+// [lo, hi) block ordinals of this launch: the whole plan or the configured shard
+void shard_range(const Launch& L, uint64_t* lo, uint64_t* hi) {
+    const uint64_t total = L.plan.blocks();
+    *lo = 0;
+    *hi = total;
+    if (L.cfg->shard_count > 0) {
+        *lo = std::min<uint64_t>(L.cfg->shard_begin, total);
+        *hi = std::min<uint64_t>(*lo + L.cfg->shard_count, total);
+    }
+}
+
 template <typename Cell, int OP>
 int launch_tile(const Launch& L, const void* src, void* dst, unsigned long long* sum,
                 uint32_t birth, uint32_t survive) {
-    const uint32_t tiles = (uint32_t)L.plan.blocks();
+    uint64_t lo, hi;
+    shard_range(L, &lo, &hi);
+    const uint32_t tiles = (uint32_t)(hi - lo);
     // workers > 1: contiguous ordinal chunks (dispatch.cpp:419-427), run in order
     const uint32_t workers = (uint32_t)std::max(1, L.cfg->workers);
     const uint32_t chunk = (tiles + workers - 1) / workers;
     for (uint32_t w = 0; w < workers; ++w) {
-        const uint32_t begin = w * chunk;
-        if (begin >= tiles) break;
-        const uint32_t count = std::min(chunk, tiles - begin);
+        const uint32_t begin = (uint32_t)lo + w * chunk;
+        if (w * chunk >= tiles) break;
+        const uint32_t count = std::min(chunk, tiles - w * chunk);
         int rc = L.cfg->mode == NBB_MODE_BB
                      ? dispatch_tile_rho<Cell, OP, true>(L, src, dst, sum, birth, survive, begin, count)
                      : dispatch_tile_rho<Cell, OP, false>(L, src, dst, sum, birth, survive, begin, count);
@@ -253,7 +266,7 @@ int launch_tile(const Launch& L, const void* src, void* dst, unsigned long long*
 
 template <typename Cell, int OP, bool BB, int STRATEGY, int BACKEND>
 int run_percell(const Launch& L, const PercellArgs& a) {
-    const uint64_t B = a.total_blocks;
+    const uint64_t B = a.launch_count;
     if (B == 0) return NBB_OK;
     const unsigned threads = (unsigned)std::max(32, a.edge * a.edge);
     const uint64_t X = std::min<uint64_t>(B, 65536);
@@ -274,6 +287,10 @@ int launch_percell(const Launch& L, const void* src, void* dst, uint32_t birth, 
     a.partials = L.ctx->partials;
     a.n = L.plan.n;
     a.total_blocks = L.plan.blocks();
+    uint64_t lo, hi;
+    shard_range(L, &lo, &hi);
+    a.ordinal_base = lo;
+    a.launch_count = hi - lo;
     a.gw = (uint64_t)L.plan.gw;
     a.edge = L.plan.edge;
     a.map_level = L.plan.map_level;
@@ -711,6 +728,40 @@ int nbb_gpu_lambda_coords(const nbb_config* cfg, int32_t level, int64_t* xy) {
     NBB_CHECK(nbb_gpu_lambda_coords_dev(cfg, level, d, 8, ctx->stream));
     NBB_CUDA(cudaMemcpyAsync(xy, d, bytes, cudaMemcpyDeviceToHost, ctx->stream));
     NBB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return NBB_OK;
+}
+
+int nbb_gpu_gather_cells_dev(const nbb_config* cfg, const void* d_grid, const int64_t* d_idx,
+                             int64_t count, void* d_out, void* stream) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    if (count <= 0) return NBB_OK;
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    const unsigned blocks = (unsigned)std::min<int64_t>((count + 255) / 256, 65535);
+    if (cfg->cell_width == 8)
+        gather_cells_kernel<long long><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+            (const long long*)d_grid, (const long long*)d_idx, count, (long long*)d_out);
+    else
+        gather_cells_kernel<unsigned char><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+            (const unsigned char*)d_grid, (const long long*)d_idx, count, (unsigned char*)d_out);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+int nbb_gpu_scatter_cells_dev(const nbb_config* cfg, void* d_grid, const int64_t* d_idx,
+                              int64_t count, const void* d_vals, void* stream) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    if (count <= 0) return NBB_OK;
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    const unsigned blocks = (unsigned)std::min<int64_t>((count + 255) / 256, 65535);
+    if (cfg->cell_width == 8)
+        scatter_cells_kernel<long long><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+            (long long*)d_grid, (const long long*)d_idx, count, (const long long*)d_vals);
+    else
+        scatter_cells_kernel<unsigned char><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+            (unsigned char*)d_grid, (const long long*)d_idx, count, (const unsigned char*)d_vals);
+    NBB_CUDA(cudaGetLastError());
     return NBB_OK;
 }
 

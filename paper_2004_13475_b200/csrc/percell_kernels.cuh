@@ -24,7 +24,9 @@ struct PercellArgs {
     void* dst;
     unsigned long long* partials;  // RD: 4096 slots, pre-zeroed
     int64_t n;
-    uint64_t total_blocks;         // launched blocks (incl. mma2 padding)
+    uint64_t total_blocks;         // blocks of the whole plan (incl. mma2 padding)
+    uint64_t ordinal_base;         // first ordinal of this launch (shard)
+    uint64_t launch_count;         // ordinals in this launch
     uint64_t gw;                   // launch grid width (blocks)
     int edge;                      // thread-block edge (ρ, or ρ/2 for mma2)
     int map_level;                 // levels per block origin
@@ -99,8 +101,9 @@ __global__ void percell_kernel(PercellArgs a) {
     __shared__ int64_t s_origin[2];
     __shared__ unsigned long long s_red[32];
 
-    const uint64_t ordinal = flat_block();
-    if (ordinal >= a.total_blocks) return;
+    const uint64_t flat = flat_block();
+    if (flat >= a.launch_count) return;
+    const uint64_t ordinal = a.ordinal_base + flat;
     const int edge = a.edge;
     const int tid = threadIdx.x;
     const bool real = tid < edge * edge;

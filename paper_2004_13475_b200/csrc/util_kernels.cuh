@@ -147,6 +147,21 @@ __global__ void scatter_members_kernel(const long long* values, long long* grid,
     }
 }
 
+// ---- halo pack / unpack (K4) for sharded CA -----------------------------------
+template <typename Cell>
+__global__ void gather_cells_kernel(const Cell* grid, const long long* idx, long long count, Cell* out) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = grid[idx[i]];
+}
+
+template <typename Cell>
+__global__ void scatter_cells_kernel(Cell* grid, const long long* idx, long long count, const Cell* vals) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (long long)gridDim.x * blockDim.x)
+        grid[idx[i]] = vals[i];
+}
+
 // ---- K0: λ map of a whole orthotope (scalar closed form) ----------------------
 // 4 ordinals per thread; int32 pairs -> one 32-byte store, int64 pairs -> two.
 template <typename Coord>

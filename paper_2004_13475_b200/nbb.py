@@ -216,6 +216,8 @@ class DispatchConfig:
     cell_width: int = 8
     kernel: KernelFamily = KernelFamily.Auto
     device: int = 0
+    shard_begin: int = 0
+    shard_count: int = 0  # 0 = every block ordinal of the plan
 
     def to_c(self) -> _abi.NbbConfig:
         c = _abi.NbbConfig()
@@ -231,6 +233,8 @@ class DispatchConfig:
         c.kernel = int(self.kernel)
         c.device = self.device
         c.max_cells = self.max_cells
+        c.shard_begin = self.shard_begin
+        c.shard_count = self.shard_count
         return c
 
     def validate(self) -> None:                         # dispatch.cpp:50-114

@@ -1,0 +1,315 @@
+"""GPU parity: every kernel family against the C oracle / the reference's golden
+outputs, bit-exact (integer and byte work). Run on a B200 with `pytest -m gpu`."""
+import itertools
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from _oracle import (GASKET, ROOT, fnv1a64, orc_ca, orc_lambda_coords, orc_random_member_grid,
+                     orc_reduction, orc_single_write)
+from paper_2004_13475_b200 import _abi, nbb
+from paper_2004_13475_b200.nbb import (CaRule, DispatchConfig, Grid, IntraBlockStrategy,
+                                       KernelFamily, LambdaBackend, MapMode)
+
+pytestmark = pytest.mark.gpu
+
+B3S23 = CaRule()
+
+
+def cfg(**kw):
+    c = DispatchConfig()
+    for k, v in kw.items():
+        setattr(c, k, v)
+    n = c.spec.side_length(c.r)
+    c.max_cells = max(c.max_cells, n * n)
+    return c
+
+
+def grid(values, r):
+    return Grid(GASKET, r, np.ascontiguousarray(values, dtype=np.int64))
+
+
+def nonmember_mask(r):
+    n = 1 << r
+    yy, xx = np.mgrid[0:n, 0:n]
+    return (xx & (n - 1 - yy)) != 0
+
+
+def with_garbage(values, r, seed=0):
+    g = values.copy()
+    m = nonmember_mask(r)
+    rng = np.random.default_rng(seed)
+    g[m] = rng.integers(-2**62, 2**62, size=int(m.sum()))
+    return g
+
+
+KERNEL_COMBOS = [  # (mode, rho, kernel, cell_width)
+    (MapMode.Lambda, rho, k, cw)
+    for rho in (1, 2, 4, 8, 16, 32) for k in (KernelFamily.Auto, KernelFamily.PerCell)
+    for cw in (8, 1)
+] + [(MapMode.BoundingBox, rho, k, cw)
+     for rho in (1, 2, 4, 8, 16, 32) for k in (KernelFamily.Auto, KernelFamily.PerCell)
+     for cw in (8, 1)]
+
+
+def test_device_present():
+    assert nbb.device_count() >= 1
+
+
+@pytest.mark.parametrize("r", [0, 1, 2, 3, 5, 6, 8, 10])
+def test_single_write(r):
+    want = orc_single_write(r)
+    for mode, rho, k, _ in KERNEL_COMBOS:
+        if (1 << r) % rho:
+            continue
+        got = nbb.run_single_write(cfg(r=r, rho=rho, mode=mode, kernel=k))
+        assert np.array_equal(got.grid.values, want), (mode, rho, k)
+        assert got.report.csv_row() == nbb.plan_report(cfg(r=r, rho=rho, mode=mode)).csv_row()
+
+
+@pytest.mark.parametrize("r", [0, 2, 4, 5, 7, 9, 10])
+def test_reduction_ignores_nonmember_garbage(r):
+    g = with_garbage(orc_random_member_grid(r, 5 + r, 1 << 40), r, seed=r)
+    want = orc_reduction(r, g)
+    for mode, rho, k, cw in KERNEL_COMBOS:
+        if (1 << r) % rho or cw != 8:
+            continue
+        got = nbb.run_reduction(cfg(r=r, rho=rho, mode=mode, kernel=k), grid(g, r))
+        assert got.value == want, (mode, rho, k)
+
+
+def test_reduction_wraps_like_int64():
+    r = 6
+    g = orc_random_member_grid(r, 3, 2)
+    g[g == 1] = 2**62 + 12345  # sum overflows int64: must wrap identically
+    assert nbb.run_reduction(cfg(r=r, rho=8), grid(g, r)).value == orc_reduction(r, g)
+
+
+RULES = [CaRule(), CaRule(birth=(1 << 3) | (1 << 6), survive=(1 << 2) | (1 << 3)),
+         CaRule(birth=1 << 2, survive=0), CaRule(birth=0x1FF, survive=0x1FF),
+         CaRule(birth=1 | (1 << 8), survive=(1 << 1) | (1 << 8)), CaRule(birth=0, survive=0)]
+
+
+@pytest.mark.parametrize("r", [1, 2, 3, 5, 6, 8, 9])
+def test_ca_all_kernels(r):
+    init = with_garbage(orc_random_member_grid(r, 40 + r, 2), r, seed=r) if r >= 2 else \
+        orc_random_member_grid(r, 40 + r, 2)
+    for rule in RULES[:3] if r > 6 else RULES:
+        for steps in (1, 3):
+            want = orc_ca(r, init, steps, rule.birth, rule.survive)
+            for mode, rho, k, cw in KERNEL_COMBOS:
+                if (1 << r) % rho:
+                    continue
+                got = nbb.run_ca(cfg(r=r, rho=rho, mode=mode, kernel=k, cell_width=cw),
+                                 grid(init, r), steps, rule)
+                assert np.array_equal(got.grid.values, want), (mode, rho, k, cw, rule, steps)
+                assert len(got.reports) == steps
+                assert got.grid.generation() == steps
+
+
+def test_ca_semantics_probes():
+    """App. B.4: steps=0 returns the input unchanged (garbage included); alive means != 0."""
+    r = 6
+    g = with_garbage(orc_random_member_grid(r, 1, 2), r)
+    c = cfg(r=r, rho=8)
+    assert np.array_equal(nbb.run_ca(c, grid(g, r), 0).grid.values, g)
+    g5 = orc_random_member_grid(r, 1, 2)
+    a = nbb.run_ca(c, grid(g5 * 5, r), 4).grid.values
+    assert np.array_equal(a, nbb.run_ca(c, grid(g5, r), 4).grid.values)
+    dead = np.zeros_like(g5)
+    assert not nbb.run_ca(c, grid(dead, r), 3).grid.values.any()
+    lonely = dead.copy()
+    lonely[0, 0] = 1
+    assert not nbb.run_ca(c, grid(lonely, r), 1).grid.values.any()
+
+
+def test_reference_pins(golden):
+    p = golden["pins"]
+    for seed in (1234, 2024):
+        g = orc_random_member_grid(5, seed, 2)
+        for rho, mode in ((1, MapMode.Lambda), (8, MapMode.Lambda), (32, MapMode.Lambda),
+                          (1, MapMode.BoundingBox), (32, MapMode.BoundingBox)):
+            for steps in (1, 4, 10):
+                out = nbb.run_ca(cfg(r=5, rho=rho, mode=mode), grid(g, 5), steps).grid.values
+                assert fnv1a64(out) == p[f"ca_r5_seed{seed}"]["steps"][steps], (seed, rho, steps)
+    g = orc_random_member_grid(5, 99, 1000)
+    assert nbb.run_reduction(cfg(r=5, rho=4), grid(g, 5)).value == p["rd_r5_seed99_mod1000"]
+
+
+def test_mode_equivalence_matrix(golden):
+    """acceptance.cpp:153-208 — every valid (rho, strategy, backend) computes the same
+    SW grid, RD value and 2-step CA grid as the reference, r <= 8."""
+    for r in range(0, 9):
+        w = golden["workloads"][str(r)]
+        rd = orc_random_member_grid(r, 17 + r, 100)
+        ca = orc_random_member_grid(r, 71 + r, 2)
+        combos = 0
+        for rho, st, be in itertools.product((1, 2, 4, 8, 16), IntraBlockStrategy, LambdaBackend):
+            c = cfg(r=r, rho=rho, strategy=st, backend=be)
+            try:
+                c.validate()
+            except nbb.InvalidArgument:
+                continue
+            tag = (r, rho, st.name, be.name)
+            assert fnv1a64(nbb.run_single_write(c).grid.values) == w["sw_fnv"], tag
+            assert nbb.run_reduction(c, grid(rd, r)).value == w["acceptance_rd_value"], tag
+            assert fnv1a64(nbb.run_ca(c, grid(ca, r), 2).grid.values) == w["acceptance_ca2_fnv"], tag
+            combos += 1
+        assert combos > 0
+
+
+@pytest.mark.parametrize("r", [11, 12, 13, 14])
+def test_golden_workloads_tile_path(golden, r):
+    w = golden["workloads"][str(r)]
+    for rho in (8, 16, 32):
+        for mode in (MapMode.Lambda, MapMode.BoundingBox):
+            c = cfg(r=r, rho=rho, mode=mode, kernel=KernelFamily.Tile)
+            assert fnv1a64(nbb.run_single_write(c).grid.values) == w["sw_fnv"], (rho, mode)
+    g = nbb.random_member_grid(GASKET, r, 1 + r, 100, max_cells=1 << (2 * r))
+    assert fnv1a64(g.values) == w["rd_grid_fnv"]
+    for rho in (8, 16, 32):
+        assert nbb.run_reduction(cfg(r=r, rho=rho, kernel=KernelFamily.Tile), g).value == w["rd_value"]
+    g = nbb.random_member_grid(GASKET, r, 1 + r, 2, max_cells=1 << (2 * r))
+    for rho, cw, mode in ((32, 8, MapMode.Lambda), (16, 8, MapMode.Lambda), (8, 8, MapMode.Lambda),
+                          (32, 1, MapMode.Lambda), (32, 8, MapMode.BoundingBox),
+                          (32, 1, MapMode.BoundingBox)):
+        c = cfg(r=r, rho=rho, mode=mode, cell_width=cw, kernel=KernelFamily.Tile)
+        for k, (pop, digest) in w["ca"].items():
+            out = nbb.run_ca(c, g, int(k)).grid.values
+            assert (int(out.sum()), fnv1a64(out)) == (pop, digest), (rho, cw, mode, k)
+
+
+def test_lambda_coords_map_kernels(golden):
+    for level in range(0, 16):
+        want = golden["lambda_digests"][str(level)]
+        assert fnv1a64(nbb.lambda_coords(cfg(r=level), level)) == want, level
+        if level <= 16:
+            got = nbb.lambda_coords(cfg(r=level, backend=LambdaBackend.MmaV2), level)
+            assert fnv1a64(got) == want, ("tc", level)
+    assert np.array_equal(nbb.lambda_coords(cfg(), 9), orc_lambda_coords(9))
+
+
+def test_workers_shard_the_ordinal_range():
+    """Contiguous ordinal chunks (dispatch.cpp:419-427) give identical results for any count."""
+    r = 9
+    g = orc_random_member_grid(r, 8, 2)
+    v = orc_random_member_grid(r, 8, 50)
+    base = None
+    for workers in (1, 2, 3, 5, 8):
+        c = cfg(r=r, rho=16, workers=workers)
+        out = (fnv1a64(nbb.run_single_write(c).grid.values), nbb.run_reduction(c, grid(v, r)).value,
+               fnv1a64(nbb.run_ca(c, grid(g, r), 4).grid.values))
+        base = base or out
+        assert out == base, workers
+
+
+def test_timing_reports_micros():
+    r = 10
+    c = cfg(r=r, rho=32, timing=True)
+    res = nbb.run_ca(c, grid(orc_random_member_grid(r, 1, 2), r), 2)
+    assert all(rep.micros >= 0 for rep in res.reports)
+    assert nbb.run_single_write(cfg(r=r, rho=32)).report.micros == 0
+
+
+def test_device_resident_api():
+    torch = pytest.importorskip("torch")
+    from paper_2004_13475_b200 import device as dev
+    r = 12
+    n = 1 << r
+    c = cfg(r=r, rho=32)
+    values = nbb.random_member_values(GASKET, r, 13, 2)
+    d_vals = torch.from_numpy(values).cuda()
+    a = torch.zeros((n, n), dtype=torch.int64, device="cuda")
+    b = torch.zeros_like(a)
+    s = torch.cuda.current_stream().cuda_stream
+    dev.scatter_members_dev(c, d_vals.data_ptr(), a.data_ptr(), s)
+    host = nbb.random_member_grid(GASKET, r, 13, 2)
+    assert np.array_equal(a.cpu().numpy(), host.values)
+    want = orc_ca(r, host.values, 3)
+    for _ in range(3):
+        dev.ca_step_dev(c, a.data_ptr(), b.data_ptr(), CaRule(), s)
+        a, b = b, a
+    assert np.array_equal(a.cpu().numpy(), want)
+    # uint8 state path: pack -> steps -> unpack
+    a8 = torch.zeros((n, n), dtype=torch.uint8, device="cuda")
+    b8 = torch.zeros_like(a8)
+    g64 = torch.from_numpy(with_garbage(host.values, r)).cuda()
+    c8 = cfg(r=r, rho=32, cell_width=1)
+    dev.pack_alive_dev(c8, g64.data_ptr(), a8.data_ptr(), s)
+    for _ in range(3):
+        dev.ca_step_dev(c8, a8.data_ptr(), b8.data_ptr(), CaRule(), s)
+        a8, b8 = b8, a8
+    out64 = torch.empty_like(g64)
+    dev.unpack_alive_dev(c8, a8.data_ptr(), out64.data_ptr(), s)
+    assert np.array_equal(out64.cpu().numpy(), want)
+    # sanitize zeroes exactly the non-members
+    gg = torch.from_numpy(with_garbage(host.values, r)).cuda()
+    dev.sanitize_dev(c, gg.data_ptr(), s)
+    assert np.array_equal(gg.cpu().numpy(), host.values)
+    # reduction into device memory
+    val = torch.zeros(1, dtype=torch.int64, device="cuda")
+    hv = nbb.random_member_grid(GASKET, r, 5, 1000)
+    dv = torch.from_numpy(hv.values).cuda()
+    dev.reduction_dev(c, dv.data_ptr(), val.data_ptr(), s)
+    assert int(val.item()) == orc_reduction(r, hv.values)
+    # map kernel into device memory, int32 pairs
+    xy = torch.empty((3 ** 10, 2), dtype=torch.int32, device="cuda")
+    dev.lambda_coords_dev(c, 10, xy.data_ptr(), 4, s)
+    assert np.array_equal(xy.cpu().numpy().astype(np.int64), orc_lambda_coords(10))
+
+
+def test_cpp_shim_on_gpu():
+    src = os.path.join(ROOT, "tests", "cpp", "shim_example.cpp")
+    out = "/tmp/nbb_shim_example_gpu"
+    libdir = os.path.dirname(_abi.LIB_PATH)
+    subprocess.run(["/usr/bin/g++", "-std=c++17", f"-I{os.path.join(ROOT, 'include')}", src, "-o", out,
+                    f"-L{libdir}", "-lnbbgpu", f"-Wl,-rpath,{libdir}"], check=True)
+    r = subprocess.run([out], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ca pop 10398" in r.stdout
+
+
+@pytest.mark.slow
+def test_full_size_r16_properties():
+    """n = 2^16: λ tile, BB tile and λ per-cell kernels agree (mode equivalence at full
+    size) on SW / RD / one CA step, RD equals the reference's value (App. B.2), and the
+    populations are consistent."""
+    torch = pytest.importorskip("torch")
+    from paper_2004_13475_b200 import device as dev
+    r, n = 16, 1 << 16
+    s = torch.cuda.current_stream().cuda_stream
+    c = cfg(r=r, rho=32)
+    a = torch.zeros((n, n), dtype=torch.int64, device="cuda")
+    vals = torch.from_numpy(nbb.random_member_values(GASKET, r, 17, 100)).cuda()
+    dev.scatter_members_dev(c, vals.data_ptr(), a.data_ptr(), s)
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for cc in (c, cfg(r=r, rho=32, mode=MapMode.BoundingBox), cfg(r=r, rho=16),
+               cfg(r=r, rho=32, kernel=KernelFamily.PerCell)):
+        dev.reduction_dev(cc, a.data_ptr(), out.data_ptr(), s)
+        assert int(out.item()) == 2131135664
+    del vals
+    # CA: seed 17 mod 2 (BASELINE C3)
+    a.zero_()
+    vals = torch.from_numpy(nbb.random_member_values(GASKET, r, 17, 2)).cuda()
+    dev.scatter_members_dev(c, vals.data_ptr(), a.data_ptr(), s)
+    pop0 = int(a.sum().item())
+    assert pop0 == int(vals.sum().item())
+    b = torch.zeros_like(a)
+    dev.ca_step_dev(c, a.data_ptr(), b.data_ptr(), CaRule(), s)
+    ref_sum = int(b.sum().item())
+    rows, cols = b.sum(dim=1), b.sum(dim=0)  # checksum pair: row and column populations
+    for cc in (cfg(r=r, rho=32, mode=MapMode.BoundingBox), cfg(r=r, rho=16),
+               cfg(r=r, rho=32, kernel=KernelFamily.PerCell)):
+        b.zero_()
+        dev.ca_step_dev(cc, a.data_ptr(), b.data_ptr(), CaRule(), s)
+        assert int(b.sum().item()) == ref_sum
+        assert torch.equal(b.sum(dim=1), rows) and torch.equal(b.sum(dim=0), cols)
+    # uint8 path agrees too
+    a8 = torch.zeros((n, n), dtype=torch.uint8, device="cuda")
+    b8 = torch.zeros_like(a8)
+    c8 = cfg(r=r, rho=32, cell_width=1)
+    dev.pack_alive_dev(c8, a.data_ptr(), a8.data_ptr(), s)
+    dev.ca_step_dev(c8, a8.data_ptr(), b8.data_ptr(), CaRule(), s)
+    assert int(b8.sum(dtype=torch.int64).item()) == ref_sum

@@ -1,0 +1,113 @@
+"""Multi-rank partition of the λ launch on CPU (gloo, world_size 2 and 3): contiguous
+ordinal chunks + static halo lists + all_to_all exchange reproduce the single-domain
+CA exactly. Each rank updates only the tiles it owns (a numpy stepper standing in for
+the device kernel), from a replica whose non-owned cells are stale except for the
+exchanged halo cells — so a missing halo cell shows up as a wrong state."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from _oracle import orc_ca, orc_random_member_grid
+from paper_2004_13475_b200.shard import ShardPlan, lambda_blocks, lambda_inverse_blocks
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _ca_owned_tiles(src: np.ndarray, plan: ShardPlan, birth=8, survive=12) -> np.ndarray:
+    """One B/S step for the cells of this rank's tiles (others copied unchanged)."""
+    n = src.shape[0]
+    rho = plan.rho
+    alive = (src != 0).astype(np.int64)
+    yy, xx = np.mgrid[0:n, 0:n]
+    member = (xx & (n - 1 - yy)) == 0
+    alive &= member
+    pad = np.pad(alive, 1)
+    live = sum(pad[1 + dy:1 + dy + n, 1 + dx:1 + dx + n]
+               for dy in (-1, 0, 1) for dx in (-1, 0, 1) if (dx, dy) != (0, 0))
+    rule = np.where(alive == 1, (survive >> live) & 1, (birth >> live) & 1)
+    nxt = (rule & member).astype(np.int64)
+    out = src.copy()
+    t = np.arange(plan.begin, plan.begin + plan.count, dtype=np.int64)
+    bx, by = lambda_blocks(t, plan.W)
+    for x0, y0 in zip(bx * rho, by * rho):
+        out[y0:y0 + rho, x0:x0 + rho] = nxt[y0:y0 + rho, x0:x0 + rho]
+    return out
+
+
+def _worker(rank, world, port, r, rho, steps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    plan = ShardPlan(r=r, rho=rho, world=world, rank=rank)
+    g = torch.from_numpy(orc_random_member_grid(r, 1234, 2))
+    # make non-owned cells stale garbage: only owned tiles + halos may be trusted
+    own = np.zeros(g.shape, dtype=bool)
+    t = np.arange(plan.begin, plan.begin + plan.count, dtype=np.int64)
+    bx, by = lambda_blocks(t, plan.W)
+    for x0, y0 in zip(bx * rho, by * rho):
+        own[y0:y0 + rho, x0:x0 + rho] = True
+    g[torch.from_numpy(~own)] = 7
+    gather = lambda flat, idx: flat[idx].clone()  # noqa: E731
+    def scatter(flat, idx, vals):
+        flat[idx] = vals
+    for _ in range(steps):
+        plan.exchange_halo(g, dist, gather=gather, scatter=scatter)
+        g = torch.from_numpy(_ca_owned_tiles(g.numpy(), plan))
+    # collect owned tiles on rank 0
+    full = torch.where(torch.from_numpy(own), g, torch.zeros_like(g))
+    dist.all_reduce(full)
+    if rank == 0:
+        q.put((full.numpy(), plan.halo_cells_received()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,r,rho", [(2, 7, 8), (3, 7, 4), (2, 8, 16)])
+def test_sharded_ca_matches_single_domain(world, r, rho):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(i, world, port, r, rho, 5, q)) for i in range(world)]
+    for p in procs:
+        p.start()
+    got, halo = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = orc_ca(r, orc_random_member_grid(r, 1234, 2), 5)
+    assert np.array_equal(got, want)
+    assert halo > 0
+
+
+def test_halo_lists_are_symmetric_and_small():
+    """App. A.5: each tile needs <= 8 remote cells; what rank a receives from b is
+    exactly what b sends to a."""
+    r, rho = 12, 32
+    for world in (2, 4, 8):
+        plans = [ShardPlan(r=r, rho=rho, world=world, rank=k) for k in range(world)]
+        for a in range(world):
+            assert sum(p.count for p in plans) == 3 ** (r - 5)
+            for b in range(world):
+                recv_ab = plans[a].recv_idx[sum(plans[a].recv_counts[:b]):
+                                            sum(plans[a].recv_counts[:b + 1])]
+                send_ba = plans[b].send_idx[sum(plans[b].send_counts[:a]):
+                                            sum(plans[b].send_counts[:a + 1])]
+                assert np.array_equal(recv_ab, send_ba)
+            assert plans[a].halo_cells_received() <= 8 * plans[a].count
+
+
+def test_lambda_inverse_blocks_round_trip():
+    for r_b in range(0, 9):
+        W = 3 ** ((r_b + 1) // 2)
+        t = np.arange(3 ** r_b, dtype=np.int64)
+        bx, by = lambda_blocks(t, W)
+        assert np.array_equal(lambda_inverse_blocks(bx, by, r_b, W), t)
