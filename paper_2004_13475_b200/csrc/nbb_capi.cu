@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -23,6 +24,8 @@
 #include "nbb_host.hpp"
 #include "percell_kernels.cuh"
 #include "tile_kernels.cuh"
+#include "ca_pipe_kernel.cuh"
+#include "bits_kernels.cuh"
 #include "util_kernels.cuh"
 
 using namespace nbbgpu;
@@ -178,13 +181,101 @@ bool tile_supported(const nbb_config& c, int op, int cell_width) {
         return false;
     if (c.r > 17) return false;
     if (cell_width == 8) return c.rho == 8 || c.rho == 16 || c.rho == 32;
+    if (cell_width == 0) return c.rho == 32 && op == OP_CA;
     return c.rho == 32 && op != OP_RD;
+}
+
+// CA on the bit-packed state (bits_kernels.cuh)
+template <bool BB>
+int run_ca_bits(const Launch& L, const TileArgs& a) {
+    auto kern = ca_bits_kernel<BB, 2>;
+    static int occ = 0;
+    if (occ == 0) {
+        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0));
+        if (occ < 1) occ = 1;
+    }
+    const uint64_t units = (a.tiles + 1) / 2;
+    const uint64_t want = (units + 7) / 8;
+    const uint64_t cap = (uint64_t)L.ctx->sms * (uint64_t)occ;
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min(want, cap));
+    if (a.tiles == 0) return NBB_OK;
+    kern<<<blocks, 256, 0, L.stream>>>(a);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+TileArgs make_tile_args(const Launch& L, const void* src, void* dst, unsigned long long* sum,
+                        uint32_t birth, uint32_t survive, uint32_t tile_begin, uint32_t tiles) {
+    TileArgs a;
+    a.src = src;
+    a.dst = dst;
+    a.sum = sum;
+    a.n = L.plan.n;
+    a.tile_begin = tile_begin;
+    a.tiles = tiles;
+    a.gw = (uint32_t)L.plan.gw;
+    nbbhost::fastdiv_magic(a.gw, &a.div_gw.m, &a.div_gw.s);
+    a.div_gw.d = a.gw;
+    a.birth = birth;
+    a.survive = survive;
+    return a;
+}
+
+// CA through the cp.async pipeline kernel (ca_pipe_kernel.cuh)
+template <typename Cell, int RHO, bool BB, int STAGES, int WARPS>
+int run_ca_pipe(const Launch& L, const TileArgs& a) {
+    using P = CaPipeShape<Cell, RHO, BB, STAGES, WARPS>;
+    auto kern = ca_pipe_kernel<Cell, RHO, BB, STAGES, WARPS>;
+    static int occ = 0;
+    if (occ == 0) {
+        NBB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM));
+        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, P::SMEM));
+        if (occ < 1) return fail(NBB_ERR_RESOURCE, "ca pipeline kernel does not fit on an SM");
+    }
+    constexpr int TPW = 32 / RHO;
+    const uint64_t units = (a.tiles + TPW - 1) / TPW;
+    const uint64_t want = (units + WARPS - 1) / WARPS;
+    const uint64_t cap = (uint64_t)L.ctx->sms * (uint64_t)occ;
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min(want, cap));
+    if (a.tiles == 0) return NBB_OK;
+    kern<<<blocks, WARPS * 32, P::SMEM, L.stream>>>(a);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+// pipeline shape: NBB_CA_PIPE="stages,warps" (tuning), "0" = register-staged tile kernel
+int ca_pipe_choice() {
+    static int choice = -1;
+    if (choice < 0) {
+        choice = 1;
+        if (const char* e = std::getenv("NBB_CA_PIPE")) {
+            const std::string s(e);
+            choice = s == "0" ? 0 : s == "2,8" ? 1 : s == "3,4" ? 2 : s == "4,4" ? 3 : s == "3,8" ? 4 : 1;
+        }
+    }
+    return choice;
+}
+
+template <typename Cell, int RHO, bool BB>
+int run_ca_tile(const Launch& L, const TileArgs& a) {
+    switch (ca_pipe_choice()) {
+        case 2: return run_ca_pipe<Cell, RHO, BB, 3, 4>(L, a);
+        case 3: return run_ca_pipe<Cell, RHO, BB, 4, 4>(L, a);
+        case 4: return run_ca_pipe<Cell, RHO, BB, 3, 8>(L, a);
+        default: return run_ca_pipe<Cell, RHO, BB, 2, 8>(L, a);
+    }
 }
 
 // rule masks travel in TileArgs; thin wrapper so CA can set them.
 template <typename Cell, int RHO, int OP, bool BB>
 int run_tile_rule(const Launch& L, const void* src, void* dst, unsigned long long* sum,
                   uint32_t birth, uint32_t survive, uint32_t tile_begin, uint32_t tiles) {
+    if constexpr (OP == OP_CA && !BB) {  // BB keeps the register-staged kernel (faster for BB)
+        if (ca_pipe_choice() != 0) {
+            return run_ca_tile<Cell, RHO, BB>(
+                L, make_tile_args(L, src, dst, sum, birth, survive, tile_begin, tiles));
+        }
+    }
     auto kern = tile_kernel<Cell, RHO, OP, BB>;
     static int occ = 0;
     if (occ == 0) {
@@ -350,6 +441,22 @@ int launch_op(const Launch& L, int op, const void* src, void* dst, unsigned long
         NBB_CUDA(cudaGetLastError());
         return NBB_OK;
     }
+    if (cw == 0) {  // bit-packed alive state: CA through the ρ = 32 tile kernel only
+        if (!tile)
+            return fail(NBB_ERR_INVALID_ARGUMENT,
+                        "the 1-bit packed state (cell_width 0) runs the CA step through the tile "
+                        "kernel only: bb or lambda/subbox/direct with rho = 32");
+        uint64_t lo, hi;
+        shard_range(L, &lo, &hi);
+        const uint32_t workers = (uint32_t)std::max(1, c.workers);
+        const uint32_t tiles = (uint32_t)(hi - lo), chunk = (tiles + workers - 1) / workers;
+        for (uint32_t w = 0; w < workers && w * chunk < tiles; ++w) {
+            const TileArgs a = make_tile_args(L, src, dst, nullptr, birth, survive,
+                                              (uint32_t)lo + w * chunk, std::min(chunk, tiles - w * chunk));
+            NBB_CHECK(c.mode == NBB_MODE_BB ? run_ca_bits<true>(L, a) : run_ca_bits<false>(L, a));
+        }
+        return NBB_OK;
+    }
     if (cw == 8) {
         if (tile) {
             return op == OP_SW ? launch_tile<long long, OP_SW>(L, src, dst, nullptr, 0, 0)
@@ -391,13 +498,20 @@ int sanitize(const Launch& L, void* d_grid, int cell_width, cudaStream_t s) {
     const int blocks = L.ctx->sms * 8;
     if (cell_width == 8)
         sanitize_kernel<long long><<<blocks, 256, 0, s>>>((long long*)d_grid, L.plan.n, 0);
-    else
+    else if (cell_width == 1)
         sanitize_kernel<unsigned char><<<blocks, 256, 0, s>>>((unsigned char*)d_grid, L.plan.n, 0);
+    else
+        sanitize_bits_kernel<<<blocks, 256, 0, s>>>((uint32_t*)d_grid, L.plan.n);
     NBB_CUDA(cudaGetLastError());
     return NBB_OK;
 }
 
-size_t grid_bytes(const Launch& L, int cw) { return (size_t)L.plan.n * (size_t)L.plan.n * cw; }
+// bytes of an n x n grid of cw-byte cells (cw = 0: 1-bit packed, 32-bit words per row)
+size_t grid_bytes(const Launch& L, int cw) {
+    const size_t n = (size_t)L.plan.n;
+    if (cw == 0) return n * std::max<size_t>(1, n / 32) * 4;
+    return n * n * (size_t)cw;
+}
 
 }  // namespace
 
@@ -556,8 +670,12 @@ int nbb_gpu_sanitize_dev(const nbb_config* cfg, void* d_grid, void* stream) {
 int nbb_gpu_pack_alive_dev(const nbb_config* cfg, const void* d64, void* d8, void* stream) {
     Launch L;
     NBB_CHECK(prepare(cfg, OP_CA, &L, false));
-    pack_alive_kernel<<<L.ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>(
-        (const long long*)d64, (unsigned char*)d8, L.plan.n);
+    if (cfg->cell_width == 0)
+        pack_bits_kernel<<<L.ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>(
+            (const long long*)d64, (uint32_t*)d8, L.plan.n);
+    else
+        pack_alive_kernel<<<L.ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>(
+            (const long long*)d64, (unsigned char*)d8, L.plan.n);
     NBB_CUDA(cudaGetLastError());
     return NBB_OK;
 }
@@ -565,8 +683,12 @@ int nbb_gpu_pack_alive_dev(const nbb_config* cfg, const void* d64, void* d8, voi
 int nbb_gpu_unpack_alive_dev(const nbb_config* cfg, const void* d8, void* d64, void* stream) {
     Launch L;
     NBB_CHECK(prepare(cfg, OP_CA, &L, false));
-    unpack_alive_kernel<<<L.ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>(
-        (const unsigned char*)d8, (long long*)d64, L.plan.n);
+    if (cfg->cell_width == 0)  // writes member sectors only: d64's non-member cells must be 0
+        unpack_bits_kernel<<<L.ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>(
+            (const uint32_t*)d8, (long long*)d64, L.plan.n);
+    else
+        unpack_alive_kernel<<<L.ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>(
+            (const unsigned char*)d8, (long long*)d64, L.plan.n);
     NBB_CUDA(cudaGetLastError());
     return NBB_OK;
 }
@@ -689,7 +811,7 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
         NBB_CHECK(device_buffer(*L.ctx, 1, b64, &db));
         NBB_CHECK(sanitize(L, da, 8, L.stream));
         NBB_CUDA(cudaMemsetAsync(db, 0, b64, L.stream));
-    } else {
+    } else if (cw == 1) {
         const size_t b8 = grid_bytes(L, 1);
         NBB_CHECK(device_buffer(*L.ctx, 1, b8, &da));
         NBB_CHECK(device_buffer(*L.ctx, 2, b8, &db));
@@ -697,6 +819,15 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
                                                                 (unsigned char*)da, L.plan.n);
         NBB_CUDA(cudaGetLastError());
         NBB_CUDA(cudaMemsetAsync(db, 0, b8, L.stream));
+    } else {  // 1-bit packed: sanitize the int64 copy (unpack writes member sectors only)
+        const size_t bb = grid_bytes(L, 0);
+        NBB_CHECK(device_buffer(*L.ctx, 1, bb, &da));
+        NBB_CHECK(device_buffer(*L.ctx, 2, bb, &db));
+        NBB_CHECK(sanitize(L, d64, 8, L.stream));
+        pack_bits_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)d64,
+                                                               (uint32_t*)da, L.plan.n);
+        NBB_CUDA(cudaGetLastError());
+        NBB_CUDA(cudaMemsetAsync(db, 0, bb, L.stream));
     }
     for (int s = 0; s < steps; ++s) {
         Timer t(cfg->timing != 0, L.stream);
@@ -708,6 +839,11 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
     if (cw == 1) {
         unpack_alive_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const unsigned char*)da,
                                                                   (long long*)d64, L.plan.n);
+        NBB_CUDA(cudaGetLastError());
+        da = d64;
+    } else if (cw == 0) {
+        unpack_bits_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const uint32_t*)da,
+                                                                 (long long*)d64, L.plan.n);
         NBB_CUDA(cudaGetLastError());
         da = d64;
     }
@@ -741,6 +877,9 @@ int nbb_gpu_gather_cells_dev(const nbb_config* cfg, const void* d_grid, const in
     if (cfg->cell_width == 8)
         gather_cells_kernel<long long><<<blocks, 256, 0, (cudaStream_t)stream>>>(
             (const long long*)d_grid, (const long long*)d_idx, count, (long long*)d_out);
+    else if (cfg->cell_width == 0)  // bit state: idx are 32-bit word indices
+        gather_cells_kernel<uint32_t><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+            (const uint32_t*)d_grid, (const long long*)d_idx, count, (uint32_t*)d_out);
     else
         gather_cells_kernel<unsigned char><<<blocks, 256, 0, (cudaStream_t)stream>>>(
             (const unsigned char*)d_grid, (const long long*)d_idx, count, (unsigned char*)d_out);
@@ -758,6 +897,9 @@ int nbb_gpu_scatter_cells_dev(const nbb_config* cfg, void* d_grid, const int64_t
     if (cfg->cell_width == 8)
         scatter_cells_kernel<long long><<<blocks, 256, 0, (cudaStream_t)stream>>>(
             (long long*)d_grid, (const long long*)d_idx, count, (const long long*)d_vals);
+    else if (cfg->cell_width == 0)
+        scatter_cells_kernel<uint32_t><<<blocks, 256, 0, (cudaStream_t)stream>>>(
+            (uint32_t*)d_grid, (const long long*)d_idx, count, (const uint32_t*)d_vals);
     else
         scatter_cells_kernel<unsigned char><<<blocks, 256, 0, (cudaStream_t)stream>>>(
             (unsigned char*)d_grid, (const long long*)d_idx, count, (const unsigned char*)d_vals);

@@ -90,9 +90,9 @@ Error validate(const nbb_config& c) {
     if (n % rho != 0)
         return err(NBB_ERR_INVALID_ARGUMENT,
                    "rho " + std::to_string(rho) + " does not divide n = " + std::to_string(n));
-    if (c.cell_width != 8 && c.cell_width != 1)
-        return err(NBB_ERR_INVALID_ARGUMENT,
-                   "cell_width " + std::to_string(c.cell_width) + " is not 8 (int64) or 1 (uint8)");
+    if (c.cell_width != 8 && c.cell_width != 1 && c.cell_width != 0)
+        return err(NBB_ERR_INVALID_ARGUMENT, "cell_width " + std::to_string(c.cell_width) +
+                                                 " is not 8 (int64), 1 (uint8) or 0 (1-bit packed)");
     if (c.mode == NBB_MODE_BB) {
         if (c.backend != NBB_BACKEND_DIRECT)
             return err(NBB_ERR_INVALID_ARGUMENT, "lambda backends apply to lambda mode only");

@@ -109,6 +109,27 @@ def test_ca_all_kernels(r):
                 assert got.grid.generation() == steps
 
 
+@pytest.mark.parametrize("r", [5, 6, 8, 10, 12])
+def test_ca_bit_packed_state(golden, r):
+    """cell_width 0: the alive state is one bit per cell (exact: CA reads != 0, writes 0/1)."""
+    init = with_garbage(orc_random_member_grid(r, 90 + r, 2), r, seed=r) if r <= 10 else \
+        orc_random_member_grid(r, 90 + r, 2)
+    for rule in (RULES[:4] if r <= 8 else RULES[:1]):
+        for steps in (1, 2, 7):
+            want = orc_ca(r, init, steps, rule.birth, rule.survive)
+            for mode in (MapMode.Lambda, MapMode.BoundingBox):
+                got = nbb.run_ca(cfg(r=r, rho=32, mode=mode, cell_width=0), grid(init, r), steps, rule)
+                assert np.array_equal(got.grid.values, want), (r, mode, rule, steps)
+    if r >= 10:
+        w = golden["workloads"][str(r)]
+        g = nbb.random_member_grid(GASKET, r, 1 + r, 2, max_cells=1 << (2 * r))
+        for k, (pop, digest) in w["ca"].items():
+            out = nbb.run_ca(cfg(r=r, rho=32, cell_width=0), g, int(k)).grid.values
+            assert (int(out.sum()), fnv1a64(out)) == (pop, digest), k
+    with pytest.raises(nbb.InvalidArgument, match="1-bit packed"):
+        nbb.run_ca(cfg(r=r, rho=16, cell_width=0), grid(init, r), 1)
+
+
 def test_ca_semantics_probes():
     """App. B.4: steps=0 returns the input unchanged (garbage included); alive means != 0."""
     r = 6
@@ -313,3 +334,16 @@ def test_full_size_r16_properties():
     dev.pack_alive_dev(c8, a.data_ptr(), a8.data_ptr(), s)
     dev.ca_step_dev(c8, a8.data_ptr(), b8.data_ptr(), CaRule(), s)
     assert int(b8.sum(dtype=torch.int64).item()) == ref_sum
+    del a8, b8
+    # and the 1-bit packed state: pack -> step -> unpack reproduces the int64 step exactly
+    c1 = cfg(r=r, rho=32, cell_width=0)
+    w1 = torch.zeros((n, n // 32), dtype=torch.int32, device="cuda")
+    w2 = torch.zeros_like(w1)
+    dev.pack_alive_dev(c1, a.data_ptr(), w1.data_ptr(), s)
+    for cc in (c1, cfg(r=r, rho=32, cell_width=0, mode=MapMode.BoundingBox)):
+        w2.zero_()
+        dev.ca_step_dev(cc, w1.data_ptr(), w2.data_ptr(), CaRule(), s)
+        b.zero_()
+        dev.unpack_alive_dev(c1, w2.data_ptr(), b.data_ptr(), s)
+        assert int(b.sum().item()) == ref_sum
+        assert torch.equal(b.sum(dim=1), rows) and torch.equal(b.sum(dim=0), cols)
