@@ -140,7 +140,7 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    r, rho = args.r, 32
+    r, rho = args.level, 32
     steps = max(1, min(args.steps, args.ref_max_steps))
     cores = os.cpu_count() or 1
     secs, micros = reference_ca(r, rho, steps, 17, cores)
@@ -176,7 +176,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--r", type=int, default=16)
+    ap.add_argument("--level", type=int, default=16, help="scale level r (n = 2^r)")
     ap.add_argument("--ref-max-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
@@ -196,13 +196,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    local = local % ndev  # ranks may share a GPU in test setups
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world <= ndev:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # more ranks than GPUs (functional test of the sharded path): gloo
+            dist.init_process_group("gloo")
 
-    r, n = args.r, 1 << args.r
+    r, n = args.level, 1 << args.level
     stream = torch.cuda.current_stream()
     s = stream.cuda_stream
     spec = nbb.FractalSpec.sierpinski()
@@ -222,7 +227,8 @@ def main():
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dev_t = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], device=dev_t, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -308,7 +314,7 @@ def main():
             kk = K if "tile" in name else max(5, K // 10)
             results[name] = timed(ca_runner(c, a, b), kk, W)
 
-    # uint8 alive state (exact: CA only reads != 0 and writes 0/1)
+    # uint8 / 1-bit alive states (exact: CA only reads != 0 and writes 0/1)
     if world == 1:
         a8 = torch.zeros((n, n), dtype=torch.uint8, device="cuda")
         b8 = torch.zeros_like(a8)
@@ -317,6 +323,13 @@ def main():
         results["ca_bb_tile_rho32_u8"] = timed(
             ca_runner(cfg(cell_width=1, mode=nbb.MapMode.BoundingBox), a8, b8), K, W)
         del a8, b8
+        w1 = torch.zeros((n, n // 32), dtype=torch.int32, device="cuda")
+        w2 = torch.zeros_like(w1)
+        dev.pack_alive_dev(cfg(cell_width=0), a.data_ptr(), w1.data_ptr(), s)
+        results["ca_lambda_tile_rho32_bit"] = timed(ca_runner(cfg(cell_width=0), w1, w2), K, W)
+        results["ca_bb_tile_rho32_bit"] = timed(
+            ca_runner(cfg(cell_width=0, mode=nbb.MapMode.BoundingBox), w1, w2), K, W)
+        del w1, w2
 
         # single write and reduction (C2 / C3-RD) on the same buffers
         def sw(c):
@@ -395,6 +408,9 @@ def main():
     best_bb = min((results[k] for k in results if k.startswith("ca_bb") and k.endswith("i64")),
                   default=None)
     best_bb_percell = min((results[k] for k in results if k.startswith("ca_bb_percell")), default=None)
+
+    def ratio(bb, lam):
+        return results[bb] / results[lam] if bb in results and lam in results else None
     line = {
         "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": head_ms, "higher_is_better": True, "scaling": "weak",
@@ -406,11 +422,21 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
-                     "kernel": "tile_kernel<int64, rho=32, CA, lambda>"},
+                     "kernel": "ca_pipe_kernel<int64, rho=32, lambda, 2 stages, 8 warps>"},
         "clocks": sampler.summary(),
         "speedup_vs_bb": {
-            "ca_best_bb_over_lambda": (best_bb / head_ms) if best_bb else None,
-            "ca_paper_bb_percell_over_lambda": (best_bb_percell / head_ms) if best_bb_percell else None,
+            "ca_i64_best_bb_over_lambda": (best_bb / head_ms) if best_bb else None,
+            "ca_i64_paper_bb_percell_over_lambda": (best_bb_percell / head_ms) if best_bb_percell else None,
+            "ca_u8_bb_over_lambda": ratio("ca_bb_tile_rho32_u8", "ca_lambda_tile_rho32_u8"),
+            "ca_bit_bb_over_lambda": ratio("ca_bb_tile_rho32_bit", "ca_lambda_tile_rho32_bit"),
+            "sw_best_bb_over_lambda": ratio("sw_bb_tile_rho32", "sw_lambda_tile_rho32"),
+            "rd_best_bb_over_lambda": ratio("rd_bb_tile_rho32", "rd_lambda_tile_rho32"),
+        },
+        "line_granular_floor": {
+            "note": "B200 reads whole 128 B lines (probe: tools/probe_dram3.cu); int64 lines holding "
+                    "a member: 2^4*3^12 x 128 B = 1088.4 MB read + 612.2 MB sector writes per step",
+            "hw_min_bytes_per_step": 1088391168 + 612220032,
+            "achieved_GBps_vs_hw_min": (1088391168 + 612220032) / (head_ms * 1e-3) / 1e9,
         },
         "workloads_ms": results,
         "workloads_cells_per_s": {k: cells(k) for k in results},

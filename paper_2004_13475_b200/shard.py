@@ -164,8 +164,15 @@ class ShardPlan:
             scatter = _kernel_scatter
         send = gather(flat, sidx)
         recv = torch.empty(int(sum(self.recv_counts)), dtype=grid.dtype, device=grid.device)
-        dist.all_to_all_single(recv, send, output_split_sizes=self.recv_counts,
-                               input_split_sizes=self.send_counts, group=group)
+        if grid.is_cuda and dist.get_backend(group) == "gloo":
+            # ranks sharing one GPU (test setups): stage the tiny halo through host memory
+            send_h, recv_h = send.cpu(), recv.cpu()
+            dist.all_to_all_single(recv_h, send_h, output_split_sizes=self.recv_counts,
+                                   input_split_sizes=self.send_counts, group=group)
+            recv.copy_(recv_h)
+        else:
+            dist.all_to_all_single(recv, send, output_split_sizes=self.recv_counts,
+                                   input_split_sizes=self.send_counts, group=group)
         scatter(flat, ridx, recv)
 
 

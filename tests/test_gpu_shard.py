@@ -1,0 +1,74 @@
+"""The multi-GPU CA path on one B200: world_size ranks (gloo, all on cuda:0) each
+launch only their contiguous chunk of λ tiles (nbb_config.shard_begin/count) on a
+full replica, exchange the halo cells with the library's gather/scatter kernels
+before every step, and together reproduce the single-domain oracle exactly."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from _oracle import orc_ca, orc_random_member_grid
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, r, rho, steps, cell_width, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2004_13475_b200 import device as dev
+    from paper_2004_13475_b200 import nbb
+    from paper_2004_13475_b200.shard import ShardPlan, lambda_blocks
+    n = 1 << r
+    plan = ShardPlan(r=r, rho=rho, world=world, rank=rank)
+    g = orc_random_member_grid(r, 4321, 2)
+    dt = torch.int64 if cell_width == 8 else torch.uint8
+    a = torch.from_numpy(g).to(dt).cuda()
+    b = torch.zeros_like(a)
+    c = nbb.DispatchConfig(r=r, rho=rho, max_cells=n * n, cell_width=cell_width)
+    lc = plan.local_config(c)
+    s = torch.cuda.current_stream().cuda_stream
+    for _ in range(steps):
+        plan.exchange_halo(a, dist)
+        dev.ca_step_dev(lc, a.data_ptr(), b.data_ptr(), nbb.CaRule(), s)
+        a, b = b, a
+    torch.cuda.synchronize()
+    own = np.zeros((n, n), dtype=bool)
+    t = np.arange(plan.begin, plan.begin + plan.count, dtype=np.int64)
+    bx, by = lambda_blocks(t, plan.W)
+    for x0, y0 in zip(bx * rho, by * rho):
+        own[y0:y0 + rho, x0:x0 + rho] = True
+    mine = torch.where(torch.from_numpy(own), a.cpu().to(torch.int64), torch.zeros(n, n, dtype=torch.int64))
+    dist.all_reduce(mine)
+    if rank == 0:
+        q.put(mine.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,r,rho,cw", [(2, 10, 32, 8), (3, 10, 16, 8), (2, 11, 32, 1)])
+def test_sharded_ca_on_gpu(world, r, rho, cw):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    steps = 6
+    procs = [ctx.Process(target=_worker, args=(i, world, port, r, rho, steps, cw, q)) for i in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = orc_ca(r, orc_random_member_grid(r, 4321, 2), steps)
+    assert np.array_equal(got, want)
