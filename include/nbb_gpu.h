@@ -96,7 +96,17 @@ typedef struct nbb_config {
      * chunk, as the reference splits ordinals over workers (dispatch.cpp:419-427). */
     uint64_t shard_begin;
     uint64_t shard_count;
+    uint32_t flags;     /* NBB_FLAG_* */
+    uint32_t reserved0;
 } nbb_config;
+
+/* nbb_config.flags
+ * NBB_FLAG_OUT_ZEROED: the caller guarantees that the non-member cells of the host
+ *   out_grid are already 0 (e.g. a reused output buffer, or one allocated zeroed); host
+ *   calls may then write member cells only. With pinned (cudaHostAlloc/-Register)
+ *   buffers the kernels then move only member sectors over PCIe (zero-copy) instead of
+ *   the whole n*n grid. Without the flag out_grid is always written in full. */
+#define NBB_FLAG_OUT_ZEROED 1u
 
 /* WorkReport (dispatch.hpp:44-61) */
 typedef struct nbb_report {

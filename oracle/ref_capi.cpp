@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cstring>
 #include <new>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -349,6 +350,17 @@ int ref_csv_row(const nbb_report* report, char* buf, size_t len) {
         const auto row = to_report(*report).csv_row();
         if (row.size() + 1 > len) throw std::length_error("csv buffer too small");
         std::memcpy(buf, row.c_str(), row.size() + 1);
+    });
+}
+
+// std::ostream << double, as nbbmap bench formats the quotient column (nbbmap.cpp:611-613)
+int ref_format_double(double v, char* buf, size_t len) {
+    return guarded([&] {
+        std::ostringstream s;
+        s << v;
+        const auto str = s.str();
+        if (str.size() + 1 > len) throw std::length_error("buffer too small");
+        std::memcpy(buf, str.c_str(), str.size() + 1);
     });
 }
 

@@ -59,7 +59,12 @@ class NbbConfig(Structure):
         ("max_cells", c_uint64),
         ("shard_begin", c_uint64),
         ("shard_count", c_uint64),
+        ("flags", ctypes.c_uint32),
+        ("reserved0", ctypes.c_uint32),
     ]
+
+
+FLAG_OUT_ZEROED = 1
 
 
 class NbbReport(Structure):

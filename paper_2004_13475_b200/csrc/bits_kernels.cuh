@@ -130,7 +130,7 @@ __global__ void pack_bits_kernel(const long long* g64, uint32_t* bits, int64_t n
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const uint32_t nib = (memb >> (4 * q)) & 0xFu;
-                if (nib) w |= (alive4_i64(ldg_sector(g64 + (int64_t)Y * n + X + 4 * q)) & nib) << (4 * q);
+                if (nib) w |= (alive4_i64(ld_sector(g64 + (int64_t)Y * n + X + 4 * q)) & nib) << (4 * q);
             }
         }
         bits[i] = w;

@@ -507,6 +507,18 @@ int sanitize(const Launch& L, void* d_grid, int cell_width, cudaStream_t s) {
 }
 
 // bytes of an n x n grid of cw-byte cells (cw = 0: 1-bit packed, 32-bit words per row)
+// Device-usable address of a pinned (page-locked, mapped) host buffer, or nullptr for
+// pageable memory (then the whole grid is staged with cudaMemcpy).
+void* mapped_host_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (p == nullptr || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (a.type != cudaMemoryTypeHost || a.devicePointer == nullptr) return nullptr;
+    return a.devicePointer;
+}
+
 size_t grid_bytes(const Launch& L, int cw) {
     const size_t n = (size_t)L.plan.n;
     if (cw == 0) return n * std::max<size_t>(1, n / 32) * 4;
@@ -803,31 +815,39 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
         return NBB_OK;
     }
     const int cw = cfg->cell_width;
-    void *d64, *da, *db;
-    NBB_CHECK(device_buffer(*L.ctx, 0, b64, &d64));
-    NBB_CUDA(cudaMemcpyAsync(d64, initial, b64, cudaMemcpyHostToDevice, L.stream));
+    const int blocks = L.ctx->sms * 8;
+    // zero-copy: pinned host buffers are read/written in place, member sectors only
+    const long long* h_in = (const long long*)mapped_host_ptr(initial);
+    long long* h_out = (cfg->flags & NBB_FLAG_OUT_ZEROED) ? (long long*)mapped_host_ptr(out_grid) : nullptr;
+    void *d64 = nullptr, *da, *db;
     if (cw == 8) {
-        da = d64;
+        NBB_CHECK(device_buffer(*L.ctx, 0, b64, &da));
         NBB_CHECK(device_buffer(*L.ctx, 1, b64, &db));
-        NBB_CHECK(sanitize(L, da, 8, L.stream));
+        if (h_in) {
+            NBB_CUDA(cudaMemsetAsync(da, 0, b64, L.stream));
+            copy_member_sectors_kernel<<<blocks, 256, 0, L.stream>>>(h_in, (long long*)da, L.plan.n, 1);
+            NBB_CUDA(cudaGetLastError());
+        } else {
+            NBB_CUDA(cudaMemcpyAsync(da, initial, b64, cudaMemcpyHostToDevice, L.stream));
+            NBB_CHECK(sanitize(L, da, 8, L.stream));
+        }
         NBB_CUDA(cudaMemsetAsync(db, 0, b64, L.stream));
-    } else if (cw == 1) {
-        const size_t b8 = grid_bytes(L, 1);
-        NBB_CHECK(device_buffer(*L.ctx, 1, b8, &da));
-        NBB_CHECK(device_buffer(*L.ctx, 2, b8, &db));
-        pack_alive_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)d64,
-                                                                (unsigned char*)da, L.plan.n);
+    } else {
+        const size_t bs = grid_bytes(L, cw);
+        NBB_CHECK(device_buffer(*L.ctx, 1, bs, &da));
+        NBB_CHECK(device_buffer(*L.ctx, 2, bs, &db));
+        const long long* src64 = h_in;
+        if (!src64) {  // stage the whole grid in HBM
+            NBB_CHECK(device_buffer(*L.ctx, 0, b64, &d64));
+            NBB_CUDA(cudaMemcpyAsync(d64, initial, b64, cudaMemcpyHostToDevice, L.stream));
+            src64 = (const long long*)d64;
+        }
+        if (cw == 1)
+            pack_alive_kernel<<<blocks, 256, 0, L.stream>>>(src64, (unsigned char*)da, L.plan.n);
+        else
+            pack_bits_kernel<<<blocks, 256, 0, L.stream>>>(src64, (uint32_t*)da, L.plan.n);
         NBB_CUDA(cudaGetLastError());
-        NBB_CUDA(cudaMemsetAsync(db, 0, b8, L.stream));
-    } else {  // 1-bit packed: sanitize the int64 copy (unpack writes member sectors only)
-        const size_t bb = grid_bytes(L, 0);
-        NBB_CHECK(device_buffer(*L.ctx, 1, bb, &da));
-        NBB_CHECK(device_buffer(*L.ctx, 2, bb, &db));
-        NBB_CHECK(sanitize(L, d64, 8, L.stream));
-        pack_bits_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)d64,
-                                                               (uint32_t*)da, L.plan.n);
-        NBB_CUDA(cudaGetLastError());
-        NBB_CUDA(cudaMemsetAsync(db, 0, bb, L.stream));
+        NBB_CUDA(cudaMemsetAsync(db, 0, bs, L.stream));
     }
     for (int s = 0; s < steps; ++s) {
         Timer t(cfg->timing != 0, L.stream);
@@ -836,14 +856,25 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
         if (per_step) fill_report(cfg, &per_step[s], us);
         std::swap(da, db);
     }
-    if (cw == 1) {
-        unpack_alive_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const unsigned char*)da,
-                                                                  (long long*)d64, L.plan.n);
+    if (h_out) {  // member sectors straight into the (zeroed) pinned host grid
+        if (cw == 8)
+            copy_member_sectors_kernel<<<blocks, 256, 0, L.stream>>>((const long long*)da, h_out, L.plan.n, 0);
+        else if (cw == 1)
+            unpack_alive_kernel<<<blocks, 256, 0, L.stream>>>((const unsigned char*)da, h_out, L.plan.n, 1);
+        else
+            unpack_bits_kernel<<<blocks, 256, 0, L.stream>>>((const uint32_t*)da, h_out, L.plan.n);
         NBB_CUDA(cudaGetLastError());
-        da = d64;
-    } else if (cw == 0) {
-        unpack_bits_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const uint32_t*)da,
-                                                                 (long long*)d64, L.plan.n);
+        NBB_CUDA(cudaStreamSynchronize(L.stream));
+        return NBB_OK;
+    }
+    if (cw != 8) {  // materialise the full int64 grid (non-members 0) in HBM
+        NBB_CHECK(device_buffer(*L.ctx, 0, b64, &d64));
+        NBB_CUDA(cudaMemsetAsync(d64, 0, b64, L.stream));
+        if (cw == 1)
+            unpack_alive_kernel<<<blocks, 256, 0, L.stream>>>((const unsigned char*)da, (long long*)d64,
+                                                              L.plan.n, 1);
+        else
+            unpack_bits_kernel<<<blocks, 256, 0, L.stream>>>((const uint32_t*)da, (long long*)d64, L.plan.n);
         NBB_CUDA(cudaGetLastError());
         da = d64;
     }

@@ -84,13 +84,15 @@ __global__ void pack_alive_kernel(const long long* g64, unsigned char* g8, int64
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const uint32_t nib = (memb >> (4 * q)) & 0xFu;
-            if (nib) bits |= (alive4_i64(ldg_sector(g64 + (int64_t)Y * n + X + 4 * q)) & nib) << (4 * q);
+            if (nib) bits |= (alive4_i64(ld_sector(g64 + (int64_t)Y * n + X + 4 * q)) & nib) << (4 * q);
         }
         stg_sector(g8 + (int64_t)Y * n + X, expand32_u8(bits));
     }
 }
 
-__global__ void unpack_alive_kernel(const unsigned char* g8, long long* g64, int64_t n) {
+// members_only: skip 32-cell runs without members (their int64 cells must already be 0)
+__global__ void unpack_alive_kernel(const unsigned char* g8, long long* g64, int64_t n,
+                                    int members_only = 0) {
     const uint64_t runs_per_row = (uint64_t)(n >= 32 ? n / 32 : 1);
     const uint64_t total = (uint64_t)n * runs_per_row;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -107,10 +109,45 @@ __global__ void unpack_alive_kernel(const unsigned char* g8, long long* g64, int
         }
         const uint32_t Yc = nm1 - Y;
         const uint32_t memb = ((X & Yc) == 0u) ? submask_bits((~Yc) & 31u) : 0u;
+        if (members_only && !memb) continue;
         const uint32_t bits = memb ? (alive32_u8(ldg_sector(g8 + (int64_t)Y * n + X)) & memb) : 0u;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-            stg_sector(g64 + (int64_t)Y * n + X + 4 * q, expand4_i64((bits >> (4 * q)) & 0xFu));
+            if (!members_only || ((memb >> (4 * q)) & 0xFu))
+                stg_sector(g64 + (int64_t)Y * n + X + 4 * q, expand4_i64((bits >> (4 * q)) & 0xFu));
+    }
+}
+
+// ---- member-sector copy (zero-copy host transfers) -------------------------------
+// Copy the member sectors of an int64 grid, one warp per row: row y's member sectors
+// are s ⊆ (y >> 2), its member cells inside a sector are i ⊆ (y & 3). `mask` zeroes
+// the non-member cells of each copied sector (sanitizes an arbitrary source). Either
+// side may be mapped pinned host memory: only 2^popc(y>>2) sectors per row cross PCIe.
+__device__ __forceinline__ uint32_t pdep32(uint32_t j, uint32_t m);
+__global__ void copy_member_sectors_kernel(const long long* src, long long* dst, int64_t n, int mask) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (n < 4) {  // tiny grids: cell by cell
+        if (warp == 0 && lane == 0)
+            for (int64_t y = 0; y < n; ++y)
+                for (int64_t x = 0; x < n; ++x)
+                    if (gasket_member(x, y, n)) dst[y * n + x] = src[y * n + x];
+        return;
+    }
+    for (uint32_t y = warp; y < (uint32_t)n; y += nwarps) {
+        const uint32_t m = y >> 2, cnt = 1u << __popc(m);
+        const uint32_t nib = submask_bits(y & 3u) & 0xFu;
+        for (uint32_t j = (uint32_t)lane; j < cnt; j += 32u) {
+            const int64_t off = (int64_t)y * n + 4 * (int64_t)pdep32(j, m);
+            Sector v = ld_sector(src + off);
+            if (mask) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (!((nib >> c) & 1u)) v.w[2 * c] = v.w[2 * c + 1] = 0u;
+            }
+            stg_sector(dst + off, v);
+        }
     }
 }
 

@@ -218,6 +218,7 @@ class DispatchConfig:
     device: int = 0
     shard_begin: int = 0
     shard_count: int = 0  # 0 = every block ordinal of the plan
+    flags: int = 0        # _abi.FLAG_* (e.g. FLAG_OUT_ZEROED)
 
     def to_c(self) -> _abi.NbbConfig:
         c = _abi.NbbConfig()
@@ -235,6 +236,7 @@ class DispatchConfig:
         c.max_cells = self.max_cells
         c.shard_begin = self.shard_begin
         c.shard_count = self.shard_count
+        c.flags = self.flags
         return c
 
     def validate(self) -> None:                         # dispatch.cpp:50-114

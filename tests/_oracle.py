@@ -117,6 +117,7 @@ def ref_lib():
             "ref_csv_row": (c_int, [RP, c_char_p, c_size_t]),
             "ref_csv_header": (c_char_p, []),
             "ref_compact_store": (c_int, [SP, c_int32, c_void_p, c_void_p]),
+            "ref_format_double": (c_int, [c_double, c_char_p, c_size_t]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

@@ -136,6 +136,57 @@ def main() -> None:
     pins["lambda_examples"] = [[2, 1, 1, 0, 3], [2, 2, 2, 3, 3], [0, 0, 0, 0, 0]]
     out["pins"] = pins
 
+    # nbbmap bench CSV (tools/nbbmap.cpp:530-625) rebuilt from the reference library's
+    # own reports (the CLI binary cannot be built: vendor/CLI11.hpp is absent); the
+    # quotient is formatted by C++ std::ostream (ref_format_double)
+    def fmt(q):
+        buf = ctypes.create_string_buffer(64)
+        assert ref_lib().ref_format_double(q, buf, 64) == 0
+        return buf.value.decode()
+
+    def cli_bench(workload, rmin, rmax, rhos, mode="both", strategy="BoundingSubBoxes", backend="Direct",
+                  seed=1, steps=4):
+        lines = ["# spec,r,rho,mode,strategy,backend,blocks,threads,active,wasted,map_ops,micros"
+                 ",workload,quotient"]
+        modes = [m for m, k in ((MapMode.BoundingBox, "bb"), (MapMode.Lambda, "lambda"))
+                 if mode in (k, "both")]
+        for r in range(rmin, rmax + 1):
+            rdg = ref_random_member_grid(r, seed + r, 100) if workload == "rd" else None
+            cag = ref_random_member_grid(r, seed + r, 2) if workload == "ca" else None
+            for rho in rhos:
+                for m in modes:
+                    c = cfg(r=r, rho=rho, mode=m, strategy=IntraBlockStrategy[strategy],
+                            backend=LambdaBackend.Direct if m == MapMode.BoundingBox
+                            else LambdaBackend[backend])
+                    c.max_cells = 1 << 24
+                    if ref_validate(c)[0]:
+                        continue
+                    if workload == "sw":
+                        rep = ref_single_write(c)[2]
+                    elif workload == "rd":
+                        rep = ref_reduction(c, rdg, r)[2]
+                    else:
+                        rep = ref_ca(c, cag, steps)[2][0]
+                    n = 1 << r
+                    lines.append(f"{ref_csv_row(rep)},{workload},{fmt(n * n / rep.threads_launched)}")
+        return "\n".join(lines) + "\n"
+
+    S, U, L = "BoundingSubBoxes", "FurtherUnrolling", "SharedLookupTable"
+    out["cli_bench"] = [
+        {"args": "bench --workload sw --rmin 0 --rmax 8 --rho 1 --mode both",
+         "csv": cli_bench("sw", 0, 8, [1], strategy=S)},
+        {"args": "bench --workload rd --rmin 2 --rmax 6 --rho 1,2,4 --mode both --seed 7",
+         "csv": cli_bench("rd", 2, 6, [1, 2, 4], strategy=S, seed=7)},
+        {"args": "bench --workload ca --rmin 2 --rmax 6 --rho 1,2,4 --mode both --seed 7",
+         "csv": cli_bench("ca", 2, 6, [1, 2, 4], strategy=S, seed=7)},
+        {"args": "bench --workload rd --rmin 2 --rmax 6 --rho 1,2,4 --mode both --strategy unroll --seed 9",
+         "csv": cli_bench("rd", 2, 6, [1, 2, 4], strategy=U, seed=9)},
+        {"args": "bench --workload ca --rmin 3 --rmax 5 --steps 3 --seed 4",
+         "csv": cli_bench("ca", 3, 5, [1], strategy=S, seed=4, steps=3)},
+        {"args": "bench --workload sw --rmin 2 --rmax 7 --rho 2,4,8 --mode lambda --strategy lut --backend mma2",
+         "csv": cli_bench("sw", 2, 7, [2, 4, 8], mode="lambda", strategy=L, backend="MmaV2")},
+    ]
+
     path = os.path.join(HERE, "golden.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)

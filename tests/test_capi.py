@@ -176,3 +176,24 @@ def test_cpp_shim_compiles():
     r = subprocess.run([out, "--host-only"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "sierpinski,8,1,lambda,subbox,direct,6561,6561,6561,0,59049,0" in r.stdout
+
+
+def test_nbbmap_quotient_format_matches_cpp():
+    """nbbmap prints the quotient with std::ostream defaults (%g, 6 significant)."""
+    from _oracle import ref_available, ref_lib
+    from paper_2004_13475_b200.nbbmap import _fmt_double
+    if not ref_available():
+        pytest.skip("reference library not built")
+    buf = ctypes.create_string_buffer(64)
+    for r in range(0, 24):
+        for rho in (1, 2, 4, 8, 16, 32):
+            for q in (4 ** r / 3 ** r, 4 ** r / (rho * rho * 3 ** max(r - 1, 0)), 1.0, 100.0 / 81.0):
+                assert ref_lib().ref_format_double(q, buf, 64) == 0
+                assert _fmt_double(q) == buf.value.decode(), q
+
+
+def test_nbbmap_cli_errors():
+    from paper_2004_13475_b200 import nbbmap
+    assert nbbmap.main(["bench", "--workload", "xx"]) == 2
+    assert nbbmap.main(["bench", "--rmin", "3", "--rmax", "2"]) == 2
+    assert nbbmap.main(["bench", "--rmin", "13", "--rmax", "13"]) == 3

@@ -130,6 +130,33 @@ def test_ca_bit_packed_state(golden, r):
         nbb.run_ca(cfg(r=r, rho=16, cell_width=0), grid(init, r), 1)
 
 
+@pytest.mark.parametrize("cw", [8, 1, 0])
+def test_ca_host_buffers_pinned_zero_copy(cw):
+    """nbb_gpu_ca on pinned host buffers: member sectors move in place over PCIe; with
+    FLAG_OUT_ZEROED only member cells of out are written; without it out is written whole."""
+    torch = pytest.importorskip("torch")
+    import ctypes
+    r, n = 11, 1 << 11
+    init = with_garbage(orc_random_member_grid(r, 77, 2), r, seed=5)
+    want = orc_ca(r, init, 5)
+    lib = _abi.load()
+    h_in = torch.from_numpy(init.copy()).pin_memory()
+    for flags, out_init in ((_abi.FLAG_OUT_ZEROED, 0), (0, 0), (0, 7)):
+        h_out = torch.full((n, n), out_init, dtype=torch.int64).pin_memory()
+        c = cfg(r=r, rho=32, cell_width=cw, flags=flags).to_c()
+        rc = lib.nbb_gpu_ca(ctypes.byref(c), ctypes.c_void_p(h_in.data_ptr()), r, 5, 8, 12,
+                            ctypes.c_void_p(h_out.data_ptr()), None)
+        assert rc == 0, lib.nbb_gpu_last_error()
+        assert np.array_equal(h_out.numpy(), want), (cw, flags, out_init)
+    assert np.array_equal(h_in.numpy(), init)  # the input is never written
+    # in place (out aliases the pinned input): full write, garbage cleared
+    h_io = torch.from_numpy(init.copy()).pin_memory()
+    c = cfg(r=r, rho=32, cell_width=cw).to_c()
+    assert lib.nbb_gpu_ca(ctypes.byref(c), ctypes.c_void_p(h_io.data_ptr()), r, 5, 8, 12,
+                          ctypes.c_void_p(h_io.data_ptr()), None) == 0
+    assert np.array_equal(h_io.numpy(), want)
+
+
 def test_ca_semantics_probes():
     """App. B.4: steps=0 returns the input unchanged (garbage included); alive means != 0."""
     r = 6
@@ -279,6 +306,24 @@ def test_device_resident_api():
     xy = torch.empty((3 ** 10, 2), dtype=torch.int32, device="cuda")
     dev.lambda_coords_dev(c, 10, xy.data_ptr(), 4, s)
     assert np.array_equal(xy.cpu().numpy().astype(np.int64), orc_lambda_coords(10))
+
+
+def test_nbbmap_bench_csv_byte_identical(golden, tmp_path):
+    """`nbbmap bench` over the GPU path prints the reference CLI's CSV bytes
+    (tools/nbbmap.cpp:530-625; test_cli.cpp:151-175), for any worker count."""
+    from paper_2004_13475_b200 import nbbmap
+    for case in golden["cli_bench"]:
+        for extra in ([], ["--workers", "4"]):
+            out = tmp_path / "b.csv"
+            rc = nbbmap.main(case["args"].split() + extra + ["--out", str(out)])
+            assert rc == 0, case["args"]
+            assert out.read_text() == case["csv"], (case["args"], extra)
+    out = tmp_path / "t.csv"
+    assert nbbmap.main("bench --workload ca --rmin 10 --rmax 10 --rho 32 --timing --out".split() +
+                       [str(out)]) == 0
+    rows = out.read_text().splitlines()[1:]
+    assert len(rows) == 2 and all(int(r.split(",")[11]) >= 0 for r in rows)
+    assert nbbmap.main("bench --rmin 13 --rmax 13".split()) == 3  # --max-cells budget
 
 
 def test_cpp_shim_on_gpu():
