@@ -68,6 +68,55 @@ __host__ __device__ __forceinline__ bool gasket_member(int64_t x, int64_t y, int
     return x >= 0 && y >= 0 && x < n && y < n && (x & (n - 1 - y)) == 0;
 }
 
+
+// ---- generic NBB specs (vicsek, carpet, …) ---------------------------------------
+// Table-driven descriptor for the per-cell kernels; the gasket keeps the bit-test and
+// closed-form fast paths (`gasket` = 1).
+struct DevSpec {
+    int k, s;
+    int ox[9], oy[9];
+    int replica_at[9];  // step-box cell cy*s + cx -> replica index, -1 if empty
+    int gasket;
+};
+
+// is_member (fractal.cpp:194-214): descend the replica chain; false outside the embedding
+__device__ __forceinline__ bool member_spec(const DevSpec& sp, int64_t x, int64_t y, int level) {
+    int64_t n = 1;
+    for (int i = 0; i < level; ++i) n *= sp.s;
+    if (sp.gasket) return gasket_member(x, y, n);
+    if (x < 0 || y < 0 || x >= n || y >= n) return false;
+    int64_t scale = n / sp.s;
+    for (int mu = level; mu >= 1; --mu) {
+        const int cx = (int)(x / scale), cy = (int)(y / scale);
+        if (sp.replica_at[cy * sp.s + cx] < 0) return false;
+        x -= cx * scale;
+        y -= cy * scale;
+        scale /= sp.s;
+    }
+    return true;
+}
+
+// lambda_map (block_map.cpp:77-111): odd levels consume base-k digits of ωx, even of ωy
+__device__ __forceinline__ void lambda_spec(const DevSpec& sp, uint64_t ox, uint64_t oy, int level,
+                                            int64_t& x, int64_t& y) {
+    int64_t px = 0, py = 0, scale = 1;
+    for (int mu = 1; mu <= level; ++mu) {
+        int beta;
+        if (mu & 1) {
+            beta = (int)(ox % (uint64_t)sp.k);
+            ox /= (uint64_t)sp.k;
+        } else {
+            beta = (int)(oy % (uint64_t)sp.k);
+            oy /= (uint64_t)sp.k;
+        }
+        px += sp.ox[beta] * scale;
+        py += sp.oy[beta] * scale;
+        scale *= sp.s;
+    }
+    x = px;
+    y = py;
+}
+
 // ---- λ(ω) ------------------------------------------------------------------
 // LUT over 6 base-3 digits: entry v (< 729) = X6(v) | Y6(v) << 16, X6/Y6 < 2^11.
 __constant__ uint32_t c_xy729[729];

@@ -126,9 +126,33 @@ int device_buffer(DeviceCtx& c, int slot, size_t bytes, void** out) {
     return NBB_OK;
 }
 
+DevSpec dev_spec(const nbb_spec& s) {
+    DevSpec d;
+    std::memset(&d, 0, sizeof(d));
+    d.k = s.k;
+    d.s = s.s;
+    for (int i = 0; i < 9; ++i) {
+        d.ox[i] = i < s.k ? s.offset_x[i] : 0;
+        d.oy[i] = i < s.k ? s.offset_y[i] : 0;
+        d.replica_at[i] = -1;
+    }
+    for (int i = 0; i < s.k && i < 9; ++i) d.replica_at[s.offset_y[i] * s.s + s.offset_x[i]] = i;
+    d.gasket = nbbhost::is_gasket(s) ? 1 : 0;
+    return d;
+}
+
 int local_table(DeviceCtx& c, const nbb_spec& s, int edge, const int16_t** out) {
     int l = 0;
     while ((1 << l) < edge) ++l;
+    if (!nbbhost::is_gasket(s)) {  // generic specs: refill a scratch table every call
+        static thread_local int16_t* scratch = nullptr;
+        if (!scratch) NBB_CUDA(cudaMalloc(&scratch, 32 * 32 * 2 * sizeof(int16_t)));
+        std::vector<int16_t> h((size_t)edge * edge * 2);
+        nbbhost::local_cell_table(s, edge, h.data());
+        NBB_CUDA(cudaMemcpy(scratch, h.data(), h.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
+        *out = scratch;
+        return NBB_OK;
+    }
     if (!c.lut[l]) {
         std::vector<int16_t> h((size_t)edge * edge * 2);
         nbbhost::local_cell_table(s, edge, h.data());
@@ -176,6 +200,7 @@ struct Launch {
 
 bool tile_supported(const nbb_config& c, int op, int cell_width) {
     if (c.kernel == NBB_KERNEL_PERCELL) return false;
+    if (!nbbhost::is_gasket(c.spec)) return false;  // tile kernels use the gasket bit structure
     if (c.mode == NBB_MODE_LAMBDA &&
         (c.strategy != NBB_STRATEGY_SUBBOX || c.backend != NBB_BACKEND_DIRECT))
         return false;
@@ -393,6 +418,8 @@ int launch_percell(const Launch& L, const void* src, void* dst, uint32_t birth, 
     a.lut = nullptr;
     a.birth = birth;
     a.survive = survive;
+    a.r = c.r;
+    a.spec = dev_spec(c.spec);
     if (c.mode == NBB_MODE_LAMBDA && c.strategy == NBB_STRATEGY_LUT)
         NBB_CHECK(local_table(*L.ctx, c.spec, L.plan.edge, &a.lut));
     if (c.mode == NBB_MODE_BB)
@@ -473,10 +500,16 @@ int launch_op(const Launch& L, int op, const void* src, void* dst, unsigned long
                        : launch_percell<unsigned char, OP_CA>(L, src, dst, birth, survive);
 }
 
-int prepare(const nbb_config* cfg, int op, Launch* L, bool need_budget) {
+// gasket_only: layout kernels (sanitize/pack/unpack/scatter) that use the gasket bit test
+int prepare(const nbb_config* cfg, int op, Launch* L, bool need_budget, bool gasket_only = false) {
     if (cfg == nullptr) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_TRY(nbbhost::validate_spec(cfg->spec));
     NBB_TRY(nbbhost::validate(*cfg));
-    NBB_TRY(nbbhost::require_gasket(cfg->spec));
+    if (gasket_only) NBB_TRY(nbbhost::require_gasket(cfg->spec));
+    if (!nbbhost::is_gasket(cfg->spec) && cfg->cell_width != 8)
+        return fail(NBB_ERR_INVALID_ARGUMENT,
+                    "uint8 and 1-bit CA states run on the sierpinski gasket only; use cell_width 8 for '" +
+                        std::string(cfg->spec.name) + "'");
     if (need_budget) NBB_TRY(nbbhost::member_mask_budget(cfg->spec, cfg->r, cfg->max_cells));
     L->cfg = cfg;
     L->op = op;
@@ -496,7 +529,10 @@ void fill_report(const nbb_config* cfg, nbb_report* r, uint64_t micros) {
 
 int sanitize(const Launch& L, void* d_grid, int cell_width, cudaStream_t s) {
     const int blocks = L.ctx->sms * 8;
-    if (cell_width == 8)
+    if (!nbbhost::is_gasket(L.cfg->spec))
+        sanitize_generic_kernel<<<blocks, 256, 0, s>>>(dev_spec(L.cfg->spec), (long long*)d_grid,
+                                                       L.plan.n, L.cfg->r);
+    else if (cell_width == 8)
         sanitize_kernel<long long><<<blocks, 256, 0, s>>>((long long*)d_grid, L.plan.n, 0);
     else if (cell_width == 1)
         sanitize_kernel<unsigned char><<<blocks, 256, 0, s>>>((unsigned char*)d_grid, L.plan.n, 0);
@@ -675,13 +711,13 @@ int nbb_gpu_ca_step_dev(const nbb_config* cfg, const void* d_src, void* d_dst, u
 
 int nbb_gpu_sanitize_dev(const nbb_config* cfg, void* d_grid, void* stream) {
     Launch L;
-    NBB_CHECK(prepare(cfg, OP_CA, &L, false));
+    NBB_CHECK(prepare(cfg, OP_CA, &L, false, true));
     return sanitize(L, d_grid, cfg->cell_width, (cudaStream_t)stream);
 }
 
 int nbb_gpu_pack_alive_dev(const nbb_config* cfg, const void* d64, void* d8, void* stream) {
     Launch L;
-    NBB_CHECK(prepare(cfg, OP_CA, &L, false));
+    NBB_CHECK(prepare(cfg, OP_CA, &L, false, true));
     if (cfg->cell_width == 0)
         pack_bits_kernel<<<L.ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>(
             (const long long*)d64, (uint32_t*)d8, L.plan.n);
@@ -694,7 +730,7 @@ int nbb_gpu_pack_alive_dev(const nbb_config* cfg, const void* d64, void* d8, voi
 
 int nbb_gpu_unpack_alive_dev(const nbb_config* cfg, const void* d8, void* d64, void* stream) {
     Launch L;
-    NBB_CHECK(prepare(cfg, OP_CA, &L, false));
+    NBB_CHECK(prepare(cfg, OP_CA, &L, false, true));
     if (cfg->cell_width == 0)  // writes member sectors only: d64's non-member cells must be 0
         unpack_bits_kernel<<<L.ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>(
             (const uint32_t*)d8, (long long*)d64, L.plan.n);
@@ -708,7 +744,7 @@ int nbb_gpu_unpack_alive_dev(const nbb_config* cfg, const void* d8, void* d64, v
 int nbb_gpu_scatter_members_dev(const nbb_config* cfg, const void* d_values, void* d_grid,
                                 void* stream) {
     Launch L;
-    NBB_CHECK(prepare(cfg, OP_CA, &L, false));
+    NBB_CHECK(prepare(cfg, OP_CA, &L, false, true));
     scatter_members_kernel<<<L.ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>(
         (const long long*)d_values, (long long*)d_grid, L.plan.n);
     NBB_CUDA(cudaGetLastError());
@@ -718,8 +754,27 @@ int nbb_gpu_scatter_members_dev(const nbb_config* cfg, const void* d_values, voi
 int nbb_gpu_lambda_coords_dev(const nbb_config* cfg, int32_t level, void* d_xy, int32_t coord_bytes,
                               void* stream) {
     if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
-    NBB_TRY(nbbhost::require_gasket(cfg->spec));
+    NBB_TRY(nbbhost::validate_spec(cfg->spec));
     if (level < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "lambda: negative level");
+    if (!nbbhost::is_gasket(cfg->spec)) {  // table-driven digit loop for any NBB spec
+        DeviceCtx* gctx;
+        NBB_CHECK(ensure_device(cfg->device, &gctx));
+        int64_t gw, gh;
+        NBB_TRY(nbbhost::orthotope_dims(cfg->spec, level, &gw, &gh));
+        const uint64_t gtotal = (uint64_t)gw * (uint64_t)gh;
+        if (gtotal > (uint64_t(1) << 31)) return fail(NBB_ERR_RESOURCE, "orthotope too large for the map kernel");
+        const unsigned gb = (unsigned)std::min<uint64_t>((gtotal + 255) / 256, (uint64_t)gctx->sms * 16);
+        if (coord_bytes == 4)
+            lambda_map_generic_kernel<int32_t><<<std::max(1u, gb), 256, 0, (cudaStream_t)stream>>>(
+                dev_spec(cfg->spec), (int32_t*)d_xy, gtotal, (uint64_t)gw, level);
+        else if (coord_bytes == 8)
+            lambda_map_generic_kernel<long long><<<std::max(1u, gb), 256, 0, (cudaStream_t)stream>>>(
+                dev_spec(cfg->spec), (long long*)d_xy, gtotal, (uint64_t)gw, level);
+        else
+            return fail(NBB_ERR_INVALID_ARGUMENT, "coord_bytes must be 4 or 8");
+        NBB_CUDA(cudaGetLastError());
+        return NBB_OK;
+    }
     if (level > 17) return fail(NBB_ERR_RESOURCE, "lambda map kernel supports levels <= 17");
     if (coord_bytes != 4 && coord_bytes != 8)
         return fail(NBB_ERR_INVALID_ARGUMENT, "coord_bytes must be 4 or 8");
@@ -817,8 +872,10 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
     const int cw = cfg->cell_width;
     const int blocks = L.ctx->sms * 8;
     // zero-copy: pinned host buffers are read/written in place, member sectors only
-    const long long* h_in = (const long long*)mapped_host_ptr(initial);
-    long long* h_out = (cfg->flags & NBB_FLAG_OUT_ZEROED) ? (long long*)mapped_host_ptr(out_grid) : nullptr;
+    const bool gasket = nbbhost::is_gasket(cfg->spec);  // member-sector kernels need the gasket
+    const long long* h_in = gasket ? (const long long*)mapped_host_ptr(initial) : nullptr;
+    long long* h_out = (gasket && (cfg->flags & NBB_FLAG_OUT_ZEROED))
+                           ? (long long*)mapped_host_ptr(out_grid) : nullptr;
     void *d64 = nullptr, *da, *db;
     if (cw == 8) {
         NBB_CHECK(device_buffer(*L.ctx, 0, b64, &da));

@@ -24,6 +24,28 @@ Error require_gasket(const nbb_spec& s) {
     return {};
 }
 
+Error validate_spec(const nbb_spec& s) {
+    if (s.k < 2) return err(NBB_ERR_INVALID_ARGUMENT, "FractalSpec: replica count must be >= 2");
+    if (s.s < 2) return err(NBB_ERR_INVALID_ARGUMENT, "FractalSpec: scale factor must be >= 2");
+    if ((int64_t)s.k > (int64_t)s.s * s.s)
+        return err(NBB_ERR_INVALID_ARGUMENT, "FractalSpec: more replicas than step-box cells (k > s^2)");
+    if (s.k > NBB_MAX_REPLICAS)
+        return err(NBB_ERR_INVALID_ARGUMENT, "FractalSpec: at most 9 replicas on the GPU path");
+    bool seen[NBB_MAX_REPLICAS] = {};
+    for (int i = 0; i < s.k; ++i) {
+        const int x = s.offset_x[i], y = s.offset_y[i];
+        if (x < 0 || y < 0 || x >= s.s || y >= s.s)
+            return err(NBB_ERR_INVALID_ARGUMENT, "FractalSpec: replica offset (" + std::to_string(x) +
+                                                     "," + std::to_string(y) + ") outside [0," +
+                                                     std::to_string(s.s - 1) + "]");
+        if (seen[y * s.s + x])
+            return err(NBB_ERR_INVALID_ARGUMENT, "FractalSpec: replica offsets overlap at (" +
+                                                     std::to_string(x) + "," + std::to_string(y) + ")");
+        seen[y * s.s + x] = true;
+    }
+    return {};
+}
+
 Error checked_pow(uint64_t base, int exp, uint64_t* out) {
     if (exp < 0) return err(NBB_ERR_INVALID_ARGUMENT, "checked_pow: negative exponent");
     uint64_t r = 1;

@@ -23,6 +23,8 @@ inline Error err(int code, std::string msg) { return Error{code, std::move(msg)}
 
 bool is_gasket(const nbb_spec& s);
 Error require_gasket(const nbb_spec& s);
+// FractalSpec constructor checks (fractal.cpp:47-78)
+Error validate_spec(const nbb_spec& s);
 Error checked_pow(uint64_t base, int exp, uint64_t* out);    // fractal.cpp:12-25
 Error level_for_size(int64_t n, int s, int* level);          // fractal.cpp:27-45
 Error side_length(const nbb_spec& s, int level, int64_t* n); // fractal.cpp:165-171

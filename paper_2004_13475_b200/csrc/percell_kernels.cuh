@@ -36,7 +36,23 @@ struct PercellArgs {
     int64_t sub_w, sub_h;          // mma2 in-range sub-orthotope
     const int16_t* lut;            // lut strategy: edge*edge (x, y) pairs, -1 = spare
     uint32_t birth, survive;
+    int r;                         // scale level of the embedding
+    DevSpec spec;                  // fractal descriptor (gasket fast paths when spec.gasket)
 };
+
+// D(8x8) = A(8x4) * B(4x8) + C on the FP64 tensor pipe (DMMA), exact for integers < 2^53
+__device__ __forceinline__ void mma_f64_884(double (&d)[2], double a, double b, const double (&c)[2]) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};"
+                 : "=d"(d[0]), "=d"(d[1])
+                 : "d"(a), "d"(b), "d"(c[0]), "d"(c[1]));
+}
+
+// β_μ(ω) for any k (block_map.cpp:57-65)
+__device__ __forceinline__ uint32_t beta_digit_k(uint64_t ox, uint64_t oy, int mu, uint32_t k) {
+    uint64_t v = (mu & 1) ? ox : oy;
+    for (int i = 0; i < (mu + 1) / 2 - 1; ++i) v /= k;
+    return (uint32_t)(v % k);
+}
 
 __device__ __forceinline__ uint64_t flat_block() {
     return ((uint64_t)blockIdx.z * gridDim.y + blockIdx.y) * (uint64_t)gridDim.x + blockIdx.x;
@@ -116,17 +132,49 @@ __global__ void percell_kernel(PercellArgs a) {
     if (BB) {
         cx = (int64_t)gx * edge + tx;
         cy = (int64_t)gy * edge + ty;
-        active = real && gasket_member(cx, cy, n);
+        active = real && (a.spec.gasket ? gasket_member(cx, cy, n) : member_spec(a.spec, cx, cy, a.r));
     } else {
         if (BACKEND == NBB_BACKEND_MMA2 && ((int64_t)gx >= a.sub_w || (int64_t)gy >= a.sub_h)) {
             return;  // padding slot of the even-rounded cover: all spare (dispatch.cpp:321-325)
         }
         int64_t ox = 0, oy = 0;
         if (BACKEND == NBB_BACKEND_DIRECT) {
-            uint32_t lx, ly;
-            lambda_arith((uint32_t)gx, (uint32_t)gy, lx, ly);
-            ox = lx;
-            oy = ly;
+            if (a.spec.gasket) {
+                uint32_t lx, ly;
+                lambda_arith((uint32_t)gx, (uint32_t)gy, lx, ly);
+                ox = lx;
+                oy = ly;
+            } else {
+                lambda_spec(a.spec, gx, gy, a.map_level, ox, oy);
+            }
+        } else if (BACKEND == NBB_BACKEND_MMA1 && !a.spec.gasket) {
+            // s = 3: powers 3^(μ-1) are not bf16-exact beyond 3^5 — variant 1 on the FP64
+            // tensor pipe (DMMA m8n8k4): A row 0 = s^(μ-1), B cols 0/1 = τx/τy; K = 16 in 4 steps
+            if (tid < 32) {
+                const int g = tid >> 2, t = tid & 3;
+                double d[2] = {0.0, 0.0};
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const int kk = 4 * ks + t;  // level μ = kk + 1
+                    double av = 0.0, bv = 0.0;
+                    if (kk < a.map_level) {
+                        double p = 1.0;
+                        for (int i = 0; i < kk; ++i) p *= a.spec.s;
+                        if (g == 0) av = p;
+                        const uint32_t beta = beta_digit_k(gx, gy, kk + 1, (uint32_t)a.spec.k);
+                        if (g == 0) bv = a.spec.ox[beta];
+                        if (g == 1) bv = a.spec.oy[beta];
+                    }
+                    mma_f64_884(d, av, bv, d);
+                }
+                if (tid == 0) {
+                    s_origin[0] = (int64_t)d[0];
+                    s_origin[1] = (int64_t)d[1];
+                }
+            }
+            __syncthreads();
+            ox = s_origin[0];
+            oy = s_origin[1];
         } else {
             // warp 0 evaluates the encoding (mma.cpp:34-118) on the tensor pipe
             const int L = a.map_level;
@@ -197,7 +245,8 @@ __global__ void percell_kernel(PercellArgs a) {
         // intra-block strategy (dispatch.cpp:357-398)
         if (real) {
             if (STRATEGY == NBB_STRATEGY_SUBBOX) {
-                active = (tx & (edge - 1 - ty)) == 0;
+                active = a.spec.gasket ? (tx & (edge - 1 - ty)) == 0
+                                       : member_spec(a.spec, tx, ty, a.local_level);
                 if (BACKEND == NBB_BACKEND_MMA3) {
                     cx = (int64_t)sD[tx * 16 + ty];  // Dx[i=tx][j=ty] = ρ·λx + tx
                     cy = (int64_t)sB[tx * 16 + ty];
@@ -208,8 +257,16 @@ __global__ void percell_kernel(PercellArgs a) {
             } else if (STRATEGY == NBB_STRATEGY_UNROLL) {
                 const int64_t rank = ty * edge + tx;
                 if (rank < a.local_members) {
-                    uint32_t lx, ly;
-                    lambda_arith((uint32_t)(rank % a.local_w), (uint32_t)(rank / a.local_w), lx, ly);
+                    int64_t lx, ly;
+                    if (a.spec.gasket) {
+                        uint32_t ux, uy;
+                        lambda_arith((uint32_t)(rank % a.local_w), (uint32_t)(rank / a.local_w), ux, uy);
+                        lx = ux;
+                        ly = uy;
+                    } else {
+                        lambda_spec(a.spec, (uint64_t)(rank % a.local_w), (uint64_t)(rank / a.local_w),
+                                    a.local_level, lx, ly);
+                    }
                     cx = ox * edge + lx;
                     cy = oy * edge + ly;
                     active = true;
@@ -256,7 +313,9 @@ __global__ void percell_kernel(PercellArgs a) {
                 for (int dx = -1; dx <= 1; ++dx) {
                     if (dx == 0 && dy == 0) continue;
                     const int64_t nx = cx + dx, ny = cy + dy;
-                    if (gasket_member(nx, ny, n) && src[ny * n + nx] != (Cell)0) ++live;
+                    const bool m = a.spec.gasket ? gasket_member(nx, ny, n)
+                                                 : member_spec(a.spec, nx, ny, a.r);
+                    if (m && src[ny * n + nx] != (Cell)0) ++live;
                 }
             const bool alive = src[cy * n + cx] != (Cell)0;
             const uint32_t bit = 1u << live;

@@ -184,6 +184,28 @@ __global__ void scatter_members_kernel(const long long* values, long long* grid,
     }
 }
 
+// ---- generic specs -------------------------------------------------------------
+// zero the non-member cells (any NBB spec; one thread per cell)
+__global__ void sanitize_generic_kernel(DevSpec sp, long long* grid, int64_t n, int r) {
+    const uint64_t total = (uint64_t)n * (uint64_t)n;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (!member_spec(sp, (int64_t)(i % (uint64_t)n), (int64_t)(i / (uint64_t)n), r)) grid[i] = 0;
+    }
+}
+
+// λ map of a whole orthotope for any spec (table-driven digit loop)
+template <typename Coord>
+__global__ void lambda_map_generic_kernel(DevSpec sp, Coord* xy, uint64_t total, uint64_t gw, int level) {
+    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
+         o += (uint64_t)gridDim.x * blockDim.x) {
+        int64_t x, y;
+        lambda_spec(sp, o % gw, o / gw, level, x, y);
+        xy[2 * o] = (Coord)x;
+        xy[2 * o + 1] = (Coord)y;
+    }
+}
+
 // ---- halo pack / unpack (K4) for sharded CA -----------------------------------
 template <typename Cell>
 __global__ void gather_cells_kernel(const Cell* grid, const long long* idx, long long count, Cell* out) {

@@ -194,7 +194,7 @@ class FractalSpec:
         c.name = self.name.encode()[:31]
         c.k = self.k
         c.s = self.s
-        for i, (x, y) in enumerate(self.offsets):
+        for i, (x, y) in enumerate(self.offsets[:_abi.MAX_REPLICAS]):  # k > 9 fails validation
             c.offset_x[i] = x
             c.offset_y[i] = y
         return c

@@ -136,6 +136,24 @@ def main() -> None:
     pins["lambda_examples"] = [[2, 1, 1, 0, 3], [2, 2, 2, 3, 3], [0, 0, 0, 0, 0]]
     out["pins"] = pins
 
+    # generic NBB specs (vicsek k=5/s=3, carpet k=8/s=3): acceptance criterion 5 data
+    generic = {}
+    for name in ("vicsek", "carpet"):
+        spec = FractalSpec.builtin(name)
+        per = {}
+        for r in range(0, 6):
+            c = cfg(spec=spec, r=r, rho=1, mode=MapMode.BoundingBox)
+            rc, sw, _ = ref_single_write(c)
+            rdg = ref_random_member_grid(r, 17 + r, 100, spec)
+            cag = ref_random_member_grid(r, 71 + r, 2, spec)
+            rc, rd, _ = ref_reduction(c, rdg, r)
+            rc, ca2, _ = ref_ca(c, cag, 2)
+            per[str(r)] = {"sw_fnv": fnv1a64(sw), "rd_grid_fnv": fnv1a64(rdg), "rd_value": rd,
+                           "ca_grid_fnv": fnv1a64(cag), "ca2_fnv": fnv1a64(ca2),
+                           "lambda_fnv": fnv1a64(ref_lambda_coords(r, spec))}
+        generic[name] = per
+    out["generic_specs"] = generic
+
     # nbbmap bench CSV (tools/nbbmap.cpp:530-625) rebuilt from the reference library's
     # own reports (the CLI binary cannot be built: vendor/CLI11.hpp is absent); the
     # quotient is formatted by C++ std::ostream (ref_format_double)

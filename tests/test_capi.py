@@ -160,8 +160,15 @@ def test_invalid_config_rejected_before_device():
         nbb.run_reduction(_cfg(r=3), nbb.Grid(GASKET, 2))
     with pytest.raises(InvalidArgument, match="negative step count"):
         nbb.run_ca(_cfg(r=2), nbb.Grid(GASKET, 2), -1)
-    with pytest.raises(InvalidArgument, match="sierpinski gasket only"):
-        nbb.run_single_write(_cfg(spec=FractalSpec.vicsek(), r=2))
+    bad = FractalSpec("bad", 10, 3, tuple((i % 3, i // 3 % 3) for i in range(10)))
+    with pytest.raises(InvalidArgument, match="more replicas than step-box cells"):
+        nbb.run_single_write(_cfg(spec=bad, r=2))
+    dup = FractalSpec("dup", 2, 2, ((0, 0), (0, 0)))
+    with pytest.raises(InvalidArgument, match="overlap"):
+        nbb.run_single_write(_cfg(spec=dup, r=2))
+    with pytest.raises(InvalidArgument, match="1-bit CA states run on the sierpinski gasket only"):
+        nbb.run_ca(_cfg(spec=FractalSpec.vicsek(), r=2, cell_width=1),
+                   nbb.Grid(FractalSpec.vicsek(), 2), 1)
 
 
 def test_cpp_shim_compiles():

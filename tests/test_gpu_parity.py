@@ -308,6 +308,36 @@ def test_device_resident_api():
     assert np.array_equal(xy.cpu().numpy().astype(np.int64), orc_lambda_coords(10))
 
 
+@pytest.mark.parametrize("name", ["vicsek", "carpet"])
+def test_generic_specs(golden, name):
+    """Vicsek (k=5, s=3) and carpet (k=8, s=3) through the table-driven per-cell kernels:
+    every valid (mode, strategy, backend) reproduces the reference's SW / RD / 2-step CA
+    (acceptance.cpp:153-208 for all specs) and λ (criterion 1)."""
+    from paper_2004_13475_b200.nbb import FractalSpec
+    spec = FractalSpec.builtin(name)
+    for r in range(0, 6):
+        w = golden["generic_specs"][name][str(r)]
+        n = spec.side_length(r)
+        rd = nbb.random_member_grid(spec, r, 17 + r, 100)
+        ca = nbb.random_member_grid(spec, r, 71 + r, 2)
+        assert fnv1a64(rd.values) == w["rd_grid_fnv"] and fnv1a64(ca.values) == w["ca_grid_fnv"]
+        combos = 0
+        for mode, st, be in itertools.product(MapMode, IntraBlockStrategy, LambdaBackend):
+            c = DispatchConfig(spec=spec, r=r, rho=1, mode=mode, strategy=st, backend=be,
+                               max_cells=max(1 << 24, n * n))
+            try:
+                c.validate()
+            except nbb.InvalidArgument:
+                continue
+            tag = (name, r, mode.name, st.name, be.name)
+            assert fnv1a64(nbb.run_single_write(c).grid.values) == w["sw_fnv"], tag
+            assert nbb.run_reduction(c, rd).value == w["rd_value"], tag
+            assert fnv1a64(nbb.run_ca(c, ca, 2).grid.values) == w["ca2_fnv"], tag
+            combos += 1
+        assert combos >= 4
+        assert fnv1a64(nbb.lambda_coords(DispatchConfig(spec=spec), r)) == w["lambda_fnv"], r
+
+
 def test_nbbmap_bench_csv_byte_identical(golden, tmp_path):
     """`nbbmap bench` over the GPU path prints the reference CLI's CSV bytes
     (tools/nbbmap.cpp:530-625; test_cli.cpp:151-175), for any worker count."""
