@@ -107,6 +107,10 @@ typedef struct nbb_config {
  *   buffers the kernels then move only member sectors over PCIe (zero-copy) instead of
  *   the whole n*n grid. Without the flag out_grid is always written in full. */
 #define NBB_FLAG_OUT_ZEROED 1u
+/* NBB_FLAG_COMPACT_STATE: nbb_gpu_ca keeps the CA state on the device in the compact
+ *   (λ-ordered CompactGrid) layout between the two conversions — int64 values, every
+ *   byte a member (gasket, cell_width 8, r >= 5, lambda mode). */
+#define NBB_FLAG_COMPACT_STATE 2u
 
 /* WorkReport (dispatch.hpp:44-61) */
 typedef struct nbb_report {
@@ -197,6 +201,38 @@ int nbb_gpu_scatter_members_dev(const nbb_config* cfg, const void* d_values, voi
  * coord_bytes = 4 (int32 pairs) or 8 (int64 pairs). */
 int nbb_gpu_lambda_coords_dev(const nbb_config* cfg, int32_t level, void* d_xy,
                               int32_t coord_bytes, void* stream);
+/* ---- compact (λ-ordered) state: CompactGrid, block_map.hpp:82-132 ----------------
+ * The k^r member values row-major over the packing orthotope (W = k^ceil(r/2) wide),
+ * value(ω) = embedded(λ(ω)). Level = cfg->r, any valid spec. */
+/* compact_store (block_map.cpp:245-262): embedded n*n -> compact k^r */
+int nbb_gpu_compact_store(const nbb_config* cfg, const int64_t* embedded, int64_t* compact);
+/* compact_load (block_map.cpp:264-282): compact -> embedded, non-members = empty_value */
+int nbb_gpu_compact_load(const nbb_config* cfg, const int64_t* compact, int64_t empty_value,
+                         int64_t* embedded);
+int nbb_gpu_compact_store_dev(const nbb_config* cfg, const void* d_embedded, void* d_compact,
+                              void* stream);
+int nbb_gpu_compact_load_dev(const nbb_config* cfg, const void* d_compact, int64_t empty_value,
+                             void* d_embedded, void* stream);
+/* lambda_inverse (block_map.cpp:113-148) of `count` points xy[2i], xy[2i+1] at `level`;
+ * omega receives (ωx, ωy) pairs. Returns NBB_ERR_OUT_OF_RANGE / NBB_ERR_DOMAIN for the
+ * first offending point (message names it), NBB_OK otherwise. */
+int nbb_gpu_lambda_inverse(const nbb_config* cfg, int32_t level, const int64_t* xy, uint64_t count,
+                           int64_t* omega);
+/* NBBC file (block_map.cpp:284-362): "NBBC", k, s, level (LE u32), values (LE i64) */
+int nbb_gpu_compact_write(const char* path, const nbb_spec* spec, int32_t level,
+                          const int64_t* values);
+/* reads into values (capacity entries); *level receives the file's level */
+int nbb_gpu_compact_read(const char* path, const nbb_spec* spec, int32_t* level, int64_t* values,
+                         uint64_t capacity);
+/* Workloads on device-resident compact state (gasket; CA needs r >= 5): one CA step
+ * d_src -> d_dst, the member sum, the single write (every member value = 1). */
+int nbb_gpu_ca_compact_step_dev(const nbb_config* cfg, const void* d_src, void* d_dst,
+                                uint16_t birth, uint16_t survive, void* stream, nbb_report* report);
+int nbb_gpu_reduction_compact_dev(const nbb_config* cfg, const void* d_compact, void* d_value,
+                                  void* stream, nbb_report* report);
+int nbb_gpu_single_write_compact_dev(const nbb_config* cfg, void* d_compact, void* stream,
+                                     nbb_report* report);
+
 /* Halo exchange helpers for sharded CA (multi-GPU): gather d_grid[idx[i]] into
  * d_out[i] and scatter d_vals[i] into d_grid[idx[i]], count cells of
  * cfg->cell_width bytes; idx are flat cell indices (y*n + x) in device memory. */

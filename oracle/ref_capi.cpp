@@ -11,6 +11,7 @@
 // block_map.hpp:25-132, mma.hpp:16-76).
 #include <chrono>
 #include <cstring>
+#include <fstream>
 #include <new>
 #include <sstream>
 #include <stdexcept>
@@ -377,6 +378,29 @@ int ref_compact_store(const nbb_spec* spec, int32_t level, const int64_t* embedd
         std::vector<std::int64_t> e(embedded, embedded + n * n);
         const auto c = nbb::compact_store(s, level, e);
         std::memcpy(compact, c.values().data(), c.values().size() * 8);
+    });
+}
+
+// NBBC file through the reference's own writer (block_map.cpp:327-338)
+int ref_write_compact(const nbb_spec* spec, int32_t level, const int64_t* values, const char* path) {
+    return guarded([&] {
+        const auto s = to_spec(*spec);
+        nbb::CompactGrid g(s, level);
+        std::memcpy(g.values().data(), values, g.values().size() * 8);
+        std::ofstream out(path, std::ios::binary);
+        nbb::write_compact(out, s, g);
+    });
+}
+
+// NBBC reader (block_map.cpp:340-362); values must hold k^level entries
+int ref_read_compact(const nbb_spec* spec, const char* path, int32_t* level, int64_t* values,
+                     uint64_t capacity) {
+    return guarded([&] {
+        std::ifstream in(path, std::ios::binary);
+        const auto g = nbb::read_compact(in, to_spec(*spec));
+        if (g.values().size() > capacity) throw std::length_error("capacity");
+        std::memcpy(values, g.values().data(), g.values().size() * 8);
+        *level = g.level();
     });
 }
 

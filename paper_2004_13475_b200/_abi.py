@@ -65,6 +65,7 @@ class NbbConfig(Structure):
 
 
 FLAG_OUT_ZEROED = 1
+FLAG_COMPACT_STATE = 2
 
 
 class NbbReport(Structure):
@@ -122,6 +123,16 @@ SIGNATURES = {
     "nbb_gpu_gather_cells_dev": (c_int, [CP, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "nbb_gpu_scatter_cells_dev": (c_int, [CP, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "nbb_gpu_release": (c_int, []),
+    "nbb_gpu_compact_store": (c_int, [CP, c_void_p, c_void_p]),
+    "nbb_gpu_compact_load": (c_int, [CP, c_void_p, c_int64, c_void_p]),
+    "nbb_gpu_compact_store_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p]),
+    "nbb_gpu_compact_load_dev": (c_int, [CP, c_void_p, c_int64, c_void_p, c_void_p]),
+    "nbb_gpu_lambda_inverse": (c_int, [CP, c_int32, c_void_p, c_uint64, c_void_p]),
+    "nbb_gpu_compact_write": (c_int, [ctypes.c_char_p, SP, c_int32, c_void_p]),
+    "nbb_gpu_compact_read": (c_int, [ctypes.c_char_p, SP, POINTER(c_int32), c_void_p, c_uint64]),
+    "nbb_gpu_ca_compact_step_dev": (c_int, [CP, c_void_p, c_void_p, c_uint16, c_uint16, c_void_p, RP]),
+    "nbb_gpu_reduction_compact_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p, RP]),
+    "nbb_gpu_single_write_compact_dev": (c_int, [CP, c_void_p, c_void_p, RP]),
 }
 
 _lib = None

@@ -26,6 +26,7 @@
 #include "tile_kernels.cuh"
 #include "ca_pipe_kernel.cuh"
 #include "bits_kernels.cuh"
+#include "compact_kernels.cuh"
 #include "util_kernels.cuh"
 
 using namespace nbbgpu;
@@ -101,6 +102,17 @@ int ensure_device(int device, DeviceCtx** out) {
         uint32_t tab[729];
         for (uint32_t v = 0; v < 729; ++v) tab[v] = xy6_arith(v);
         NBB_CUDA(cudaMemcpyToSymbol(c_xy729, tab, sizeof(tab)));
+        // local λ of a ρ = 32 tile (compact CA): li = ωy*27 + ωx <-> (x, y)
+        uint16_t pos[243], idx[1024];
+        for (int i = 0; i < 1024; ++i) idx[i] = 0xFFFF;
+        for (uint32_t li = 0; li < 243; ++li) {
+            const uint32_t ax = xy6_arith(li % 27), ay = xy6_arith(li / 27);
+            const uint32_t x = (ax & 0xFFFF) | ((ay & 0xFFFF) << 1), y = (ax >> 16) | ((ay >> 16) << 1);
+            pos[li] = (uint16_t)(x | (y << 5));
+            idx[y * 32 + x] = (uint16_t)li;
+        }
+        NBB_CUDA(cudaMemcpyToSymbol(c_local_pos, pos, sizeof(pos)));
+        NBB_CUDA(cudaMemcpyToSymbol(c_local_idx, idx, sizeof(idx)));
         NBB_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         NBB_CUDA(cudaMalloc(&c.partials, 4097 * sizeof(unsigned long long)));
         c.ready = true;
@@ -563,6 +575,68 @@ size_t grid_bytes(const Launch& L, int cw) {
 
 }  // namespace
 
+// ---- compact (λ-ordered) state ---------------------------------------------------------
+namespace {
+struct CompactShape {
+    int64_t n = 1;
+    uint64_t W = 1, H = 1, total = 1;
+};
+int compact_shape(const nbb_config* cfg, CompactShape* s) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_TRY(nbbhost::validate_spec(cfg->spec));
+    if (cfg->r < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "checked_pow: negative exponent");
+    NBB_TRY(nbbhost::side_length(cfg->spec, cfg->r, &s->n));
+    int64_t w, h;
+    NBB_TRY(nbbhost::orthotope_dims(cfg->spec, cfg->r, &w, &h));
+    s->W = (uint64_t)w;
+    s->H = (uint64_t)h;
+    s->total = s->W * s->H;
+    if (s->n > (int64_t(1) << 20)) return fail(NBB_ERR_RESOURCE, "embedding too large for the device path");
+    return NBB_OK;
+}
+unsigned grid_for(const DeviceCtx* c, uint64_t work) {
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, (uint64_t)c->sms * 16));
+}
+// compact CA / RD / SW validity: the gasket, λ launch, ρ = 32 tiles inside (r >= 5)
+int compact_workload_check(const nbb_config* cfg) {
+    NBB_TRY(nbbhost::validate(*cfg));
+    NBB_TRY(nbbhost::require_gasket(cfg->spec));
+    if (cfg->r < 5)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "compact-state workloads need r >= 5 (32 x 32 tiles)");
+    if (cfg->mode != NBB_MODE_LAMBDA)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "the compact state is the lambda orthotope: lambda mode only");
+    return NBB_OK;
+}
+int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* dst, uint16_t birth,
+                      uint16_t survive, cudaStream_t st) {
+    CompactCaArgs a;
+    a.src = (const long long*)src;
+    a.dst = (long long*)dst;
+    int64_t w, h;
+    nbbhost::orthotope_dims(cfg->spec, cfg->r, &w, &h);
+    a.W = (uint32_t)w;
+    a.rb = cfg->r - 5;
+    int64_t wb, hb;
+    nbbhost::orthotope_dims(cfg->spec, a.rb, &wb, &hb);
+    a.Wb = (uint32_t)wb;
+    a.Hb = (uint32_t)hb;
+    a.n = (int64_t)1 << cfg->r;
+    a.tiles = a.Wb * a.Hb;
+    a.birth = birth;
+    a.survive = survive;
+    static int occ = 0;
+    if (occ == 0) {
+        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ca_compact_kernel, 256, 0));
+        if (occ < 1) occ = 1;
+    }
+    const uint64_t want = (a.tiles + 7) / 8;
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
+    ca_compact_kernel<<<blocks, 256, 0, st>>>(a);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+}  // namespace
+
 // =====================================================================================
 extern "C" {
 
@@ -876,10 +950,15 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
     const long long* h_in = gasket ? (const long long*)mapped_host_ptr(initial) : nullptr;
     long long* h_out = (gasket && (cfg->flags & NBB_FLAG_OUT_ZEROED))
                            ? (long long*)mapped_host_ptr(out_grid) : nullptr;
+    const bool compact = (cfg->flags & NBB_FLAG_COMPACT_STATE) != 0;
+    if (compact) {
+        NBB_CHECK(compact_workload_check(cfg));
+        if (cw != 8) return fail(NBB_ERR_INVALID_ARGUMENT, "the compact state holds int64 values: cell_width 8");
+    }
     void *d64 = nullptr, *da, *db;
     if (cw == 8) {
         NBB_CHECK(device_buffer(*L.ctx, 0, b64, &da));
-        NBB_CHECK(device_buffer(*L.ctx, 1, b64, &db));
+        if (!compact) NBB_CHECK(device_buffer(*L.ctx, 1, b64, &db));
         if (h_in) {
             NBB_CUDA(cudaMemsetAsync(da, 0, b64, L.stream));
             copy_member_sectors_kernel<<<blocks, 256, 0, L.stream>>>(h_in, (long long*)da, L.plan.n, 1);
@@ -888,7 +967,7 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
             NBB_CUDA(cudaMemcpyAsync(da, initial, b64, cudaMemcpyHostToDevice, L.stream));
             NBB_CHECK(sanitize(L, da, 8, L.stream));
         }
-        NBB_CUDA(cudaMemsetAsync(db, 0, b64, L.stream));
+        if (!compact) NBB_CUDA(cudaMemsetAsync(db, 0, b64, L.stream));
     } else {
         const size_t bs = grid_bytes(L, cw);
         NBB_CHECK(device_buffer(*L.ctx, 1, bs, &da));
@@ -905,6 +984,26 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
             pack_bits_kernel<<<blocks, 256, 0, L.stream>>>(src64, (uint32_t*)da, L.plan.n);
         NBB_CUDA(cudaGetLastError());
         NBB_CUDA(cudaMemsetAsync(db, 0, bs, L.stream));
+    }
+    if (compact) {  // embedded -> compact state, steps on the λ orthotope, compact -> embedded
+        CompactShape cs;
+        NBB_CHECK(compact_shape(cfg, &cs));
+        void *ca, *cb;
+        NBB_CHECK(device_buffer(*L.ctx, 1, cs.total * 8, &ca));
+        NBB_CHECK(device_buffer(*L.ctx, 2, cs.total * 8, &cb));
+        NBB_CHECK(nbb_gpu_compact_store_dev(cfg, da, ca, L.stream));
+        for (int s = 0; s < steps; ++s) {
+            Timer t(cfg->timing != 0, L.stream);
+            NBB_CHECK(launch_ca_compact(L.ctx, cfg, ca, cb, birth, survive, L.stream));
+            const uint64_t us = t.stop_micros();
+            if (per_step) fill_report(cfg, &per_step[s], us);
+            std::swap(ca, cb);
+        }
+        // da's non-member cells are 0 (sanitized / zero-filled): scatter the members back
+        compact_load_kernel<<<grid_for(L.ctx, cs.total), 256, 0, L.stream>>>(
+            dev_spec(cfg->spec), (const long long*)ca, (long long*)da, cs.n, cs.W, cs.total, cfg->r);
+        NBB_CUDA(cudaGetLastError());
+        steps = 0;  // the generic loop below has nothing left to do
     }
     for (int s = 0; s < steps; ++s) {
         Timer t(cfg->timing != 0, L.stream);
@@ -992,6 +1091,158 @@ int nbb_gpu_scatter_cells_dev(const nbb_config* cfg, void* d_grid, const int64_t
         scatter_cells_kernel<unsigned char><<<blocks, 256, 0, (cudaStream_t)stream>>>(
             (unsigned char*)d_grid, (const long long*)d_idx, count, (const unsigned char*)d_vals);
     NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+
+int nbb_gpu_compact_store_dev(const nbb_config* cfg, const void* d_embedded, void* d_compact, void* stream) {
+    CompactShape s;
+    NBB_CHECK(compact_shape(cfg, &s));
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    compact_store_kernel<<<grid_for(ctx, s.total), 256, 0, (cudaStream_t)stream>>>(
+        dev_spec(cfg->spec), (const long long*)d_embedded, (long long*)d_compact, s.n, s.W, s.total, cfg->r);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+int nbb_gpu_compact_load_dev(const nbb_config* cfg, const void* d_compact, int64_t empty_value,
+                             void* d_embedded, void* stream) {
+    CompactShape s;
+    NBB_CHECK(compact_shape(cfg, &s));
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    const uint64_t cells = (uint64_t)s.n * (uint64_t)s.n;
+    fill_kernel<<<grid_for(ctx, cells), 256, 0, (cudaStream_t)stream>>>((long long*)d_embedded, cells, empty_value);
+    compact_load_kernel<<<grid_for(ctx, s.total), 256, 0, (cudaStream_t)stream>>>(
+        dev_spec(cfg->spec), (const long long*)d_compact, (long long*)d_embedded, s.n, s.W, s.total, cfg->r);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+int nbb_gpu_compact_store(const nbb_config* cfg, const int64_t* embedded, int64_t* compact) {
+    CompactShape s;
+    NBB_CHECK(compact_shape(cfg, &s));
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    const size_t be = (size_t)s.n * (size_t)s.n * 8, bc = (size_t)s.total * 8;
+    void *de, *dc;
+    NBB_CHECK(device_buffer(*ctx, 0, be, &de));
+    NBB_CHECK(device_buffer(*ctx, 1, bc, &dc));
+    NBB_CUDA(cudaMemcpyAsync(de, embedded, be, cudaMemcpyHostToDevice, ctx->stream));
+    NBB_CHECK(nbb_gpu_compact_store_dev(cfg, de, dc, ctx->stream));
+    NBB_CUDA(cudaMemcpyAsync(compact, dc, bc, cudaMemcpyDeviceToHost, ctx->stream));
+    NBB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return NBB_OK;
+}
+
+int nbb_gpu_compact_load(const nbb_config* cfg, const int64_t* compact, int64_t empty_value,
+                         int64_t* embedded) {
+    CompactShape s;
+    NBB_CHECK(compact_shape(cfg, &s));
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    const size_t be = (size_t)s.n * (size_t)s.n * 8, bc = (size_t)s.total * 8;
+    void *de, *dc;
+    NBB_CHECK(device_buffer(*ctx, 0, be, &de));
+    NBB_CHECK(device_buffer(*ctx, 1, bc, &dc));
+    NBB_CUDA(cudaMemcpyAsync(dc, compact, bc, cudaMemcpyHostToDevice, ctx->stream));
+    NBB_CHECK(nbb_gpu_compact_load_dev(cfg, dc, empty_value, de, ctx->stream));
+    NBB_CUDA(cudaMemcpyAsync(embedded, de, be, cudaMemcpyDeviceToHost, ctx->stream));
+    NBB_CUDA(cudaStreamSynchronize(ctx->stream));
+    return NBB_OK;
+}
+
+int nbb_gpu_lambda_inverse(const nbb_config* cfg, int32_t level, const int64_t* xy, uint64_t count,
+                           int64_t* omega) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_TRY(nbbhost::validate_spec(cfg->spec));
+    if (level < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "lambda_inverse: negative level");
+    int64_t n;
+    NBB_TRY(nbbhost::side_length(cfg->spec, level, &n));
+    if (count == 0) return NBB_OK;
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    void *dxy, *dom;
+    NBB_CHECK(device_buffer(*ctx, 0, count * 16, &dxy));
+    NBB_CHECK(device_buffer(*ctx, 1, count * 16 + count * 4, &dom));
+    int* dst = (int*)((char*)dom + count * 16);
+    NBB_CUDA(cudaMemcpyAsync(dxy, xy, count * 16, cudaMemcpyHostToDevice, ctx->stream));
+    lambda_inverse_kernel<<<grid_for(ctx, count), 256, 0, ctx->stream>>>(
+        dev_spec(cfg->spec), (const long long*)dxy, (long long*)dom, dst, count, level);
+    NBB_CUDA(cudaGetLastError());
+    std::vector<int> st(count);
+    NBB_CUDA(cudaMemcpyAsync(omega, dom, count * 16, cudaMemcpyDeviceToHost, ctx->stream));
+    NBB_CUDA(cudaMemcpyAsync(st.data(), dst, count * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    NBB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (uint64_t i = 0; i < count; ++i) {
+        if (st[i] == NBB_ERR_OUT_OF_RANGE)
+            return fail(NBB_ERR_OUT_OF_RANGE, "lambda_inverse: (" + std::to_string(xy[2 * i]) + "," +
+                                                  std::to_string(xy[2 * i + 1]) + ") outside " +
+                                                  std::to_string(n) + "^2");
+        if (st[i] == NBB_ERR_DOMAIN)
+            return fail(NBB_ERR_DOMAIN, "lambda_inverse: (" + std::to_string(xy[2 * i]) + "," +
+                                            std::to_string(xy[2 * i + 1]) +
+                                            ") is not a member cell at level " + std::to_string(level));
+    }
+    return NBB_OK;
+}
+
+int nbb_gpu_compact_write(const char* path, const nbb_spec* spec, int32_t level, const int64_t* values) {
+    NBB_TRY(nbbhost::validate_spec(*spec));
+    NBB_TRY(nbbhost::write_compact(path, *spec, level, values));
+    return NBB_OK;
+}
+
+int nbb_gpu_compact_read(const char* path, const nbb_spec* spec, int32_t* level, int64_t* values,
+                         uint64_t capacity) {
+    NBB_TRY(nbbhost::validate_spec(*spec));
+    int lv = 0;
+    NBB_TRY(nbbhost::read_compact(path, *spec, &lv, values, capacity));
+    *level = lv;
+    return NBB_OK;
+}
+
+int nbb_gpu_ca_compact_step_dev(const nbb_config* cfg, const void* d_src, void* d_dst, uint16_t birth,
+                                uint16_t survive, void* stream, nbb_report* report) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_CHECK(compact_workload_check(cfg));
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    Timer t(cfg->timing != 0, (cudaStream_t)stream);
+    NBB_CHECK(launch_ca_compact(ctx, cfg, d_src, d_dst, birth, survive, (cudaStream_t)stream));
+    fill_report(cfg, report, t.stop_micros());
+    return NBB_OK;
+}
+
+int nbb_gpu_reduction_compact_dev(const nbb_config* cfg, const void* d_compact, void* d_value, void* stream,
+                                  nbb_report* report) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_CHECK(compact_workload_check(cfg));
+    CompactShape s;
+    NBB_CHECK(compact_shape(cfg, &s));
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    Timer t(cfg->timing != 0, (cudaStream_t)stream);
+    NBB_CUDA(cudaMemsetAsync(d_value, 0, 8, (cudaStream_t)stream));
+    dense_sum_kernel<<<ctx->sms * 4, 256, 0, (cudaStream_t)stream>>>((const long long*)d_compact, s.total,
+                                                                      (unsigned long long*)d_value);
+    NBB_CUDA(cudaGetLastError());
+    fill_report(cfg, report, t.stop_micros());
+    return NBB_OK;
+}
+
+int nbb_gpu_single_write_compact_dev(const nbb_config* cfg, void* d_compact, void* stream, nbb_report* report) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_CHECK(compact_workload_check(cfg));
+    CompactShape s;
+    NBB_CHECK(compact_shape(cfg, &s));
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    Timer t(cfg->timing != 0, (cudaStream_t)stream);
+    fill_kernel<<<ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>((long long*)d_compact, s.total, 1);
+    NBB_CUDA(cudaGetLastError());
+    fill_report(cfg, report, t.stop_micros());
     return NBB_OK;
 }
 

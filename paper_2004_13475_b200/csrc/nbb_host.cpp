@@ -1,6 +1,7 @@
 // nbb_host.cpp — host-side logic of the engine; see nbb_host.hpp.
 #include "nbb_host.hpp"
 
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <random>
@@ -390,6 +391,90 @@ void local_cell_table(const nbb_spec& s, int edge, int16_t* out) {
             e[1] = (int16_t)py;
         }
     }
+}
+
+static void put_u32(std::vector<unsigned char>& b, uint32_t v) {
+    for (int i = 0; i < 4; ++i) b.push_back((unsigned char)(v >> (8 * i)));
+}
+
+Error write_compact(const char* path, const nbb_spec& s, int level, const int64_t* values) {
+    uint64_t count;
+    Error e = checked_pow((uint64_t)s.k, level, &count);
+    if (!e.ok()) return e;
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) return err(NBB_ERR_RUNTIME, std::string("cannot open '") + path + "' for writing");
+    std::vector<unsigned char> head = {'N', 'B', 'B', 'C'};
+    put_u32(head, (uint32_t)s.k);
+    put_u32(head, (uint32_t)s.s);
+    put_u32(head, (uint32_t)level);
+    bool ok = std::fwrite(head.data(), 1, head.size(), f) == head.size();
+    std::vector<unsigned char> buf;
+    buf.reserve(1 << 20);
+    for (uint64_t i = 0; i < count && ok; ++i) {
+        const uint64_t v = (uint64_t)values[i];
+        for (int b = 0; b < 8; ++b) buf.push_back((unsigned char)(v >> (8 * b)));
+        if (buf.size() >= (1 << 20) || i + 1 == count) {
+            ok = std::fwrite(buf.data(), 1, buf.size(), f) == buf.size();
+            buf.clear();
+        }
+    }
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) return err(NBB_ERR_RUNTIME, "compact file: write failed");
+    return {};
+}
+
+Error read_compact(const char* path, const nbb_spec& s, int* level, int64_t* values, uint64_t capacity) {
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) return err(NBB_ERR_INVALID_ARGUMENT, std::string("cannot open '") + path + "'");
+    unsigned char head[16];
+    const size_t got = std::fread(head, 1, 16, f);
+    auto u32 = [&](int o) {
+        return (uint32_t)head[o] | ((uint32_t)head[o + 1] << 8) | ((uint32_t)head[o + 2] << 16) |
+               ((uint32_t)head[o + 3] << 24);
+    };
+    if (got < 4 || std::memcmp(head, "NBBC", 4) != 0) {
+        std::fclose(f);
+        return err(NBB_ERR_INVALID_ARGUMENT, "compact file: bad magic");
+    }
+    if (got < 16) {
+        std::fclose(f);
+        return err(NBB_ERR_INVALID_ARGUMENT, "compact file: truncated header");
+    }
+    const uint32_t k = u32(4), ss = u32(8), lv = u32(12);
+    if (k != (uint32_t)s.k || ss != (uint32_t)s.s) {
+        std::fclose(f);
+        return err(NBB_ERR_INVALID_ARGUMENT, "compact file: header (k=" + std::to_string(k) + ", s=" +
+                                                 std::to_string(ss) + ") does not match spec '" +
+                                                 s.name + "'");
+    }
+    if (lv > 64) {
+        std::fclose(f);
+        return err(NBB_ERR_INVALID_ARGUMENT, "compact file: implausible level " + std::to_string(lv));
+    }
+    uint64_t count;
+    Error e = checked_pow((uint64_t)s.k, (int)lv, &count);
+    if (!e.ok()) {
+        std::fclose(f);
+        return e;
+    }
+    if (count > capacity) {
+        std::fclose(f);
+        return err(NBB_ERR_RESOURCE, "compact file: " + std::to_string(count) +
+                                         " values exceed the buffer of " + std::to_string(capacity));
+    }
+    std::vector<unsigned char> buf(8);
+    for (uint64_t i = 0; i < count; ++i) {
+        if (std::fread(buf.data(), 1, 8, f) != 8) {
+            std::fclose(f);
+            return err(NBB_ERR_INVALID_ARGUMENT, "compact file: truncated payload");
+        }
+        uint64_t v = 0;
+        for (int b = 0; b < 8; ++b) v |= (uint64_t)buf[b] << (8 * b);
+        values[i] = (int64_t)v;
+    }
+    std::fclose(f);
+    *level = (int)lv;
+    return {};
 }
 
 void fastdiv_magic(uint32_t d, uint32_t* m, uint32_t* s) {

@@ -65,6 +65,10 @@ Error random_member_grid(const nbb_spec& s, int r, uint64_t seed, uint64_t modul
 // LocalCellTable (block_map.cpp:197-206): edge*edge (x, y) int16 pairs, -1 = spare
 void local_cell_table(const nbb_spec& s, int edge, int16_t* out);
 
+// NBBC compact file (block_map.cpp:284-362)
+Error write_compact(const char* path, const nbb_spec& s, int level, const int64_t* values);
+Error read_compact(const char* path, const nbb_spec& s, int* level, int64_t* values, uint64_t capacity);
+
 // precomputed fast division magic (see common.cuh FastDiv), exact for x < 2^31
 void fastdiv_magic(uint32_t d, uint32_t* m, uint32_t* s);
 

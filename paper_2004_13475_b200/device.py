@@ -59,6 +59,39 @@ def scatter_members_dev(config: DispatchConfig, d_values: int, d_grid: int, stre
                                               _vp(d_grid), _vp(stream)))
 
 
+def compact_store_dev(config: DispatchConfig, d_embedded: int, d_compact: int, stream: int = 0) -> None:
+    _check(_lib().nbb_gpu_compact_store_dev(ctypes.byref(config.to_c()), _vp(d_embedded),
+                                            _vp(d_compact), _vp(stream)))
+
+
+def compact_load_dev(config: DispatchConfig, d_compact: int, d_embedded: int, empty_value: int = 0,
+                     stream: int = 0) -> None:
+    _check(_lib().nbb_gpu_compact_load_dev(ctypes.byref(config.to_c()), _vp(d_compact), empty_value,
+                                           _vp(d_embedded), _vp(stream)))
+
+
+def ca_compact_step_dev(config: DispatchConfig, d_src: int, d_dst: int, rule: CaRule = CaRule(),
+                        stream: int = 0) -> WorkReport:
+    rep = _abi.NbbReport()
+    _check(_lib().nbb_gpu_ca_compact_step_dev(ctypes.byref(config.to_c()), _vp(d_src), _vp(d_dst),
+                                              rule.birth, rule.survive, _vp(stream), ctypes.byref(rep)))
+    return WorkReport.from_c(rep)
+
+
+def reduction_compact_dev(config: DispatchConfig, d_compact: int, d_value: int, stream: int = 0) -> WorkReport:
+    rep = _abi.NbbReport()
+    _check(_lib().nbb_gpu_reduction_compact_dev(ctypes.byref(config.to_c()), _vp(d_compact),
+                                                _vp(d_value), _vp(stream), ctypes.byref(rep)))
+    return WorkReport.from_c(rep)
+
+
+def single_write_compact_dev(config: DispatchConfig, d_compact: int, stream: int = 0) -> WorkReport:
+    rep = _abi.NbbReport()
+    _check(_lib().nbb_gpu_single_write_compact_dev(ctypes.byref(config.to_c()), _vp(d_compact),
+                                                   _vp(stream), ctypes.byref(rep)))
+    return WorkReport.from_c(rep)
+
+
 def lambda_coords_dev(config: DispatchConfig, level: int, d_xy: int, coord_bytes: int = 4,
                       stream: int = 0) -> None:
     _check(_lib().nbb_gpu_lambda_coords_dev(ctypes.byref(config.to_c()), level, _vp(d_xy),

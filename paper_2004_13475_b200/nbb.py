@@ -434,6 +434,100 @@ def lambda_coords(config: DispatchConfig, level: int) -> np.ndarray:
     return out
 
 
+# ---- compact codec (block_map.hpp:82-132) ------------------------------------------
+class CompactGrid:
+    """k^level values row-major over the packing orthotope (x fastest): value(ω) =
+    embedded(λ(ω)). `values` is a (height, width) int64 array."""
+
+    def __init__(self, spec: FractalSpec, level: int, values: Optional[np.ndarray] = None):
+        w, h = spec.orthotope_dims(level)
+        self.spec, self._level, self._w, self._h = spec, level, w, h
+        if values is None:
+            values = np.zeros((h, w), dtype=np.int64)
+        self.values = np.ascontiguousarray(np.asarray(values, dtype=np.int64).reshape(h, w))
+
+    def level(self) -> int:
+        return self._level
+
+    def width(self) -> int:
+        return self._w
+
+    def height(self) -> int:
+        return self._h
+
+    def size(self) -> int:
+        return self._w * self._h
+
+    def at(self, ox: int, oy: int) -> int:
+        return int(self.values[oy, ox])
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, CompactGrid) and self._level == other._level and
+                np.array_equal(self.values, other.values))
+
+
+def compact_store(spec: FractalSpec, level: int, embedded: np.ndarray) -> CompactGrid:
+    """block_map.cpp:245-262 on the device."""
+    n = spec.side_length(level)
+    emb = np.ascontiguousarray(embedded, dtype=np.int64)
+    if emb.size != n * n:
+        raise InvalidArgument(f"compact_store: embedded grid holds {emb.size} cells, expected {n * n}")
+    out = CompactGrid(spec, level)
+    c = DispatchConfig(spec=spec, r=level, max_cells=max(1 << 24, n * n))
+    _check(_lib().nbb_gpu_compact_store(ctypes.byref(c.to_c()), emb.ctypes.data_as(ctypes.c_void_p),
+                                        out.values.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def compact_load(spec: FractalSpec, compact: CompactGrid, empty_value: int = 0) -> np.ndarray:
+    """block_map.cpp:264-282 on the device: (n, n) int64, non-members = empty_value."""
+    w, h = spec.orthotope_dims(compact.level())
+    if (compact.width(), compact.height()) != (w, h):
+        raise InvalidArgument(f"compact_load: grid shape does not match spec '{spec.name}' at level "
+                              f"{compact.level()}")
+    n = spec.side_length(compact.level())
+    out = np.empty((n, n), dtype=np.int64)
+    c = DispatchConfig(spec=spec, r=compact.level(), max_cells=max(1 << 24, n * n))
+    _check(_lib().nbb_gpu_compact_load(ctypes.byref(c.to_c()),
+                                       compact.values.ctypes.data_as(ctypes.c_void_p), empty_value,
+                                       out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def lambda_inverse(spec: FractalSpec, level: int, points) -> np.ndarray:
+    """block_map.cpp:113-148 for an (m, 2) array of (x, y) -> (m, 2) array of (ωx, ωy).
+    Raises OutOfRange / DomainError for the first offending point, like the reference."""
+    xy = np.ascontiguousarray(np.asarray(points, dtype=np.int64).reshape(-1, 2))
+    out = np.empty_like(xy)
+    c = DispatchConfig(spec=spec)
+    _check(_lib().nbb_gpu_lambda_inverse(ctypes.byref(c.to_c()), level,
+                                         xy.ctypes.data_as(ctypes.c_void_p), xy.shape[0],
+                                         out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def write_compact(path: str, spec: FractalSpec, grid: CompactGrid) -> None:
+    """NBBC file (block_map.cpp:327-338)."""
+    _check(_lib().nbb_gpu_compact_write(str(path).encode(), ctypes.byref(spec.to_c()), grid.level(),
+                                        grid.values.ctypes.data_as(ctypes.c_void_p)))
+
+
+def read_compact(path: str, spec: FractalSpec, max_values: int = 1 << 28) -> CompactGrid:
+    """NBBC file (block_map.cpp:340-362)."""
+    buf = np.empty(max_values, dtype=np.int64) if max_values <= (1 << 22) else None
+    if buf is None:  # size the buffer from the header
+        import struct
+        with open(path, "rb") as f:
+            head = f.read(16)
+        lv = struct.unpack("<I", head[12:16])[0] if len(head) == 16 and head[:4] == b"NBBC" else 0
+        buf = np.empty(max(1, min(max_values, spec.k ** min(lv, 40))), dtype=np.int64)
+    lv = ctypes.c_int32()
+    _check(_lib().nbb_gpu_compact_read(str(path).encode(), ctypes.byref(spec.to_c()), ctypes.byref(lv),
+                                       buf.ctypes.data_as(ctypes.c_void_p), buf.size))
+    w, h = spec.orthotope_dims(lv.value)
+    return CompactGrid(spec, lv.value, buf[:w * h].copy())
+
+
 def device_count() -> int:
     c = ctypes.c_int32()
     _check(_lib().nbb_gpu_device_count(ctypes.byref(c)))

@@ -118,6 +118,8 @@ def ref_lib():
             "ref_csv_header": (c_char_p, []),
             "ref_compact_store": (c_int, [SP, c_int32, c_void_p, c_void_p]),
             "ref_format_double": (c_int, [c_double, c_char_p, c_size_t]),
+            "ref_write_compact": (c_int, [SP, c_int32, c_void_p, c_char_p]),
+            "ref_read_compact": (c_int, [SP, c_char_p, POINTER(c_int32), c_void_p, c_uint64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

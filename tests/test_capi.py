@@ -204,3 +204,33 @@ def test_nbbmap_cli_errors():
     assert nbbmap.main(["bench", "--workload", "xx"]) == 2
     assert nbbmap.main(["bench", "--rmin", "3", "--rmax", "2"]) == 2
     assert nbbmap.main(["bench", "--rmin", "13", "--rmax", "13"]) == 3
+
+
+def test_nbbc_file_matches_reference(tmp_path):
+    """NBBC compact files (block_map.cpp:284-362): our writer's bytes equal the reference
+    writer's, each reader reads the other's files, and the error texts match."""
+    from _oracle import ref_available, ref_lib
+    rng = np.random.default_rng(1)
+    for spec, level in ((GASKET, 5), (FractalSpec.vicsek(), 3), (FractalSpec.carpet(), 2)):
+        w, h = spec.orthotope_dims(level)
+        g = nbb.CompactGrid(spec, level, rng.integers(-2**62, 2**62, size=(h, w)))
+        ours = tmp_path / f"ours_{spec.name}.nbbc"
+        nbb.write_compact(str(ours), spec, g)
+        raw = ours.read_bytes()
+        assert raw[:4] == b"NBBC" and len(raw) == 16 + 8 * w * h
+        assert nbb.read_compact(str(ours), spec) == g
+        if ref_available():
+            theirs = tmp_path / f"ref_{spec.name}.nbbc"
+            assert ref_lib().ref_write_compact(ctypes.byref(spec.to_c()), level,
+                                               g.values.ctypes.data_as(ctypes.c_void_p),
+                                               str(theirs).encode()) == 0
+            assert theirs.read_bytes() == raw
+    bad = tmp_path / "bad.nbbc"
+    bad.write_bytes(b"NBBX" + bytes(12))
+    with pytest.raises(InvalidArgument, match="compact file: bad magic"):
+        nbb.read_compact(str(bad), GASKET)
+    bad.write_bytes(raw[:20])  # carpet header, truncated payload, read as carpet
+    with pytest.raises(InvalidArgument, match="truncated payload"):
+        nbb.read_compact(str(bad), FractalSpec.carpet())
+    with pytest.raises(InvalidArgument, match=r"header \(k=8, s=3\) does not match spec 'sierpinski'"):
+        nbb.read_compact(str(ours), GASKET)

@@ -338,6 +338,78 @@ def test_generic_specs(golden, name):
         assert fnv1a64(nbb.lambda_coords(DispatchConfig(spec=spec), r)) == w["lambda_fnv"], r
 
 
+def test_compact_codec_matches_reference():
+    """compact_store / compact_load (block_map.cpp:245-282) and λ⁻¹ (:113-148) on the device,
+    against the reference library (criterion 7: round trip, k^r slots)."""
+    import ctypes
+    from _oracle import ref_available, ref_lib
+    from paper_2004_13475_b200.nbb import FractalSpec
+    for spec, rmax in ((GASKET, 10), (FractalSpec.vicsek(), 5), (FractalSpec.carpet(), 4)):
+        for r in range(0, rmax + 1):
+            n = spec.side_length(r)
+            dense = nbb.random_member_grid(spec, r, 1234 + r, 100000, max_cells=max(1 << 24, n * n)).values
+            comp = nbb.compact_store(spec, r, dense)
+            assert comp.size() == spec.volume(r)
+            if ref_available():
+                want = np.empty(spec.volume(r), dtype=np.int64)
+                assert ref_lib().ref_compact_store(ctypes.byref(spec.to_c()), r,
+                                                   dense.ctypes.data_as(ctypes.c_void_p),
+                                                   want.ctypes.data_as(ctypes.c_void_p)) == 0
+                assert np.array_equal(comp.values.ravel(), want), (spec.name, r)
+            assert np.array_equal(nbb.compact_load(spec, comp, 0), dense), (spec.name, r)
+            full = nbb.compact_load(spec, comp, -7)
+            assert np.count_nonzero(full == -7) >= n * n - spec.volume(r)
+    # λ⁻¹ round trip and the reference's errors
+    xy = nbb.lambda_coords(cfg(), 9)
+    om = nbb.lambda_inverse(GASKET, 9, xy)
+    w = 3 ** 5
+    assert np.array_equal(om[:, 1] * w + om[:, 0], np.arange(3 ** 9))
+    with pytest.raises(nbb.DomainError, match="is not a member cell at level 2"):
+        nbb.lambda_inverse(GASKET, 2, [(0, 0), (1, 0)])
+    with pytest.raises(nbb.OutOfRange, match="outside 4\\^2"):
+        nbb.lambda_inverse(GASKET, 2, [(4, 0)])
+
+
+@pytest.mark.parametrize("r", [5, 6, 9, 12])
+def test_ca_compact_state(golden, r):
+    """NBB_FLAG_COMPACT_STATE: the CA state lives in the λ-ordered compact layout on the
+    device (ca_compact_kernel); results equal the oracle / the reference's golden."""
+    from paper_2004_13475_b200 import _abi as abi
+    init = with_garbage(orc_random_member_grid(r, 50 + r, 2), r, seed=r) if r <= 9 else \
+        orc_random_member_grid(r, 50 + r, 2)
+    for rule in (RULES[:4] if r <= 6 else RULES[:1]):
+        for steps in (1, 3, 10):
+            want = orc_ca(r, init, steps, rule.birth, rule.survive)
+            got = nbb.run_ca(cfg(r=r, rho=32, flags=abi.FLAG_COMPACT_STATE), grid(init, r), steps, rule)
+            assert np.array_equal(got.grid.values, want), (r, rule, steps)
+    w = golden["workloads"][str(r)]
+    g = nbb.random_member_grid(GASKET, r, 1 + r, 2, max_cells=1 << (2 * r))
+    for k, (pop, digest) in w["ca"].items():
+        out = nbb.run_ca(cfg(r=r, rho=32, flags=abi.FLAG_COMPACT_STATE), g, int(k)).grid.values
+        assert (int(out.sum()), fnv1a64(out)) == (pop, digest), k
+    with pytest.raises(nbb.InvalidArgument, match="lambda mode only"):
+        nbb.run_ca(cfg(r=r, rho=32, mode=MapMode.BoundingBox, flags=abi.FLAG_COMPACT_STATE), g, 1)
+
+
+def test_compact_device_workloads():
+    torch = pytest.importorskip("torch")
+    from paper_2004_13475_b200 import device as dev
+    r = 12
+    c = cfg(r=r, rho=32)
+    s = torch.cuda.current_stream().cuda_stream
+    host = nbb.random_member_grid(GASKET, r, 5, 1000)
+    emb = torch.from_numpy(host.values).cuda()
+    comp = torch.empty(3 ** r, dtype=torch.int64, device="cuda")
+    dev.compact_store_dev(c, emb.data_ptr(), comp.data_ptr(), s)
+    val = torch.zeros(1, dtype=torch.int64, device="cuda")
+    dev.reduction_compact_dev(c, comp.data_ptr(), val.data_ptr(), s)
+    assert int(val.item()) == orc_reduction(r, host.values)
+    dev.single_write_compact_dev(c, comp.data_ptr(), s)
+    back = torch.zeros_like(emb)
+    dev.compact_load_dev(c, comp.data_ptr(), back.data_ptr(), 0, s)
+    assert np.array_equal(back.cpu().numpy(), orc_single_write(r))
+
+
 def test_nbbmap_bench_csv_byte_identical(golden, tmp_path):
     """`nbbmap bench` over the GPU path prints the reference CLI's CSV bytes
     (tools/nbbmap.cpp:530-625; test_cli.cpp:151-175), for any worker count."""
