@@ -314,6 +314,7 @@ def main():
             kk = K if "tile" in name else max(5, K // 10)
             results[name] = timed(ca_runner(c, a, b), kk, W)
 
+    sweep = None
     # uint8 / 1-bit alive states (exact: CA only reads != 0 and writes 0/1)
     if world == 1:
         a8 = torch.zeros((n, n), dtype=torch.uint8, device="cuda")
@@ -346,6 +347,39 @@ def main():
                         "rd_bb_percell_rho32": cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell),
                         "rd_lambda_percell_rho16": cfg(rho=16, kernel=nbb.KernelFamily.PerCell)}.items():
             results[name] = timed(rd(c), K if "tile" in name else max(5, K // 10), W)
+
+        # the compact (λ-ordered CompactGrid) state: every byte a member value (int64)
+        c1 = torch.empty(members, dtype=torch.int64, device="cuda")
+        c2 = torch.empty_like(c1)
+        dev.compact_store_dev(cfg(), a.data_ptr(), c1.data_ptr(), s)
+        cbufs = [c1, c2]
+        cstate = {"i": 0}
+
+        def ca_compact():
+            i = cstate["i"]
+            dev.ca_compact_step_dev(cfg(), cbufs[i & 1].data_ptr(), cbufs[(i + 1) & 1].data_ptr(),
+                                    nbb.CaRule(), s)
+            cstate["i"] = i + 1
+        results["ca_lambda_compact_i64"] = timed(ca_compact, K, W)
+        results["rd_lambda_compact_i64"] = timed(
+            lambda: dev.reduction_compact_dev(cfg(), c1.data_ptr(), out.data_ptr(), s), K, W)
+        results["sw_lambda_compact_i64"] = timed(lambda: dev.single_write_compact_dev(cfg(), c2.data_ptr(), s), K, W)
+        del c1, c2, cbufs
+
+        # C4: the λ map alone over a whole orthotope, scalar closed form vs tensor core (K0-TC)
+        xy = torch.empty(3 ** 17 * 2, dtype=torch.int32, device="cuda")
+        sweep = {}
+        for lvl in (10, 12, 14, 16, 17):
+            row = {"omegas": 3 ** lvl}
+            for label, be in (("scalar", nbb.LambdaBackend.Direct), ("tensor_core", nbb.LambdaBackend.MmaV2)):
+                if be != nbb.LambdaBackend.Direct and lvl > 16:
+                    continue
+                c = cfg(backend=be)
+                ms = timed(lambda: dev.lambda_coords_dev(c, lvl, xy.data_ptr(), 4, s), max(5, K // 4), W)
+                row[label + "_ms"] = ms
+                row[label + "_omega_per_s"] = 3 ** lvl * 1e3 / ms
+            sweep[str(lvl)] = row
+        del xy
 
     # ---- roofline of the dominant kernel ----------------------------------------------
     peak, peak_kind = measured_peaks()
@@ -441,6 +475,7 @@ def main():
             "ca_i64_paper_bb_percell_over_lambda": (best_bb_percell / head_ms) if best_bb_percell else None,
             "ca_u8_bb_over_lambda": ratio("ca_bb_tile_rho32_u8", "ca_lambda_tile_rho32_u8"),
             "ca_bit_bb_over_lambda": ratio("ca_bb_tile_rho32_bit", "ca_lambda_tile_rho32_bit"),
+            "ca_compact_vs_bb_i64": ratio("ca_bb_tile_rho32_i64", "ca_lambda_compact_i64"),
             "sw_best_bb_over_lambda": ratio("sw_bb_tile_rho32", "sw_lambda_tile_rho32"),
             "rd_best_bb_over_lambda": ratio("rd_bb_tile_rho32", "rd_lambda_tile_rho32"),
         },
@@ -452,6 +487,7 @@ def main():
         },
         "workloads_ms": results,
         "workloads_cells_per_s": {k: cells(k) for k in results},
+        "map_sweep_C4": sweep,
         "cpu_baseline": cpu,
         "e2e": e2e,
     }

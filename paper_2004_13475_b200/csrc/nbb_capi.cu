@@ -223,15 +223,15 @@ bool tile_supported(const nbb_config& c, int op, int cell_width) {
 }
 
 // CA on the bit-packed state (bits_kernels.cuh)
-template <bool BB>
-int run_ca_bits(const Launch& L, const TileArgs& a) {
-    auto kern = ca_bits_kernel<BB, 2>;
+template <bool BB, int ILP>
+int run_ca_bits_ilp(const Launch& L, const TileArgs& a) {
+    auto kern = ca_bits_kernel<BB, ILP>;
     static int occ = 0;
     if (occ == 0) {
         NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0));
         if (occ < 1) occ = 1;
     }
-    const uint64_t units = (a.tiles + 1) / 2;
+    const uint64_t units = (a.tiles + ILP - 1) / ILP;
     const uint64_t want = (units + 7) / 8;
     const uint64_t cap = (uint64_t)L.ctx->sms * (uint64_t)occ;
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min(want, cap));
@@ -240,6 +240,22 @@ int run_ca_bits(const Launch& L, const TileArgs& a) {
     NBB_CUDA(cudaGetLastError());
     return NBB_OK;
 }
+
+template <bool BB>
+int run_ca_bits(const Launch& L, const TileArgs& a) {
+    static int ilp = -1;
+    if (ilp < 0) {
+        const char* e = std::getenv("NBB_BITS_ILP");
+        ilp = e ? std::atoi(e) : 0;
+    }
+    // Measured on B200 at n = 2^16 (profiles/r1_bits_ilp.json): λ tiles favour 8 words in
+    // flight per thread (0.098 vs 0.108 ms at 4), the BB grid favours 2 (0.636 vs 0.718 ms).
+    if (ilp == 0) return BB ? run_ca_bits_ilp<BB, 2>(L, a) : run_ca_bits_ilp<BB, 8>(L, a);
+    if (ilp == 2) return run_ca_bits_ilp<BB, 2>(L, a);
+    if (ilp == 8) return run_ca_bits_ilp<BB, 8>(L, a);
+    return run_ca_bits_ilp<BB, 4>(L, a);
+}
+
 
 TileArgs make_tile_args(const Launch& L, const void* src, void* dst, unsigned long long* sum,
                         uint32_t birth, uint32_t survive, uint32_t tile_begin, uint32_t tiles) {
@@ -401,7 +417,16 @@ int run_percell(const Launch& L, const PercellArgs& a) {
     const uint64_t Y = std::min<uint64_t>((B + X - 1) / X, 65535);
     const uint64_t Z = (B + X * Y - 1) / (X * Y);
     dim3 grid((unsigned)X, (unsigned)Y, (unsigned)Z);
-    percell_kernel<Cell, OP, BB, STRATEGY, BACKEND><<<grid, threads, 0, L.stream>>>(a);
+    // Generic (non-gasket) specs are a separate instantiation so the gasket kernels carry
+    // no table-driven code; validate() restricts generic specs to int64 cells.
+    if constexpr (sizeof(Cell) == 8) {
+        if (!a.spec.gasket) {
+            percell_kernel<Cell, OP, BB, STRATEGY, BACKEND, true><<<grid, threads, 0, L.stream>>>(a);
+            NBB_CUDA(cudaGetLastError());
+            return NBB_OK;
+        }
+    }
+    percell_kernel<Cell, OP, BB, STRATEGY, BACKEND, false><<<grid, threads, 0, L.stream>>>(a);
     NBB_CUDA(cudaGetLastError());
     return NBB_OK;
 }

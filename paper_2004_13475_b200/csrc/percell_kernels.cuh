@@ -111,7 +111,7 @@ __device__ __forceinline__ uint32_t beta_digit(uint64_t ox, uint64_t oy, int mu)
     return (uint32_t)(v % 3u);
 }
 
-template <typename Cell, int OP, bool BB, int STRATEGY, int BACKEND>
+template <typename Cell, int OP, bool BB, int STRATEGY, int BACKEND, bool GEN>
 __global__ void percell_kernel(PercellArgs a) {
     __shared__ float sA[256], sB[256], sC[256], sD[256], sE[256];
     __shared__ int64_t s_origin[2];
@@ -132,14 +132,14 @@ __global__ void percell_kernel(PercellArgs a) {
     if (BB) {
         cx = (int64_t)gx * edge + tx;
         cy = (int64_t)gy * edge + ty;
-        active = real && (a.spec.gasket ? gasket_member(cx, cy, n) : member_spec(a.spec, cx, cy, a.r));
+        active = real && (!GEN ? gasket_member(cx, cy, n) : member_spec(a.spec, cx, cy, a.r));
     } else {
         if (BACKEND == NBB_BACKEND_MMA2 && ((int64_t)gx >= a.sub_w || (int64_t)gy >= a.sub_h)) {
             return;  // padding slot of the even-rounded cover: all spare (dispatch.cpp:321-325)
         }
         int64_t ox = 0, oy = 0;
         if (BACKEND == NBB_BACKEND_DIRECT) {
-            if (a.spec.gasket) {
+            if (!GEN) {
                 uint32_t lx, ly;
                 lambda_arith((uint32_t)gx, (uint32_t)gy, lx, ly);
                 ox = lx;
@@ -147,7 +147,7 @@ __global__ void percell_kernel(PercellArgs a) {
             } else {
                 lambda_spec(a.spec, gx, gy, a.map_level, ox, oy);
             }
-        } else if (BACKEND == NBB_BACKEND_MMA1 && !a.spec.gasket) {
+        } else if (BACKEND == NBB_BACKEND_MMA1 && GEN) {
             // s = 3: powers 3^(μ-1) are not bf16-exact beyond 3^5 — variant 1 on the FP64
             // tensor pipe (DMMA m8n8k4): A row 0 = s^(μ-1), B cols 0/1 = τx/τy; K = 16 in 4 steps
             if (tid < 32) {
@@ -245,7 +245,7 @@ __global__ void percell_kernel(PercellArgs a) {
         // intra-block strategy (dispatch.cpp:357-398)
         if (real) {
             if (STRATEGY == NBB_STRATEGY_SUBBOX) {
-                active = a.spec.gasket ? (tx & (edge - 1 - ty)) == 0
+                active = !GEN ? (tx & (edge - 1 - ty)) == 0
                                        : member_spec(a.spec, tx, ty, a.local_level);
                 if (BACKEND == NBB_BACKEND_MMA3) {
                     cx = (int64_t)sD[tx * 16 + ty];  // Dx[i=tx][j=ty] = ρ·λx + tx
@@ -258,7 +258,7 @@ __global__ void percell_kernel(PercellArgs a) {
                 const int64_t rank = ty * edge + tx;
                 if (rank < a.local_members) {
                     int64_t lx, ly;
-                    if (a.spec.gasket) {
+                    if (!GEN) {
                         uint32_t ux, uy;
                         lambda_arith((uint32_t)(rank % a.local_w), (uint32_t)(rank / a.local_w), ux, uy);
                         lx = ux;
@@ -313,7 +313,7 @@ __global__ void percell_kernel(PercellArgs a) {
                 for (int dx = -1; dx <= 1; ++dx) {
                     if (dx == 0 && dy == 0) continue;
                     const int64_t nx = cx + dx, ny = cy + dy;
-                    const bool m = a.spec.gasket ? gasket_member(nx, ny, n)
+                    const bool m = !GEN ? gasket_member(nx, ny, n)
                                                  : member_spec(a.spec, nx, ny, a.r);
                     if (m && src[ny * n + nx] != (Cell)0) ++live;
                 }
