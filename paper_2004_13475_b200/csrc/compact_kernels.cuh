@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "tile_kernels.cuh"
+#include "util_kernels.cuh"
 
 namespace nbbgpu {
 
@@ -25,9 +26,10 @@ __constant__ uint16_t c_local_pos[243];
 // inverse: local (x, y) -> li, or 0xFFFF for non-members
 __constant__ uint16_t c_local_idx[1024];
 
+template <bool GEN>
 __device__ __forceinline__ void lambda_point(const DevSpec& sp, uint64_t ox, uint64_t oy, int level,
                                              int64_t& x, int64_t& y) {
-    if (sp.gasket) {
+    if (!GEN) {
         uint32_t lx, ly;
         lambda_arith((uint32_t)ox, (uint32_t)oy, lx, ly);
         x = lx;
@@ -38,23 +40,25 @@ __device__ __forceinline__ void lambda_point(const DevSpec& sp, uint64_t ox, uin
 }
 
 // compact[c] = embedded[λ(ω_c)], one thread per compact cell
+template <bool GEN>
 __global__ void compact_store_kernel(DevSpec sp, const long long* emb, long long* comp, int64_t n,
                                      uint64_t W, uint64_t total, int level) {
     for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < total;
          c += (uint64_t)gridDim.x * blockDim.x) {
         int64_t x, y;
-        lambda_point(sp, c % W, c / W, level, x, y);
+        lambda_point<GEN>(sp, c % W, c / W, level, x, y);
         comp[c] = emb[y * n + x];
     }
 }
 
 // embedded[λ(ω_c)] = compact[c] (the non-member fill happens before)
+template <bool GEN>
 __global__ void compact_load_kernel(DevSpec sp, const long long* comp, long long* emb, int64_t n,
                                     uint64_t W, uint64_t total, int level) {
     for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < total;
          c += (uint64_t)gridDim.x * blockDim.x) {
         int64_t x, y;
-        lambda_point(sp, c % W, c / W, level, x, y);
+        lambda_point<GEN>(sp, c % W, c / W, level, x, y);
         emb[y * n + x] = comp[c];
     }
 }
@@ -154,84 +158,227 @@ struct CompactCaArgs {
     uint32_t birth, survive;
 };
 
+// Base-3 value of a bit mask read as digits in {0,1}: the 8 values of 3 bits packed as nibbles.
+__device__ __forceinline__ uint32_t bits_base3(uint32_t b) {
+    constexpr uint32_t L = 0xDCA94310u;  // 0,1,3,4,9,10,12,13
+    return ((L >> (4u * (b & 7u))) & 15u) + 27u * ((L >> (4u * ((b >> 3) & 7u))) & 15u) +
+           729u * ((L >> (4u * ((b >> 6) & 7u))) & 15u);
+}
+// bits 0,2,4,... of v (< 2^18) packed together
+__device__ __forceinline__ uint32_t even_bits(uint32_t v) {
+    v &= 0x15555u;
+    v = (v | (v >> 1)) & 0x13333u;
+    v = (v | (v >> 2)) & 0x10F0Fu;
+    v = (v | (v >> 4)) & 0x100FFu;
+    return (v | (v >> 8)) & 0x1FFu;
+}
+// Compact offset (ωy·W + ωx) of a gasket member cell (x, y): λ⁻¹ at full level, where every
+// digit is β = bit_x + bit_y (gasket offsets (0,0),(0,1),(1,1); block_map.cpp:113-148), odd
+// levels μ (bit μ−1 even) feeding ωx and even levels feeding ωy. Valid for r ≤ 18.
+__device__ __forceinline__ uint64_t gasket_compact_offset(uint32_t x, uint32_t y, uint32_t W) {
+    const uint32_t ox = bits_base3(even_bits(x)) + bits_base3(even_bits(y));
+    const uint32_t oy = bits_base3(even_bits(x >> 1)) + bits_base3(even_bits(y >> 1));
+    return (uint64_t)oy * W + ox;
+}
+
 // One warp per tile; tile u -> (ωx_b = u / Hb, ωy_b = u % Hb) so consecutive warps walk along a
-// compact row block. 243 values per tile = slots k = 0..7 of lane l: li = 32k + l.
-__global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a) {
-    __shared__ uint32_t s_rows[8][32];
+// compact row block. 243 values per tile = slots k = 0..7 of lane l: li = 32k + l (k < 7 valid
+// for every lane, k = 7 for lanes < 19).
+//
+// Per tile: 8 coalesced 8-byte loads per lane (compact rows of 27 values), the 8 halo cells
+// (compact offsets by the bit form of λ⁻¹), alive bits scattered as bytes into a per-warp
+// 32 x 32 byte tile (non-member bytes stay 0, so no atomics and no clearing), rows packed back
+// to bit masks (lane = row) for the bit-sliced rule, and 8 stores per lane. The kernel is
+// issue-bound as much as DRAM-bound (ncu: ALU pipe 66%, long-scoreboard 61% of stalls),
+// hence the instruction diet. Tried and slower on B200 (profiles/r1_compact_ca_tuning.md):
+// a cp.async ring (8-byte copies), L2 bulk prefetch one tile ahead, 64/48-register budgets,
+// and cp.async.bulk row copies into an mbarrier ring.
+__global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, FastDiv div_hb) {
+    __shared__ __align__(16) uint8_t s_cell[8][32 * 32];
     __shared__ uint32_t s_new[8][32];
+    __shared__ uint16_t s_pos[256];  // c_local_pos (per-lane constant-bank reads serialise)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint8_t* cell = s_cell[wib];
+    s_pos[threadIdx.x] = threadIdx.x < 243 ? c_local_pos[threadIdx.x] : 0;
+    __syncthreads();
     uint32_t sl_off[8], sl_pos[8];
-    uint32_t valid = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const uint32_t li = 32u * k + lane;
         const bool ok = li < 243u;
         const uint32_t row = ok ? li / 27u : 0u, col = ok ? li % 27u : 0u;
-        sl_off[k] = row * a.W + col;               // element offset inside the tile's sub-block
-        sl_pos[k] = ok ? c_local_pos[li] : 0u;
-        valid |= (ok ? 1u : 0u) << k;
+        sl_off[k] = row * a.W + col;  // element offset inside the tile's sub-block
+        sl_pos[k] = s_pos[li];        // x | y << 5 = byte index in the 32 x 32 tile
     }
+    const bool k7 = lane < 19;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) reinterpret_cast<uint32_t*>(cell)[32 * i + lane] = 0u;
     const uint32_t hk = (uint32_t)lane & 7u;
     const int hx = (hk == 0 || hk == 3) ? -1 : (hk == 1 || hk == 7) ? 0 : (hk == 2) ? 1 : 32;
     const int hy = (hk <= 2) ? -1 : (hk == 3 || hk == 5) ? 31 : (hk == 4) ? 30 : 32;
+    const uint32_t nm1 = (uint32_t)(a.n - 1);
     const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t warp_stride = (gridDim.x * blockDim.x) >> 5;
+    __syncwarp();
 
     for (uint32_t u = warp_global; u < a.tiles; u += warp_stride) {
-        const uint32_t wxb = u / a.Hb, wyb = u - (u / a.Hb) * a.Hb;
-        const uint64_t base = (uint64_t)(9u * wxb) * a.W + 27u * wyb;
-        // loads (all 8 slots in flight)
+        const uint32_t wxb = fastdiv(u, div_hb), wyb = u - wxb * a.Hb;
+        const long long* src = a.src + (uint64_t)(9u * wxb) * a.W + 27u * wyb;
         long long v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = ((valid >> k) & 1u) ? __ldg(a.src + base + sl_off[k]) : 0ll;
-        // tile origin (λ of the block ordinal: block ordinal = ωy_b * Wb + ωx_b)
+        for (int k = 0; k < 7; ++k) v[k] = __ldg(src + sl_off[k]);
+        v[7] = k7 ? __ldg(src + sl_off[7]) : 0ll;
+        // halo cell of lanes 0..7 (its compact offset from the bits of its coordinates)
         uint32_t bx, by;
         lambda_const(wxb, wyb, bx, by);
-        const int64_t X0 = (int64_t)bx * 32, Y0 = (int64_t)by * 32;
-        // halo cell of lanes 0..7
-        uint32_t hbit = 0;
-        if (lane < 8) {
-            const int64_t gx = X0 + hx, gy = Y0 + hy;
-            if (gasket_member(gx, gy, a.n)) {
-                uint32_t ox, oy;
-                gasket_block_inverse((uint32_t)(gx >> 5), (uint32_t)(gy >> 5), a.rb, ox, oy);
-                const uint32_t li = c_local_idx[((uint32_t)gy & 31u) * 32u + ((uint32_t)gx & 31u)];
-                const uint32_t row = li / 27u, col = li % 27u;
-                const uint64_t off = (uint64_t)(9u * ox + row) * a.W + 27u * oy + col;
-                hbit = __ldg(a.src + off) != 0ll;
-            }
+        long long hv = 0;
+        {
+            const uint32_t gx = bx * 32u + (uint32_t)hx, gy = by * 32u + (uint32_t)hy;  // wraps if < 0
+            if (lane < 8 && gx <= nm1 && gy <= nm1 && (gx & (nm1 - gy)) == 0u)
+                hv = __ldg(a.src + gasket_compact_offset(gx, gy, a.W));
         }
-        const uint32_t hmask = __ballot_sync(0xFFFFFFFFu, hbit != 0u);
-        s_rows[wib][lane] = 0u;
-        __syncwarp();
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (((valid >> k) & 1u) && v[k] != 0ll)
-                atomicOr(&s_rows[wib][sl_pos[k] >> 5], 1u << (sl_pos[k] & 31u));
-        }
+        for (int k = 0; k < 7; ++k) cell[sl_pos[k]] = v[k] != 0ll;
+        if (k7) cell[sl_pos[7]] = v[7] != 0ll;
+        const uint32_t h = __ballot_sync(0xFFFFFFFFu, hv != 0ll) & 0xFFu;
         __syncwarp();
-        const uint32_t R = s_rows[wib][lane];
-        const uint64_t h = hmask & 0xFFu;
+        uint32_t R = 0;
+        {
+            const uint4 q0 = reinterpret_cast<const uint4*>(cell + 32 * lane)[0];
+            const uint4 q1 = reinterpret_cast<const uint4*>(cell + 32 * lane)[1];
+            const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) R |= ((w[i] * 0x01020408u) >> 24 & 0xFu) << (4 * i);
+        }
         uint64_t E = (uint64_t)R << 1;
-        if (lane == 31) E |= ((h >> 3) & 1u) | (((h >> 5) & 1u) << 33);
-        if (lane == 30) E |= ((h >> 4) & 1u) << 33;
+        if (lane == 31) E |= ((h >> 3) & 1u) | ((uint64_t)((h >> 5) & 1u) << 33);
+        if (lane == 30) E |= (uint64_t)((h >> 4) & 1u) << 33;
         const uint64_t top = (h & 1u) | (((h >> 1) & 1u) << 1) | (((h >> 2) & 1u) << 2);
-        const uint64_t bottom = (((h >> 7) & 1u) << 1) | (((h >> 6) & 1u) << 33);
+        const uint64_t bottom = (((h >> 7) & 1u) << 1) | ((uint64_t)((h >> 6) & 1u) << 33);
         const uint64_t Eu = __shfl_up_sync(0xFFFFFFFFu, E, 1);
         const uint64_t Ed = __shfl_down_sync(0xFFFFFFFFu, E, 1);
         const uint64_t U = lane == 0 ? top : Eu;
         const uint64_t D = lane == 31 ? bottom : Ed;
-        const uint32_t memb = submask_bits((uint32_t)lane);
         s_new[wib][lane] = life_rule((uint32_t)U, (uint32_t)(U >> 1), (uint32_t)(U >> 2), (uint32_t)E,
                                      (uint32_t)(E >> 2), (uint32_t)D, (uint32_t)(D >> 1), (uint32_t)(D >> 2),
-                                     (uint32_t)(E >> 1), a.birth, a.survive) & memb;
+                                     (uint32_t)(E >> 1), a.birth, a.survive) &
+                           submask_bits((uint32_t)lane);
         __syncwarp();
+        long long* dst = a.dst + (src - a.src);
+#pragma unroll
+        for (int k = 0; k < 7; ++k)
+            dst[sl_off[k]] = (long long)((s_new[wib][sl_pos[k] >> 5] >> (sl_pos[k] & 31u)) & 1u);
+        if (k7) dst[sl_off[7]] = (long long)((s_new[wib][sl_pos[7] >> 5] >> (sl_pos[7] & 31u)) & 1u);
+        __syncwarp();
+    }
+}
+
+
+// ---- embedded member sectors <-> compact state, tile by tile ------------------------------
+// Local compact index li = ωy_l·27 + ωx_l of member (x, y) of a ρ = 32 tile (x ⊆ y < 32).
+__device__ __forceinline__ uint32_t tile_local_index(uint32_t x, uint32_t y) {
+    const uint32_t wx = bits_base3(even_bits(x)) + bits_base3(even_bits(y));
+    const uint32_t wy = bits_base3(even_bits(x >> 1)) + bits_base3(even_bits(y >> 1));
+    return wy * 27u + wx;
+}
+
+// Slot e < 108 of a ρ = 32 int64 tile: the e-th member sector in row-major order,
+// packed y | s << 5 (row y holds the 2^popc(y>>2) sectors s ⊆ y>>2).
+__device__ __forceinline__ uint32_t tile_sector_slot(uint32_t e) {
+    uint32_t y = 0;
+    for (; y < 32u; ++y) {
+        const uint32_t cnt = 1u << __popc(y >> 2);
+        if (e < cnt) break;
+        e -= cnt;
+    }
+    return y | (pdep32(e, y >> 2) << 5);
+}
+
+// Warp per λ tile: read the tile's 108 member sectors of an embedded int64 grid (device or
+// mapped pinned host memory — every byte crossing PCIe is a member sector) and write its 243
+// values as the tile's 9 x 27 compact sub-block. Replaces embedded -> compact_store for the
+// host-buffer CA call (no 32 GiB embedded staging grid on the device).
+__global__ void __launch_bounds__(256) compact_from_sectors_kernel(const long long* emb, long long* comp,
+                                                                   CompactCaArgs a, FastDiv div_hb) {
+    __shared__ long long s_v[8][256];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint32_t slot[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t e = 32u * k + lane;
+        slot[k] = e < 108u ? tile_sector_slot(e) : 0xFFFFFFFFu;
+    }
+    const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t warp_stride = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t u = warp_global; u < a.tiles; u += warp_stride) {
+        const uint32_t wxb = fastdiv(u, div_hb), wyb = u - wxb * a.Hb;
+        uint32_t bx, by;
+        lambda_const(wxb, wyb, bx, by);
+        const int64_t org = (int64_t)by * 32 * a.n + (int64_t)bx * 32;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (slot[k] == 0xFFFFFFFFu) continue;
+            const uint32_t y = slot[k] & 31u, sx = slot[k] >> 5;
+            const Sector v = ld_sector(emb + org + (int64_t)y * a.n + 4 * sx);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t x = 4u * sx + c;
+                if ((x & ~y) == 0u)
+                    s_v[wib][tile_local_index(x, y)] =
+                        (long long)(((unsigned long long)v.w[2 * c + 1] << 32) | v.w[2 * c]);
+            }
+        }
+        __syncwarp();
+        const uint64_t base = (uint64_t)(9u * wxb) * a.W + 27u * wyb;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            if ((valid >> k) & 1u) {
-                const uint32_t bit = (s_new[wib][sl_pos[k] >> 5] >> (sl_pos[k] & 31u)) & 1u;
-                a.dst[base + sl_off[k]] = (long long)bit;
+            const uint32_t li = 32u * k + lane;
+            if (li < 243u) comp[base + (li / 27u) * a.W + li % 27u] = s_v[wib][li];
+        }
+        __syncwarp();
+    }
+}
+
+// The inverse: compact sub-block of each tile -> its 108 member sectors of an embedded int64
+// grid (non-member cells of those sectors written 0; other sectors untouched).
+__global__ void __launch_bounds__(256) compact_to_sectors_kernel(const long long* comp, long long* emb,
+                                                                 CompactCaArgs a, FastDiv div_hb) {
+    __shared__ long long s_v[8][256];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint32_t slot[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t e = 32u * k + lane;
+        slot[k] = e < 108u ? tile_sector_slot(e) : 0xFFFFFFFFu;
+    }
+    const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t warp_stride = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t u = warp_global; u < a.tiles; u += warp_stride) {
+        const uint32_t wxb = fastdiv(u, div_hb), wyb = u - wxb * a.Hb;
+        const uint64_t base = (uint64_t)(9u * wxb) * a.W + 27u * wyb;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t li = 32u * k + lane;
+            if (li < 243u) s_v[wib][li] = comp[base + (li / 27u) * a.W + li % 27u];
+        }
+        __syncwarp();
+        uint32_t bx, by;
+        lambda_const(wxb, wyb, bx, by);
+        const int64_t org = (int64_t)by * 32 * a.n + (int64_t)bx * 32;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (slot[k] == 0xFFFFFFFFu) continue;
+            const uint32_t y = slot[k] & 31u, sx = slot[k] >> 5;
+            Sector v;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t x = 4u * sx + c;
+                const unsigned long long q =
+                    (x & ~y) == 0u ? (unsigned long long)s_v[wib][tile_local_index(x, y)] : 0ull;
+                v.w[2 * c] = (uint32_t)q;
+                v.w[2 * c + 1] = (uint32_t)(q >> 32);
             }
+            stg_sector(emb + org + (int64_t)y * a.n + 4 * sx, v);
         }
         __syncwarp();
     }

@@ -632,8 +632,8 @@ int compact_workload_check(const nbb_config* cfg) {
         return fail(NBB_ERR_INVALID_ARGUMENT, "the compact state is the lambda orthotope: lambda mode only");
     return NBB_OK;
 }
-int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* dst, uint16_t birth,
-                      uint16_t survive, cudaStream_t st) {
+CompactCaArgs compact_args(const nbb_config* cfg, const void* src, void* dst, uint16_t birth,
+                           uint16_t survive, FastDiv* div_hb) {
     CompactCaArgs a;
     a.src = (const long long*)src;
     a.dst = (long long*)dst;
@@ -649,6 +649,36 @@ int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, vo
     a.tiles = a.Wb * a.Hb;
     a.birth = birth;
     a.survive = survive;
+    div_hb->d = a.Hb;
+    nbbhost::fastdiv_magic(a.Hb, &div_hb->m, &div_hb->s);
+    return a;
+}
+
+// The tile codec (compact_from/to_sectors_kernel) serves the gasket at r >= 5.
+bool compact_tiles_ok(const nbb_config* cfg) { return nbbhost::is_gasket(cfg->spec) && cfg->r >= 5; }
+
+int compact_from_sectors(DeviceCtx* ctx, const nbb_config* cfg, const void* emb, void* comp, cudaStream_t st) {
+    FastDiv d;
+    const CompactCaArgs a = compact_args(cfg, nullptr, nullptr, 0, 0, &d);
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.tiles + 7) / 8, (uint64_t)ctx->sms * 8));
+    compact_from_sectors_kernel<<<blocks, 256, 0, st>>>((const long long*)emb, (long long*)comp, a, d);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+int compact_to_sectors(DeviceCtx* ctx, const nbb_config* cfg, const void* comp, void* emb, cudaStream_t st) {
+    FastDiv d;
+    const CompactCaArgs a = compact_args(cfg, nullptr, nullptr, 0, 0, &d);
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.tiles + 7) / 8, (uint64_t)ctx->sms * 8));
+    compact_to_sectors_kernel<<<blocks, 256, 0, st>>>((const long long*)comp, (long long*)emb, a, d);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* dst, uint16_t birth,
+                      uint16_t survive, cudaStream_t st) {
+    FastDiv div_hb;
+    const CompactCaArgs a = compact_args(cfg, src, dst, birth, survive, &div_hb);
     static int occ = 0;
     if (occ == 0) {
         NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ca_compact_kernel, 256, 0));
@@ -656,7 +686,7 @@ int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, vo
     }
     const uint64_t want = (a.tiles + 7) / 8;
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
-    ca_compact_kernel<<<blocks, 256, 0, st>>>(a);
+    ca_compact_kernel<<<blocks, 256, 0, st>>>(a, div_hb);
     NBB_CUDA(cudaGetLastError());
     return NBB_OK;
 }
@@ -975,15 +1005,45 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
     const long long* h_in = gasket ? (const long long*)mapped_host_ptr(initial) : nullptr;
     long long* h_out = (gasket && (cfg->flags & NBB_FLAG_OUT_ZEROED))
                            ? (long long*)mapped_host_ptr(out_grid) : nullptr;
-    const bool compact = (cfg->flags & NBB_FLAG_COMPACT_STATE) != 0;
-    if (compact) {
+    if (cfg->flags & NBB_FLAG_COMPACT_STATE) {
+        // compact state: member sectors -> the λ-ordered compact array (2 x 8·3^r bytes on the
+        // device, no embedded grid), steps on the orthotope, compact -> member sectors.
         NBB_CHECK(compact_workload_check(cfg));
         if (cw != 8) return fail(NBB_ERR_INVALID_ARGUMENT, "the compact state holds int64 values: cell_width 8");
+        CompactShape cs;
+        NBB_CHECK(compact_shape(cfg, &cs));
+        void *ca, *cb, *stage = nullptr;
+        NBB_CHECK(device_buffer(*L.ctx, 1, cs.total * 8, &ca));
+        NBB_CHECK(device_buffer(*L.ctx, 2, cs.total * 8, &cb));
+        const void* src = h_in;
+        if (!src) {  // pageable input: stage the embedded grid in HBM
+            NBB_CHECK(device_buffer(*L.ctx, 0, b64, &stage));
+            NBB_CUDA(cudaMemcpyAsync(stage, initial, b64, cudaMemcpyHostToDevice, L.stream));
+            src = stage;
+        }
+        NBB_CHECK(compact_from_sectors(L.ctx, cfg, src, ca, L.stream));
+        for (int s = 0; s < steps; ++s) {
+            Timer t(cfg->timing != 0, L.stream);
+            NBB_CHECK(launch_ca_compact(L.ctx, cfg, ca, cb, birth, survive, L.stream));
+            const uint64_t us = t.stop_micros();
+            if (per_step) fill_report(cfg, &per_step[s], us);
+            std::swap(ca, cb);
+        }
+        if (h_out) {  // member sectors straight into the zeroed pinned output
+            NBB_CHECK(compact_to_sectors(L.ctx, cfg, ca, h_out, L.stream));
+        } else {
+            if (!stage) NBB_CHECK(device_buffer(*L.ctx, 0, b64, &stage));
+            NBB_CUDA(cudaMemsetAsync(stage, 0, b64, L.stream));
+            NBB_CHECK(compact_to_sectors(L.ctx, cfg, ca, stage, L.stream));
+            NBB_CUDA(cudaMemcpyAsync(out_grid, stage, b64, cudaMemcpyDeviceToHost, L.stream));
+        }
+        NBB_CUDA(cudaStreamSynchronize(L.stream));
+        return NBB_OK;
     }
     void *d64 = nullptr, *da, *db;
     if (cw == 8) {
         NBB_CHECK(device_buffer(*L.ctx, 0, b64, &da));
-        if (!compact) NBB_CHECK(device_buffer(*L.ctx, 1, b64, &db));
+        NBB_CHECK(device_buffer(*L.ctx, 1, b64, &db));
         if (h_in) {
             NBB_CUDA(cudaMemsetAsync(da, 0, b64, L.stream));
             copy_member_sectors_kernel<<<blocks, 256, 0, L.stream>>>(h_in, (long long*)da, L.plan.n, 1);
@@ -992,7 +1052,7 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
             NBB_CUDA(cudaMemcpyAsync(da, initial, b64, cudaMemcpyHostToDevice, L.stream));
             NBB_CHECK(sanitize(L, da, 8, L.stream));
         }
-        if (!compact) NBB_CUDA(cudaMemsetAsync(db, 0, b64, L.stream));
+        NBB_CUDA(cudaMemsetAsync(db, 0, b64, L.stream));
     } else {
         const size_t bs = grid_bytes(L, cw);
         NBB_CHECK(device_buffer(*L.ctx, 1, bs, &da));
@@ -1009,26 +1069,6 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
             pack_bits_kernel<<<blocks, 256, 0, L.stream>>>(src64, (uint32_t*)da, L.plan.n);
         NBB_CUDA(cudaGetLastError());
         NBB_CUDA(cudaMemsetAsync(db, 0, bs, L.stream));
-    }
-    if (compact) {  // embedded -> compact state, steps on the λ orthotope, compact -> embedded
-        CompactShape cs;
-        NBB_CHECK(compact_shape(cfg, &cs));
-        void *ca, *cb;
-        NBB_CHECK(device_buffer(*L.ctx, 1, cs.total * 8, &ca));
-        NBB_CHECK(device_buffer(*L.ctx, 2, cs.total * 8, &cb));
-        NBB_CHECK(nbb_gpu_compact_store_dev(cfg, da, ca, L.stream));
-        for (int s = 0; s < steps; ++s) {
-            Timer t(cfg->timing != 0, L.stream);
-            NBB_CHECK(launch_ca_compact(L.ctx, cfg, ca, cb, birth, survive, L.stream));
-            const uint64_t us = t.stop_micros();
-            if (per_step) fill_report(cfg, &per_step[s], us);
-            std::swap(ca, cb);
-        }
-        // da's non-member cells are 0 (sanitized / zero-filled): scatter the members back
-        compact_load_kernel<<<grid_for(L.ctx, cs.total), 256, 0, L.stream>>>(
-            dev_spec(cfg->spec), (const long long*)ca, (long long*)da, cs.n, cs.W, cs.total, cfg->r);
-        NBB_CUDA(cudaGetLastError());
-        steps = 0;  // the generic loop below has nothing left to do
     }
     for (int s = 0; s < steps; ++s) {
         Timer t(cfg->timing != 0, L.stream);
@@ -1125,8 +1165,13 @@ int nbb_gpu_compact_store_dev(const nbb_config* cfg, const void* d_embedded, voi
     NBB_CHECK(compact_shape(cfg, &s));
     DeviceCtx* ctx;
     NBB_CHECK(ensure_device(cfg->device, &ctx));
-    compact_store_kernel<<<grid_for(ctx, s.total), 256, 0, (cudaStream_t)stream>>>(
-        dev_spec(cfg->spec), (const long long*)d_embedded, (long long*)d_compact, s.n, s.W, s.total, cfg->r);
+    if (compact_tiles_ok(cfg)) return compact_from_sectors(ctx, cfg, d_embedded, d_compact, (cudaStream_t)stream);
+    if (nbbhost::is_gasket(cfg->spec))
+        compact_store_kernel<false><<<grid_for(ctx, s.total), 256, 0, (cudaStream_t)stream>>>(
+            dev_spec(cfg->spec), (const long long*)d_embedded, (long long*)d_compact, s.n, s.W, s.total, cfg->r);
+    else
+        compact_store_kernel<true><<<grid_for(ctx, s.total), 256, 0, (cudaStream_t)stream>>>(
+            dev_spec(cfg->spec), (const long long*)d_embedded, (long long*)d_compact, s.n, s.W, s.total, cfg->r);
     NBB_CUDA(cudaGetLastError());
     return NBB_OK;
 }
@@ -1138,9 +1183,18 @@ int nbb_gpu_compact_load_dev(const nbb_config* cfg, const void* d_compact, int64
     DeviceCtx* ctx;
     NBB_CHECK(ensure_device(cfg->device, &ctx));
     const uint64_t cells = (uint64_t)s.n * (uint64_t)s.n;
-    fill_kernel<<<grid_for(ctx, cells), 256, 0, (cudaStream_t)stream>>>((long long*)d_embedded, cells, empty_value);
-    compact_load_kernel<<<grid_for(ctx, s.total), 256, 0, (cudaStream_t)stream>>>(
-        dev_spec(cfg->spec), (const long long*)d_compact, (long long*)d_embedded, s.n, s.W, s.total, cfg->r);
+    if (empty_value == 0) {
+        NBB_CUDA(cudaMemsetAsync(d_embedded, 0, cells * 8, (cudaStream_t)stream));
+        if (compact_tiles_ok(cfg)) return compact_to_sectors(ctx, cfg, d_compact, d_embedded, (cudaStream_t)stream);
+    } else {
+        fill_kernel<<<grid_for(ctx, cells), 256, 0, (cudaStream_t)stream>>>((long long*)d_embedded, cells, empty_value);
+    }
+    if (nbbhost::is_gasket(cfg->spec))
+        compact_load_kernel<false><<<grid_for(ctx, s.total), 256, 0, (cudaStream_t)stream>>>(
+            dev_spec(cfg->spec), (const long long*)d_compact, (long long*)d_embedded, s.n, s.W, s.total, cfg->r);
+    else
+        compact_load_kernel<true><<<grid_for(ctx, s.total), 256, 0, (cudaStream_t)stream>>>(
+            dev_spec(cfg->spec), (const long long*)d_compact, (long long*)d_embedded, s.n, s.W, s.total, cfg->r);
     NBB_CUDA(cudaGetLastError());
     return NBB_OK;
 }

@@ -130,8 +130,8 @@ def test_ca_bit_packed_state(golden, r):
         nbb.run_ca(cfg(r=r, rho=16, cell_width=0), grid(init, r), 1)
 
 
-@pytest.mark.parametrize("cw", [8, 1, 0])
-def test_ca_host_buffers_pinned_zero_copy(cw):
+@pytest.mark.parametrize("cw,state", [(8, 0), (1, 0), (0, 0), (8, _abi.FLAG_COMPACT_STATE)])
+def test_ca_host_buffers_pinned_zero_copy(cw, state):
     """nbb_gpu_ca on pinned host buffers: member sectors move in place over PCIe; with
     FLAG_OUT_ZEROED only member cells of out are written; without it out is written whole."""
     torch = pytest.importorskip("torch")
@@ -143,7 +143,7 @@ def test_ca_host_buffers_pinned_zero_copy(cw):
     h_in = torch.from_numpy(init.copy()).pin_memory()
     for flags, out_init in ((_abi.FLAG_OUT_ZEROED, 0), (0, 0), (0, 7)):
         h_out = torch.full((n, n), out_init, dtype=torch.int64).pin_memory()
-        c = cfg(r=r, rho=32, cell_width=cw, flags=flags).to_c()
+        c = cfg(r=r, rho=32, cell_width=cw, flags=flags | state).to_c()
         rc = lib.nbb_gpu_ca(ctypes.byref(c), ctypes.c_void_p(h_in.data_ptr()), r, 5, 8, 12,
                             ctypes.c_void_p(h_out.data_ptr()), None)
         assert rc == 0, lib.nbb_gpu_last_error()
@@ -151,7 +151,7 @@ def test_ca_host_buffers_pinned_zero_copy(cw):
     assert np.array_equal(h_in.numpy(), init)  # the input is never written
     # in place (out aliases the pinned input): full write, garbage cleared
     h_io = torch.from_numpy(init.copy()).pin_memory()
-    c = cfg(r=r, rho=32, cell_width=cw).to_c()
+    c = cfg(r=r, rho=32, cell_width=cw, flags=state).to_c()
     assert lib.nbb_gpu_ca(ctypes.byref(c), ctypes.c_void_p(h_io.data_ptr()), r, 5, 8, 12,
                           ctypes.c_void_p(h_io.data_ptr()), None) == 0
     assert np.array_equal(h_io.numpy(), want)
@@ -494,3 +494,14 @@ def test_full_size_r16_properties():
         dev.unpack_alive_dev(c1, w2.data_ptr(), b.data_ptr(), s)
         assert int(b.sum().item()) == ref_sum
         assert torch.equal(b.sum(dim=1), rows) and torch.equal(b.sum(dim=0), cols)
+    # the compact (λ-ordered) state: codec -> pipelined compact step -> codec, bit-identical
+    del w1, w2
+    ref = torch.zeros_like(a)
+    dev.ca_step_dev(c, a.data_ptr(), ref.data_ptr(), CaRule(), s)
+    k1 = torch.empty(3 ** r, dtype=torch.int64, device="cuda")
+    k2 = torch.empty_like(k1)
+    dev.compact_store_dev(c, a.data_ptr(), k1.data_ptr(), s)
+    dev.ca_compact_step_dev(c, k1.data_ptr(), k2.data_ptr(), CaRule(), s)
+    dev.compact_load_dev(c, k2.data_ptr(), b.data_ptr(), 0, s)
+    assert torch.equal(b, ref)
+    assert int(k2.sum().item()) == ref_sum

@@ -43,6 +43,14 @@ res = {
     "sw_compact_ms": timed(lambda: dev.single_write_compact_dev(c, c2.data_ptr(), s)),
     "compact_store_ms": timed(lambda: dev.compact_store_dev(c, a.data_ptr(), c1.data_ptr(), s), 10),
 }
+back = torch.zeros_like(a)
+dev.compact_load_dev(c, c1.data_ptr(), back.data_ptr(), 0, s)
+res["codec_roundtrip_exact"] = bool(torch.equal(back, a))
+ref = torch.zeros_like(a)
+dev.ca_step_dev(c, a.data_ptr(), ref.data_ptr(), nbb.CaRule(), s)
+dev.ca_compact_step_dev(c, c1.data_ptr(), c2.data_ptr(), nbb.CaRule(), s)
+dev.compact_load_dev(c, c2.data_ptr(), back.data_ptr(), 0, s)
+res["ca_matches_int64_tile"] = bool(torch.equal(back, ref))
 res["compact_bytes_per_pass"] = 3 ** r * 8
 res["ca_compact_GBps"] = 2 * 3 ** r * 8 / (res["ca_compact_ms"] * 1e-3) / 1e9
 print(json.dumps(res))
