@@ -1,21 +1,22 @@
 #!/usr/bin/env python
-"""Benchmark of the λ(ω) hot path on B200.
+"""Benchmark of the λ(ω) hot path on B200 (see DESIGN.md §5 Measurement).
 
-Headline (BASELINE.json metric, config C3): one cellular-automaton step (B3/S23) of
-the Sierpinski gasket embedded at n = 2^16, int64 cells (the reference's Grid),
-launched over the compact λ(ω) orthotope with ρ = 32 — `value` = member-cell
-updates per second (3^16 per step) with the grid resident in HBM. Alongside: the
-same step through the bounding-box (BB) launch (paper-faithful per-cell BB and the
-sector-vectorised BB), the single-write and reduction workloads, the uint8-state
-variant, the HBM roofline of the dominant kernel, the reference CPU path timed on
-this host (`cpu_baseline`), and `e2e` = the same metric through the public C ABI
-call nbb_gpu_ca() with host buffers (H2D of the initial grid and D2H of the result
-inside the timed region).
+Headline (BASELINE.json metric, config C3): one cellular-automaton step (B3/S23) of the
+Sierpinski gasket at n = 2^16 launched over the λ(ω) orthotope (ρ = 32 tiles), with the
+CA state resident in HBM in the λ-ordered compact layout (the reference's CompactGrid,
+block_map.hpp:82-110: every byte a member value) — `value` = member-cell updates per
+second (3^16 per step). The same step on the reference's own int64 embedded Grid layout
+is reported beside it (`embedded_int64`), as are the bounding-box (BB) launches
+(paper-faithful per-cell BB and the sector-vectorised BB), the uint8 / 1-bit states, the
+single-write and reduction workloads, the C4 map sweep, the HBM roofline of the dominant
+kernel, the reference CPU path timed on this host (`cpu_baseline`), and `e2e` = the same
+metric through the public C ABI call nbb_gpu_ca() with pinned host buffers (the
+reference's int64 Grid in and out; transfers inside the timed region).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun (one process per GPU): the tile ordinal range is split in
-contiguous chunks (dispatch.cpp:419-427) and CA halo cells cross ranks via NCCL.
+N > 1 runs under torchrun (one process per GPU): the tile range is split in contiguous
+chunks (dispatch.cpp:419-427) and CA halo cells cross ranks via NCCL.
 """
 from __future__ import annotations
 
@@ -148,9 +149,9 @@ def run_reference_arm(args):
     line = {
         "metric": METRIC, "value": value, "unit": "cells/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": steps, "warmup": 0, "ms_per_step": 1e3 * secs / steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic: random_member_grid(gasket, 16, seed=17, modulus=2), B3/S23",
-        "config": config_block(r, rho),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": f"synthetic: random_member_grid(gasket, {r}, seed=17, modulus=2), B3/S23",
+        "config": config_block(r, rho, args.gpus),
         "cpu_baseline": {"value": value, "unit": "cells/s", "cores": cores, "kind": "reference",
                          "sample": f"reference run_ca(r={r}, rho={rho}, lambda/subbox/direct, "
                                    f"workers={cores}) for {steps} steps in one call; wall time of "
@@ -161,12 +162,15 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
-def config_block(r, rho):
+def config_block(r, rho, world=1):
     return {"workload": f"C3: gasket n=2^{r} cellular-automaton step (B3/S23), lambda(omega) launch, "
-                        f"rho={rho}, int64 embedded grid (reference Grid layout)",
+                        f"rho={rho} tiles; device state = the lambda-ordered compact layout "
+                        f"(CompactGrid, 8 B per member), host I/O = the reference's int64 Grid",
             "r": r, "n": 1 << r, "rho": rho, "mode": "lambda", "cells_per_step": 3 ** r,
-            "cell": "int64", "parallelism": "tile-range shards" ,
-            "l2": "no flush: each step touches 1.22 GB (> 126 MB L2)"}
+            "cell": "int64", "state": "compact",
+            "parallelism": f"{world} rank(s): contiguous tile-range shards + NCCL halo exchange"
+                           if world > 1 else "1 GPU",
+            "l2": "no flush: each step moves 689 MB compact / 1.7 GB embedded (> 126 MB L2)"}
 
 
 # ---------------------------------------------------------------------------------
@@ -190,6 +194,7 @@ def main():
         return
 
     import torch
+    from paper_2004_13475_b200 import _abi as nbb_abi
     from paper_2004_13475_b200 import device as dev
     from paper_2004_13475_b200 import nbb
 
@@ -240,9 +245,12 @@ def main():
     b = torch.zeros_like(a)
     torch.cuda.synchronize()
 
-    # shard of the tile range for this rank (weak: every rank owns one contiguous chunk)
+    # shards of the tile range for this rank: every rank owns one contiguous chunk and all
+    # ranks together update the 3^r cells of one step (the per-GPU share shrinks with N)
     from paper_2004_13475_b200 import shard
     plan = shard.ShardPlan(r=r, rho=32, world=world, rank=rank)
+    plan_c = shard.ShardPlan(r=r, rho=32, world=world, rank=rank, state="compact")
+    launches_per_step = 1 if world == 1 else 3  # + halo gather and scatter kernels
 
     def ca_runner(c, src, dst):
         bufs = [src, dst]
@@ -257,6 +265,20 @@ def main():
             else:
                 dev.ca_step_dev(c, bufs[i & 1].data_ptr(), bufs[(i + 1) & 1].data_ptr(),
                                 nbb.CaRule(), s)
+            state["i"] = i + 1
+        return step
+
+    def compact_runner(c, src, dst):
+        bufs = [src, dst]
+        state = {"i": 0}
+        lc = plan_c.local_config(c) if world > 1 else c
+
+        def step():
+            i = state["i"]
+            if world > 1:
+                plan_c.exchange_halo(bufs[i & 1], dist)
+            dev.ca_compact_step_dev(lc, bufs[i & 1].data_ptr(), bufs[(i + 1) & 1].data_ptr(),
+                                    nbb.CaRule(), s)
             state["i"] = i + 1
         return step
 
@@ -278,7 +300,15 @@ def main():
         barrier()
         return max_over_ranks(e0.elapsed_time(e1)) / K  # ms per step
 
+    # the compact CA state (λ-ordered CompactGrid): every byte a member value (int64)
+    c1 = torch.empty(members, dtype=torch.int64, device="cuda")
+    c2 = torch.empty_like(c1)
+    dev.compact_store_dev(cfg(), a.data_ptr(), c1.data_ptr(), s)
+
     if args.profile:
+        run = compact_runner(cfg(), c1, c2)
+        for _ in range(3):
+            run()
         for c in (cfg(), cfg(mode=nbb.MapMode.BoundingBox),
                   cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell)):
             run = ca_runner(c, a, b)
@@ -291,11 +321,13 @@ def main():
     sampler = ClockSampler(local)
     results = {}
 
-    # ---- headline: λ(ω) CA step, int64, ρ = 32 (tile kernel) -----------------------------
-    ms = timed(ca_runner(cfg(), a, b), K, W, sampler)
-    head_ms = ms
-    value = world * 0 + members * 1e3 / ms  # all ranks together update the 3^r cells per step
-    results["ca_lambda_tile_rho32_i64"] = ms
+    # ---- headline: λ(ω) CA step on the compact state, ρ = 32 tiles ---------------------
+    head_ms = timed(compact_runner(cfg(), c1, c2), K, W, sampler)
+    value = members * 1e3 / head_ms  # all ranks together update the 3^r cells per step
+    results["ca_lambda_compact_i64"] = head_ms
+    # ---- the same step on the reference's int64 embedded Grid layout --------------------
+    emb_ms = timed(ca_runner(cfg(), a, b), K, W)
+    results["ca_lambda_tile_rho32_i64"] = emb_ms
 
     # the other CA launch shapes (each on its own timed loop; K shortened for slow BB)
     variants = {
@@ -309,14 +341,13 @@ def main():
         "ca_lambda_percell_rho32_i64": cfg(kernel=nbb.KernelFamily.PerCell),
         "ca_lambda_percell_rho16_i64": cfg(rho=16, kernel=nbb.KernelFamily.PerCell),
     }
+    sweep = None
     if world == 1:
         for name, c in variants.items():
             kk = K if "tile" in name else max(5, K // 10)
             results[name] = timed(ca_runner(c, a, b), kk, W)
 
-    sweep = None
-    # uint8 / 1-bit alive states (exact: CA only reads != 0 and writes 0/1)
-    if world == 1:
+        # uint8 / 1-bit alive states (exact: CA only reads != 0 and writes 0/1)
         a8 = torch.zeros((n, n), dtype=torch.uint8, device="cuda")
         b8 = torch.zeros_like(a8)
         dev.pack_alive_dev(cfg(cell_width=1), a.data_ptr(), a8.data_ptr(), s)
@@ -347,24 +378,10 @@ def main():
                         "rd_bb_percell_rho32": cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell),
                         "rd_lambda_percell_rho16": cfg(rho=16, kernel=nbb.KernelFamily.PerCell)}.items():
             results[name] = timed(rd(c), K if "tile" in name else max(5, K // 10), W)
-
-        # the compact (λ-ordered CompactGrid) state: every byte a member value (int64)
-        c1 = torch.empty(members, dtype=torch.int64, device="cuda")
-        c2 = torch.empty_like(c1)
-        dev.compact_store_dev(cfg(), a.data_ptr(), c1.data_ptr(), s)
-        cbufs = [c1, c2]
-        cstate = {"i": 0}
-
-        def ca_compact():
-            i = cstate["i"]
-            dev.ca_compact_step_dev(cfg(), cbufs[i & 1].data_ptr(), cbufs[(i + 1) & 1].data_ptr(),
-                                    nbb.CaRule(), s)
-            cstate["i"] = i + 1
-        results["ca_lambda_compact_i64"] = timed(ca_compact, K, W)
         results["rd_lambda_compact_i64"] = timed(
             lambda: dev.reduction_compact_dev(cfg(), c1.data_ptr(), out.data_ptr(), s), K, W)
-        results["sw_lambda_compact_i64"] = timed(lambda: dev.single_write_compact_dev(cfg(), c2.data_ptr(), s), K, W)
-        del c1, c2, cbufs
+        results["sw_lambda_compact_i64"] = timed(
+            lambda: dev.single_write_compact_dev(cfg(), c2.data_ptr(), s), K, W)
 
         # C4: the λ map alone over a whole orthotope, scalar closed form vs tensor core (K0-TC)
         xy = torch.empty(3 ** 17 * 2, dtype=torch.int32, device="cuda")
@@ -380,55 +397,66 @@ def main():
                 row[label + "_omega_per_s"] = 3 ** lvl * 1e3 / ms
             sweep[str(lvl)] = row
         del xy
+    del c1, c2
 
-    # ---- roofline of the dominant kernel ----------------------------------------------
+    # ---- roofline of the dominant kernel (ca_compact_kernel) ---------------------------
     peak, peak_kind = measured_peaks()
-    alg_bytes = 2 * layout_bytes_per_pass(r, 8)  # read src + write dst, per launch
+    alg_bytes = 2 * 8 * members            # read src + write dst, 8 B per member, per launch
     achieved = alg_bytes / (head_ms * 1e-3) / 1e9
-    traffic = None
+    traffic = emb_traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
         with open(tf) as f:
-            traffic = json.load(f).get("ca_lambda_tile_rho32_i64")
+            tj = json.load(f)
+        traffic = tj.get("ca_lambda_compact_i64")
+        emb_traffic = tj.get("ca_lambda_tile_rho32_i64")
+    emb_alg = 2 * layout_bytes_per_pass(r, 8)  # 32-byte sectors holding a member, read + write
+    emb_achieved = emb_alg / (emb_ms * 1e-3) / 1e9
 
     # ---- e2e through the public C ABI with pinned host buffers -------------------------
-    # nbb_gpu_ca(cfg, host_initial, K steps, rule, host_out): the initial state crosses PCIe
-    # (member sectors read in place from the pinned grid), K steps run, the result comes
-    # back (member sectors written in place into the pinned output, FLAG_OUT_ZEROED: the
-    # output buffer was allocated zeroed once, outside the timed region). One call = K steps.
+    # nbb_gpu_ca(cfg, host_initial, K steps, rule, host_out) = the reference's
+    # run_ca(cfg, grid, K): the int64 Grid crosses PCIe in (member sectors read in place from
+    # the pinned grid), K steps run on the device state, the result comes back (member
+    # sectors written in place into the pinned output, FLAG_OUT_ZEROED: allocated zeroed
+    # once, outside the timed region). One call = K steps; a 1-step call is timed too.
     e2e = None
     if world == 1 and not args.no_e2e:
-        del b
+        del a, b
         torch.cuda.empty_cache()
         hin = torch.empty((n, n), dtype=torch.int64, pin_memory=True)
         hout = torch.zeros((n, n), dtype=torch.int64).pin_memory()
         lib = nbb._lib()
         lib.nbb_gpu_random_member_grid(ctypes.byref(spec.to_c()), r, 17, 2, n * n,
                                        ctypes.c_void_p(hin.data_ptr()))
-        del a
-        torch.cuda.empty_cache()
         member_bytes = layout_bytes_per_pass(r, 8)
         runs = {}
-        for label, cw in (("int64", 8), ("bit", 0)):
-            cc = cfg(cell_width=cw, flags=1).to_c()
-            lib.nbb_gpu_ca(ctypes.byref(cc), ctypes.c_void_p(hin.data_ptr()), r, 2, 8, 12,
-                           ctypes.c_void_p(hout.data_ptr()), None)  # warm (allocations)
+
+        def call(cc, steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            rc = lib.nbb_gpu_ca(ctypes.byref(cc), ctypes.c_void_p(hin.data_ptr()), r, K, 8, 12,
+            rc = lib.nbb_gpu_ca(ctypes.byref(cc), ctypes.c_void_p(hin.data_ptr()), r, steps, 8, 12,
                                 ctypes.c_void_p(hout.data_ptr()), None)
             t1 = time.perf_counter()
             if rc:
                 raise RuntimeError(lib.nbb_gpu_last_error().decode())
-            runs[label] = t1 - t0
-        e2e = {"value": members * K / runs["int64"], "unit": "cells/s",
+            return t1 - t0
+        for label, cw, fl in (("compact", 8, nbb_abi.FLAG_COMPACT_STATE), ("int64", 8, 0), ("bit", 0, 0)):
+            cc = cfg(cell_width=cw, flags=nbb_abi.FLAG_OUT_ZEROED | fl).to_c()
+            call(cc, 2)  # warm (allocations)
+            runs[label] = call(cc, K)
+            if label == "compact":
+                runs["compact_1step"] = min(call(cc, 1) for _ in range(3))
+        e2e = {"value": members * K / runs["compact"], "unit": "cells/s",
                "h2d_bytes_per_step": member_bytes // K, "d2h_bytes_per_step": member_bytes // K,
-               "call": f"nbb_gpu_ca(cfg int64 state, pinned host_initial, steps={K}, B3/S23, pinned "
-                       f"host_out, FLAG_OUT_ZEROED): member sectors of the 32 GiB grids cross PCIe "
-                       f"in place (zero-copy), wall time of the whole call",
-               "seconds": runs["int64"],
-               "bit_state": {"value": members * K / runs["bit"], "seconds": runs["bit"],
-                             "call": "same call with cell_width=0 (1-bit alive state on device)"}}
+               "call": f"nbb_gpu_ca(cfg, pinned host_initial int64 Grid, steps={K}, B3/S23, pinned "
+                       f"host_out, FLAG_OUT_ZEROED|FLAG_COMPACT_STATE) = the reference's run_ca(cfg, "
+                       f"grid, {K}); the {member_bytes / 1e6:.0f} MB of member sectors cross PCIe in place "
+                       f"(zero-copy) each way per call; wall time of the whole call",
+               "seconds": runs["compact"],
+               "one_step_call": {"value": members / runs["compact_1step"], "seconds": runs["compact_1step"],
+                                 "h2d_bytes_per_step": member_bytes, "d2h_bytes_per_step": member_bytes},
+               "other_states": {k: {"value": members * K / runs[k], "seconds": runs[k]}
+                                for k in ("int64", "bit")}}
         del hin, hout
         nbb.release()
 
@@ -451,39 +479,45 @@ def main():
     if rank != 0:
         return
     cells = lambda k: members * 1e3 / results[k] if k in results else None  # noqa: E731
-    best_bb = min((results[k] for k in results if k.startswith("ca_bb") and k.endswith("i64")),
-                  default=None)
-    best_bb_percell = min((results[k] for k in results if k.startswith("ca_bb_percell")), default=None)
 
     def ratio(bb, lam):
         return results[bb] / results[lam] if bb in results and lam in results else None
     line = {
         "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": K,
-        "warmup": W, "ms_per_step": head_ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": W, "ms_per_step": head_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic: random_member_grid(gasket, 16, seed=17, modulus=2) generated "
+        "data": f"synthetic: random_member_grid(gasket, {r}, seed=17, modulus=2) generated "
                 "bit-identically on device, B3/S23",
-        "config": config_block(r, 32),
-        "gpu_launches": K,
+        "config": config_block(r, 32, world),
+        "gpu_launches": K * launches_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
-                     "kernel": "ca_pipe_kernel<int64, rho=32, lambda, 2 stages, 8 warps>"},
+                     "kernel": "ca_compact_kernel (8 B read + 8 B write per member cell)"},
+        "embedded_int64": {
+            "note": "the same step on the reference's int64 embedded Grid (ca_pipe_kernel)",
+            "ms_per_step": emb_ms, "value": members * 1e3 / emb_ms,
+            "roofline": {"achieved": emb_achieved, "peak": peak, "frac": emb_achieved / peak,
+                         "alg_bytes_per_launch": emb_alg, "traffic": emb_traffic,
+                         "alg": "32-byte sectors holding a member (SURVEY 8(d)), read + write"},
+            "line_granular_floor": {
+                "note": "B200 reads whole 128 B lines (probe: tools/probe_dram3.cu); int64 lines "
+                        "holding a member: 2^4*3^12 x 128 B = 1088.4 MB read + 612.2 MB sector writes",
+                "hw_min_bytes_per_step": 1088391168 + 612220032,
+                "achieved_GBps_vs_hw_min": (1088391168 + 612220032) / (emb_ms * 1e-3) / 1e9},
+        },
         "clocks": sampler.summary(),
         "speedup_vs_bb": {
-            "ca_i64_best_bb_over_lambda": (best_bb / head_ms) if best_bb else None,
-            "ca_i64_paper_bb_percell_over_lambda": (best_bb_percell / head_ms) if best_bb_percell else None,
+            "ca_lambda_compact_over_bb_tile_i64": ratio("ca_bb_tile_rho32_i64", "ca_lambda_compact_i64"),
+            "ca_lambda_compact_over_bb_percell_i64": ratio("ca_bb_percell_rho32_i64", "ca_lambda_compact_i64"),
+            "ca_embedded_i64_bb_tile_over_lambda_tile": ratio("ca_bb_tile_rho32_i64", "ca_lambda_tile_rho32_i64"),
+            "ca_embedded_i64_bb_percell_over_lambda_percell": ratio("ca_bb_percell_rho32_i64",
+                                                                   "ca_lambda_percell_rho32_i64"),
             "ca_u8_bb_over_lambda": ratio("ca_bb_tile_rho32_u8", "ca_lambda_tile_rho32_u8"),
             "ca_bit_bb_over_lambda": ratio("ca_bb_tile_rho32_bit", "ca_lambda_tile_rho32_bit"),
-            "ca_compact_vs_bb_i64": ratio("ca_bb_tile_rho32_i64", "ca_lambda_compact_i64"),
-            "sw_best_bb_over_lambda": ratio("sw_bb_tile_rho32", "sw_lambda_tile_rho32"),
-            "rd_best_bb_over_lambda": ratio("rd_bb_tile_rho32", "rd_lambda_tile_rho32"),
-        },
-        "line_granular_floor": {
-            "note": "B200 reads whole 128 B lines (probe: tools/probe_dram3.cu); int64 lines holding "
-                    "a member: 2^4*3^12 x 128 B = 1088.4 MB read + 612.2 MB sector writes per step",
-            "hw_min_bytes_per_step": 1088391168 + 612220032,
-            "achieved_GBps_vs_hw_min": (1088391168 + 612220032) / (head_ms * 1e-3) / 1e9,
+            "sw_bb_tile_over_lambda_tile": ratio("sw_bb_tile_rho32", "sw_lambda_tile_rho32"),
+            "rd_bb_tile_over_lambda_tile": ratio("rd_bb_tile_rho32", "rd_lambda_tile_rho32"),
+            "rd_bb_tile_over_lambda_compact": ratio("rd_bb_tile_rho32", "rd_lambda_compact_i64"),
         },
         "workloads_ms": results,
         "workloads_cells_per_s": {k: cells(k) for k in results},

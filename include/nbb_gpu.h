@@ -225,7 +225,10 @@ int nbb_gpu_compact_write(const char* path, const nbb_spec* spec, int32_t level,
 int nbb_gpu_compact_read(const char* path, const nbb_spec* spec, int32_t* level, int64_t* values,
                          uint64_t capacity);
 /* Workloads on device-resident compact state (gasket; CA needs r >= 5): one CA step
- * d_src -> d_dst, the member sum, the single write (every member value = 1). */
+ * d_src -> d_dst, the member sum, the single write (every member value = 1).
+ * The CA step honours shard_begin/shard_count over the compact tile order
+ * u = ωx_b·H_b + ωy_b of the ρ = 32 tiles (a contiguous u range = contiguous compact
+ * rows), so each rank of the multi-GPU path updates one slab of the compact array. */
 int nbb_gpu_ca_compact_step_dev(const nbb_config* cfg, const void* d_src, void* d_dst,
                                 uint16_t birth, uint16_t survive, void* stream, nbb_report* report);
 int nbb_gpu_reduction_compact_dev(const nbb_config* cfg, const void* d_compact, void* d_value,

@@ -155,6 +155,7 @@ struct CompactCaArgs {
     int rb;            // block level r - 5
     int64_t n;         // embedding side
     uint32_t tiles;    // Wb * Hb
+    uint32_t tile_begin, tile_end;  // the CA step's shard of the tile order u (all: 0, tiles)
     uint32_t birth, survive;
 };
 
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
     const uint32_t warp_stride = (gridDim.x * blockDim.x) >> 5;
     __syncwarp();
 
-    for (uint32_t u = warp_global; u < a.tiles; u += warp_stride) {
+    for (uint32_t u = a.tile_begin + warp_global; u < a.tile_end; u += warp_stride) {
         const uint32_t wxb = fastdiv(u, div_hb), wyb = u - wxb * a.Hb;
         const long long* src = a.src + (uint64_t)(9u * wxb) * a.W + 27u * wyb;
         long long v[8];

@@ -647,6 +647,12 @@ CompactCaArgs compact_args(const nbb_config* cfg, const void* src, void* dst, ui
     a.Hb = (uint32_t)hb;
     a.n = (int64_t)1 << cfg->r;
     a.tiles = a.Wb * a.Hb;
+    a.tile_begin = 0;
+    a.tile_end = a.tiles;
+    if (cfg->shard_count > 0) {
+        a.tile_begin = (uint32_t)std::min<uint64_t>(cfg->shard_begin, a.tiles);
+        a.tile_end = (uint32_t)std::min<uint64_t>(a.tile_begin + cfg->shard_count, a.tiles);
+    }
     a.birth = birth;
     a.survive = survive;
     div_hb->d = a.Hb;
@@ -684,7 +690,8 @@ int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, vo
         NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ca_compact_kernel, 256, 0));
         if (occ < 1) occ = 1;
     }
-    const uint64_t want = (a.tiles + 7) / 8;
+    const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
+    if (want == 0) return NBB_OK;
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
     ca_compact_kernel<<<blocks, 256, 0, st>>>(a, div_hb);
     NBB_CUDA(cudaGetLastError());

@@ -13,6 +13,11 @@ lists are computed once here (host logic, numpy), packed/unpacked by the library
 gather/scatter kernels and moved by one NCCL all_to_all_single. Every rank keeps a
 full replica of the embedded grid (identical addresses on every rank), of which it
 only reads its own tiles plus the received halo cells.
+
+state="compact" partitions the λ-ordered compact CA state (ρ = 32 tiles) instead: the
+tiles are taken in the compact kernel's order u = ωx_b·H_b + ωy_b (a contiguous u range
+is a contiguous slab of compact rows), and the exchanged indices are compact offsets
+ωy·W + ωx of the halo cells (λ⁻¹ at full level). Same chunk rule, same ≤ 8 cells per tile.
 """
 from __future__ import annotations
 
@@ -84,12 +89,18 @@ class ShardPlan:
     send_counts: list = field(default=None)
     recv_idx: np.ndarray = field(default=None, repr=False)   # grouped by source
     recv_counts: list = field(default=None)
+    state: str = "embedded"   # or "compact" (λ-ordered CompactGrid CA state, ρ = 32)
     _dev: dict = field(default_factory=dict, repr=False)
 
     def __post_init__(self):
+        if self.state not in ("embedded", "compact"):
+            raise ValueError(f"unknown state '{self.state}'")
+        if self.state == "compact" and self.rho != 32:
+            raise ValueError("the compact CA state uses rho = 32 tiles")
         rt = self.rho.bit_length() - 1
         self.r_b = self.r - rt
         self.W = 3 ** ((self.r_b + 1) // 2)
+        self.Hb = 3 ** (self.r_b // 2)
         self.total = 3 ** self.r_b
         self.chunk = -(-self.total // self.world)
         self.begin = min(self.rank * self.chunk, self.total)
@@ -103,10 +114,26 @@ class ShardPlan:
     def owner(self, ordinals: np.ndarray) -> np.ndarray:
         return ordinals // self.chunk
 
+    def ordinal_of_tile(self, t: np.ndarray) -> np.ndarray:
+        """Block ordinal ωy_b·W + ωx_b of tile ids in this plan's order."""
+        if self.state == "compact":
+            return (t % self.Hb) * self.W + t // self.Hb
+        return t
+
+    def tile_of_ordinal(self, o: np.ndarray) -> np.ndarray:
+        if self.state == "compact":
+            return (o % self.W) * self.Hb + o // self.W
+        return o
+
+    def owned_blocks(self):
+        """(bx, by) block coordinates of this rank's tiles."""
+        t = np.arange(self.begin, self.begin + self.count, dtype=np.int64)
+        return lambda_blocks(self.ordinal_of_tile(t), self.W)
+
     def _build_halo_lists(self):
         n, rho = 1 << self.r, self.rho
         t = np.arange(self.total, dtype=np.int64)
-        bx, by = lambda_blocks(t, self.W)
+        bx, by = lambda_blocks(self.ordinal_of_tile(t), self.W)
         off = _halo_offsets(rho)
         cx = (bx * rho)[:, None] + off[None, :, 0]
         cy = (by * rho)[:, None] + off[None, :, 1]
@@ -115,10 +142,13 @@ class ShardPlan:
         cx, cy, needer = cx[ok], cy[ok], needer[ok]
         memb = (cx & (n - 1 - cy)) == 0
         cx, cy, needer = cx[memb], cy[memb], needer[memb]
-        own_t = lambda_inverse_blocks(cx // rho, cy // rho, self.r_b, self.W)
+        own_t = self.tile_of_ordinal(lambda_inverse_blocks(cx // rho, cy // rho, self.r_b, self.W))
         src = self.owner(own_t)
         remote = src != needer
-        flat = (cy * n + cx)[remote]
+        if self.state == "compact":  # compact offset ωy·W + ωx of the cell
+            flat = lambda_inverse_blocks(cx[remote], cy[remote], self.r, 3 ** ((self.r + 1) // 2))
+        else:
+            flat = (cy * n + cx)[remote]
         src, needer = src[remote], needer[remote]
         # unique (needer, src, cell) triples in a canonical order both sides agree on
         key = np.unique(np.stack([needer, src, flat], axis=1), axis=0)

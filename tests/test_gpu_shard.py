@@ -30,34 +30,50 @@ def _worker(rank, world, port, r, rho, steps, cell_width, q):
     torch.cuda.set_device(0)
     from paper_2004_13475_b200 import device as dev
     from paper_2004_13475_b200 import nbb
-    from paper_2004_13475_b200.shard import ShardPlan, lambda_blocks
+    from paper_2004_13475_b200.shard import ShardPlan, lambda_blocks, lambda_inverse_blocks
     n = 1 << r
-    plan = ShardPlan(r=r, rho=rho, world=world, rank=rank)
+    compact = cell_width == "compact"
+    plan = ShardPlan(r=r, rho=rho, world=world, rank=rank, state="compact" if compact else "embedded")
     g = orc_random_member_grid(r, 4321, 2)
-    dt = torch.int64 if cell_width == 8 else torch.uint8
-    a = torch.from_numpy(g).to(dt).cuda()
+    if compact:  # the λ-ordered compact state: slot c holds cell λ(c)
+        cx, cy = lambda_blocks(np.arange(3 ** r, dtype=np.int64), 3 ** ((r + 1) // 2))
+        a = torch.from_numpy(g[cy, cx].copy()).cuda()
+        c = nbb.DispatchConfig(r=r, rho=rho, max_cells=n * n)
+    else:
+        dt = torch.int64 if cell_width == 8 else torch.uint8
+        a = torch.from_numpy(g).to(dt).cuda()
+        c = nbb.DispatchConfig(r=r, rho=rho, max_cells=n * n, cell_width=cell_width)
     b = torch.zeros_like(a)
-    c = nbb.DispatchConfig(r=r, rho=rho, max_cells=n * n, cell_width=cell_width)
     lc = plan.local_config(c)
     s = torch.cuda.current_stream().cuda_stream
     for _ in range(steps):
         plan.exchange_halo(a, dist)
-        dev.ca_step_dev(lc, a.data_ptr(), b.data_ptr(), nbb.CaRule(), s)
+        if compact:
+            dev.ca_compact_step_dev(lc, a.data_ptr(), b.data_ptr(), nbb.CaRule(), s)
+        else:
+            dev.ca_step_dev(lc, a.data_ptr(), b.data_ptr(), nbb.CaRule(), s)
         a, b = b, a
     torch.cuda.synchronize()
-    own = np.zeros((n, n), dtype=bool)
-    t = np.arange(plan.begin, plan.begin + plan.count, dtype=np.int64)
-    bx, by = lambda_blocks(t, plan.W)
-    for x0, y0 in zip(bx * rho, by * rho):
-        own[y0:y0 + rho, x0:x0 + rho] = True
-    mine = torch.where(torch.from_numpy(own), a.cpu().to(torch.int64), torch.zeros(n, n, dtype=torch.int64))
+    if compact:
+        tile = plan.tile_of_ordinal(lambda_inverse_blocks(cx >> 5, cy >> 5, plan.r_b, plan.W))
+        mine_c = torch.where(torch.from_numpy(plan.owner(tile) == rank), a.cpu(), torch.zeros_like(a.cpu()))
+        mine = torch.zeros(n, n, dtype=torch.int64)
+        mine[torch.from_numpy(cy), torch.from_numpy(cx)] = mine_c
+    else:
+        own = np.zeros((n, n), dtype=bool)
+        bx, by = plan.owned_blocks()
+        for x0, y0 in zip(bx * rho, by * rho):
+            own[y0:y0 + rho, x0:x0 + rho] = True
+        mine = torch.where(torch.from_numpy(own), a.cpu().to(torch.int64),
+                           torch.zeros(n, n, dtype=torch.int64))
     dist.all_reduce(mine)
     if rank == 0:
         q.put(mine.numpy())
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,r,rho,cw", [(2, 10, 32, 8), (3, 10, 16, 8), (2, 11, 32, 1)])
+@pytest.mark.parametrize("world,r,rho,cw", [(2, 10, 32, 8), (3, 10, 16, 8), (2, 11, 32, 1),
+                                           (2, 10, 32, "compact"), (3, 11, 32, "compact")])
 def test_sharded_ca_on_gpu(world, r, rho, cw):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -38,8 +38,7 @@ def _ca_owned_tiles(src: np.ndarray, plan: ShardPlan, birth=8, survive=12) -> np
     rule = np.where(alive == 1, (survive >> live) & 1, (birth >> live) & 1)
     nxt = (rule & member).astype(np.int64)
     out = src.copy()
-    t = np.arange(plan.begin, plan.begin + plan.count, dtype=np.int64)
-    bx, by = lambda_blocks(t, plan.W)
+    bx, by = plan.owned_blocks()
     for x0, y0 in zip(bx * rho, by * rho):
         out[y0:y0 + rho, x0:x0 + rho] = nxt[y0:y0 + rho, x0:x0 + rho]
     return out
@@ -88,12 +87,59 @@ def test_sharded_ca_matches_single_domain(world, r, rho):
     assert halo > 0
 
 
+def _compact_worker(rank, world, port, r, steps, q):
+    """The compact-state partition: each rank holds a replica of the λ-ordered compact
+    array, owns a contiguous range of the compact tile order, and exchanges halo cells by
+    compact offset."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    plan = ShardPlan(r=r, rho=32, world=world, rank=rank, state="compact")
+    n = 1 << r
+    cx, cy = lambda_blocks(np.arange(3 ** r, dtype=np.int64), 3 ** ((r + 1) // 2))  # λ of each slot
+    tile = plan.tile_of_ordinal(lambda_inverse_blocks(cx >> 5, cy >> 5, plan.r_b, plan.W))
+    own = torch.from_numpy(plan.owner(tile) == rank)
+    g = torch.from_numpy(orc_random_member_grid(r, 1234, 2)[cy, cx].copy())
+    g[~own] = 7  # stale garbage outside the owned slab
+    gather = lambda flat, idx: flat[idx].clone()  # noqa: E731
+    def scatter(flat, idx, vals):
+        flat[idx] = vals
+    for _ in range(steps):
+        plan.exchange_halo(g, dist, gather=gather, scatter=scatter)
+        emb = np.zeros((n, n), dtype=np.int64)
+        emb[cy, cx] = g.numpy()
+        nxt = _ca_owned_tiles(emb, plan)
+        g = torch.where(own, torch.from_numpy(nxt[cy, cx].copy()), g)
+    full = torch.where(own, g, torch.zeros_like(g))
+    dist.all_reduce(full)
+    if rank == 0:
+        q.put((full.numpy(), plan.halo_cells_received()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,r", [(2, 8), (3, 9)])
+def test_sharded_compact_ca_matches_single_domain(world, r):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_compact_worker, args=(i, world, port, r, 4, q)) for i in range(world)]
+    for p in procs:
+        p.start()
+    got, halo = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cx, cy = lambda_blocks(np.arange(3 ** r, dtype=np.int64), 3 ** ((r + 1) // 2))
+    want = orc_ca(r, orc_random_member_grid(r, 1234, 2), 4)[cy, cx]
+    assert np.array_equal(got, want)
+    assert halo > 0
+
+
 def test_halo_lists_are_symmetric_and_small():
     """App. A.5: each tile needs <= 8 remote cells; what rank a receives from b is
     exactly what b sends to a."""
     r, rho = 12, 32
-    for world in (2, 4, 8):
-        plans = [ShardPlan(r=r, rho=rho, world=world, rank=k) for k in range(world)]
+    for world, state in ((2, "embedded"), (4, "embedded"), (8, "embedded"), (2, "compact"), (8, "compact")):
+        plans = [ShardPlan(r=r, rho=rho, world=world, rank=k, state=state) for k in range(world)]
         for a in range(world):
             assert sum(p.count for p in plans) == 3 ** (r - 5)
             for b in range(world):
