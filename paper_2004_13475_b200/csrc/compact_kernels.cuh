@@ -182,19 +182,40 @@ __device__ __forceinline__ uint64_t gasket_compact_offset(uint32_t x, uint32_t y
     return (uint64_t)oy * W + ox;
 }
 
+// The 8 halo cells of every ρ = 32 tile as compact offsets (-1: not a member / outside),
+// [tile u][k] for the tile-local positions (-1,-1) (0,-1) (1,-1) (-1,31) (32,30) (32,31)
+// (32,32) (0,32). Static per level; built once per device and level (5.7 MB at r = 16) so
+// the CA step spends one 32-byte load per tile instead of λ + λ⁻¹ arithmetic.
+__global__ void compact_halo_table_kernel(CompactCaArgs a, FastDiv div_hb, int32_t* tab) {
+    const uint32_t nm1 = (uint32_t)(a.n - 1);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (uint64_t)a.tiles * 8u;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = (uint32_t)(i >> 3), hk = (uint32_t)i & 7u;
+        const int hx = (hk == 0 || hk == 3) ? -1 : (hk == 1 || hk == 7) ? 0 : (hk == 2) ? 1 : 32;
+        const int hy = (hk <= 2) ? -1 : (hk == 3 || hk == 5) ? 31 : (hk == 4) ? 30 : 32;
+        const uint32_t wxb = fastdiv(u, div_hb), wyb = u - wxb * a.Hb;
+        uint32_t bx, by;
+        lambda_arith(wxb, wyb, bx, by);
+        const uint32_t gx = bx * 32u + (uint32_t)hx, gy = by * 32u + (uint32_t)hy;  // wraps if < 0
+        const bool ok = gx <= nm1 && gy <= nm1 && (gx & (nm1 - gy)) == 0u;
+        tab[i] = ok ? (int32_t)gasket_compact_offset(gx, gy, a.W) : -1;
+    }
+}
+
 // One warp per tile; tile u -> (ωx_b = u / Hb, ωy_b = u % Hb) so consecutive warps walk along a
 // compact row block. 243 values per tile = slots k = 0..7 of lane l: li = 32k + l (k < 7 valid
 // for every lane, k = 7 for lanes < 19).
 //
 // Per tile: 8 coalesced 8-byte loads per lane (compact rows of 27 values), the 8 halo cells
-// (compact offsets by the bit form of λ⁻¹), alive bits scattered as bytes into a per-warp
+// (compact offsets from the per-level halo table), alive bits scattered as bytes into a per-warp
 // 32 x 32 byte tile (non-member bytes stay 0, so no atomics and no clearing), rows packed back
 // to bit masks (lane = row) for the bit-sliced rule, and 8 stores per lane. The kernel is
 // issue-bound as much as DRAM-bound (ncu: ALU pipe 66%, long-scoreboard 61% of stalls),
 // hence the instruction diet. Tried and slower on B200 (profiles/r1_compact_ca_tuning.md):
 // a cp.async ring (8-byte copies), L2 bulk prefetch one tile ahead, 64/48-register budgets,
 // and cp.async.bulk row copies into an mbarrier ring.
-__global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, FastDiv div_hb) {
+__global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, FastDiv div_hb,
+                                                             const int32_t* __restrict__ halo_tab) {
     __shared__ __align__(16) uint8_t s_cell[8][32 * 32];
     __shared__ uint32_t s_new[8][32];
     __shared__ uint16_t s_pos[256];  // c_local_pos (per-lane constant-bank reads serialise)
@@ -208,36 +229,32 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
         const uint32_t li = 32u * k + lane;
         const bool ok = li < 243u;
         const uint32_t row = ok ? li / 27u : 0u, col = ok ? li % 27u : 0u;
-        sl_off[k] = row * a.W + col;  // element offset inside the tile's sub-block
-        sl_pos[k] = s_pos[li];        // x | y << 5 = byte index in the 32 x 32 tile
+        sl_off[k] = (row * a.W + col) * 8u;  // byte offset inside the tile's sub-block
+        sl_pos[k] = s_pos[li];               // x | y << 5 = byte index in the 32 x 32 tile
     }
     const bool k7 = lane < 19;
 #pragma unroll
     for (int i = 0; i < 8; ++i) reinterpret_cast<uint32_t*>(cell)[32 * i + lane] = 0u;
-    const uint32_t hk = (uint32_t)lane & 7u;
-    const int hx = (hk == 0 || hk == 3) ? -1 : (hk == 1 || hk == 7) ? 0 : (hk == 2) ? 1 : 32;
-    const int hy = (hk <= 2) ? -1 : (hk == 3 || hk == 5) ? 31 : (hk == 4) ? 30 : 32;
-    const uint32_t nm1 = (uint32_t)(a.n - 1);
     const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t warp_stride = (gridDim.x * blockDim.x) >> 5;
+    const char* src0 = reinterpret_cast<const char*>(a.src);
+    char* dst0 = reinterpret_cast<char*>(a.dst);
     __syncwarp();
 
-    for (uint32_t u = a.tile_begin + warp_global; u < a.tile_end; u += warp_stride) {
+    uint32_t u = a.tile_begin + warp_global;
+    int32_t hoff = (u < a.tile_end && lane < 8) ? __ldg(halo_tab + 8ull * u + lane) : -1;
+    for (; u < a.tile_end; u += warp_stride) {
         const uint32_t wxb = fastdiv(u, div_hb), wyb = u - wxb * a.Hb;
-        const long long* src = a.src + (uint64_t)(9u * wxb) * a.W + 27u * wyb;
+        const uint64_t base = ((uint64_t)(9u * wxb) * a.W + 27u * wyb) * 8u;
+        const char* src = src0 + base;
         long long v[8];
 #pragma unroll
-        for (int k = 0; k < 7; ++k) v[k] = __ldg(src + sl_off[k]);
-        v[7] = k7 ? __ldg(src + sl_off[7]) : 0ll;
-        // halo cell of lanes 0..7 (its compact offset from the bits of its coordinates)
-        uint32_t bx, by;
-        lambda_const(wxb, wyb, bx, by);
-        long long hv = 0;
-        {
-            const uint32_t gx = bx * 32u + (uint32_t)hx, gy = by * 32u + (uint32_t)hy;  // wraps if < 0
-            if (lane < 8 && gx <= nm1 && gy <= nm1 && (gx & (nm1 - gy)) == 0u)
-                hv = __ldg(a.src + gasket_compact_offset(gx, gy, a.W));
-        }
+        for (int k = 0; k < 7; ++k) v[k] = __ldg(reinterpret_cast<const long long*>(src + sl_off[k]));
+        v[7] = k7 ? __ldg(reinterpret_cast<const long long*>(src + sl_off[7])) : 0ll;
+        // halo cell of lanes 0..7 (offset from the table; the next tile's entry prefetched)
+        const long long hv = hoff >= 0 ? __ldg(a.src + hoff) : 0ll;
+        const uint32_t un = u + warp_stride;
+        hoff = (un < a.tile_end && lane < 8) ? __ldg(halo_tab + 8ull * un + lane) : -1;
 #pragma unroll
         for (int k = 0; k < 7; ++k) cell[sl_pos[k]] = v[k] != 0ll;
         if (k7) cell[sl_pos[7]] = v[7] != 0ll;
@@ -265,11 +282,14 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
                                      (uint32_t)(E >> 1), a.birth, a.survive) &
                            submask_bits((uint32_t)lane);
         __syncwarp();
-        long long* dst = a.dst + (src - a.src);
+        char* dst = dst0 + base;
 #pragma unroll
         for (int k = 0; k < 7; ++k)
-            dst[sl_off[k]] = (long long)((s_new[wib][sl_pos[k] >> 5] >> (sl_pos[k] & 31u)) & 1u);
-        if (k7) dst[sl_off[7]] = (long long)((s_new[wib][sl_pos[7] >> 5] >> (sl_pos[7] & 31u)) & 1u);
+            *reinterpret_cast<long long*>(dst + sl_off[k]) =
+                (long long)((s_new[wib][sl_pos[k] >> 5] >> (sl_pos[k] & 31u)) & 1u);
+        if (k7)
+            *reinterpret_cast<long long*>(dst + sl_off[7]) =
+                (long long)((s_new[wib][sl_pos[7] >> 5] >> (sl_pos[7] & 31u)) & 1u);
         __syncwarp();
     }
 }

@@ -72,6 +72,7 @@ struct DeviceCtx {
     void* bufs[3] = {nullptr, nullptr, nullptr};
     size_t buf_bytes[3] = {0, 0, 0};
     int16_t* lut[6] = {};                    // LocalCellTable per edge 2^i
+    int32_t* halo_tab[32] = {};              // compact CA halo table per level r
 };
 
 std::mutex g_mutex;
@@ -628,6 +629,8 @@ int compact_workload_check(const nbb_config* cfg) {
     NBB_TRY(nbbhost::require_gasket(cfg->spec));
     if (cfg->r < 5)
         return fail(NBB_ERR_INVALID_ARGUMENT, "compact-state workloads need r >= 5 (32 x 32 tiles)");
+    if (cfg->r > 18)  // 32-bit tile / halo indices (3^18 < 2^31)
+        return fail(NBB_ERR_RESOURCE, "compact-state workloads support r <= 18");
     if (cfg->mode != NBB_MODE_LAMBDA)
         return fail(NBB_ERR_INVALID_ARGUMENT, "the compact state is the lambda orthotope: lambda mode only");
     return NBB_OK;
@@ -681,10 +684,29 @@ int compact_to_sectors(DeviceCtx* ctx, const nbb_config* cfg, const void* comp, 
     return NBB_OK;
 }
 
+// the per-level halo table of ca_compact_kernel, built once (then cached) per device
+int compact_halo_table(DeviceCtx* ctx, const nbb_config* cfg, const CompactCaArgs& a, const FastDiv& d,
+                       const int32_t** out) {
+    std::lock_guard<std::mutex> lock(g_mutex);
+    int32_t*& t = ctx->halo_tab[cfg->r];
+    if (!t) {
+        NBB_CUDA(cudaMalloc(&t, (size_t)a.tiles * 8 * sizeof(int32_t)));
+        const uint64_t n = (uint64_t)a.tiles * 8;
+        const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sms * 16));
+        compact_halo_table_kernel<<<blocks, 256, 0, ctx->stream>>>(a, d, t);
+        NBB_CUDA(cudaGetLastError());
+        NBB_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    *out = t;
+    return NBB_OK;
+}
+
 int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* dst, uint16_t birth,
                       uint16_t survive, cudaStream_t st) {
     FastDiv div_hb;
     const CompactCaArgs a = compact_args(cfg, src, dst, birth, survive, &div_hb);
+    const int32_t* tab;
+    NBB_CHECK(compact_halo_table(ctx, cfg, a, div_hb, &tab));
     static int occ = 0;
     if (occ == 0) {
         NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ca_compact_kernel, 256, 0));
@@ -693,7 +715,7 @@ int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, vo
     const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
     if (want == 0) return NBB_OK;
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
-    ca_compact_kernel<<<blocks, 256, 0, st>>>(a, div_hb);
+    ca_compact_kernel<<<blocks, 256, 0, st>>>(a, div_hb, tab);
     NBB_CUDA(cudaGetLastError());
     return NBB_OK;
 }
@@ -1342,6 +1364,10 @@ int nbb_gpu_release(void) {
             if (c.bufs[i]) cudaFree(c.bufs[i]);
             c.bufs[i] = nullptr;
             c.buf_bytes[i] = 0;
+        }
+        for (auto& t : c.halo_tab) {
+            if (t) cudaFree(t);
+            t = nullptr;
         }
     }
     return NBB_OK;
