@@ -162,14 +162,17 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
-def config_block(r, rho, world=1):
+def config_block(r, rho, world=1, transport="p2p"):
     return {"workload": f"C3: gasket n=2^{r} cellular-automaton step (B3/S23), lambda(omega) launch, "
                         f"rho={rho} tiles; device state = the lambda-ordered compact layout "
                         f"(CompactGrid, 8 B per member), host I/O = the reference's int64 Grid",
             "r": r, "n": 1 << r, "rho": rho, "mode": "lambda", "cells_per_step": 3 ** r,
             "cell": "int64", "state": "compact",
-            "parallelism": f"{world} rank(s): contiguous tile-range shards + NCCL halo exchange"
-                           if world > 1 else "1 GPU",
+            "parallelism": "1 GPU" if world == 1 else
+                           f"{world} ranks: contiguous tile-range shards; " + (
+                               "halo cells read over peer memory (CUDA IPC) inside the step kernel"
+                               if transport == "p2p" else
+                               "halo cells exchanged by gather + NCCL all_to_all + scatter"),
             "l2": "no flush: each step moves 689 MB compact / 1.7 GB embedded (> 126 MB L2)"}
 
 
@@ -184,6 +187,9 @@ def main():
     ap.add_argument("--ref-max-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1 halo exchange: inside the step kernel over peer memory (p2p, "
+                         "default) or gather + NCCL all_to_all + scatter per step (nccl)")
     ap.add_argument("--profile", action="store_true",
                     help="only run a few λ/BB CA steps (for ncu); prints nothing")
     args = ap.parse_args()
@@ -250,7 +256,8 @@ def main():
     from paper_2004_13475_b200 import shard
     plan = shard.ShardPlan(r=r, rho=32, world=world, rank=rank)
     plan_c = shard.ShardPlan(r=r, rho=32, world=world, rank=rank, state="compact")
-    launches_per_step = 1 if world == 1 else 3  # + halo gather and scatter kernels
+    # kernels per step: 1 (N = 1, or N > 1 over peer memory); + gather and scatter with NCCL
+    launches_per_step = 3 if (world > 1 and args.transport == "nccl") else 1
 
     def ca_runner(c, src, dst):
         bufs = [src, dst]
@@ -322,7 +329,14 @@ def main():
     results = {}
 
     # ---- headline: λ(ω) CA step on the compact state, ρ = 32 tiles ---------------------
-    head_ms = timed(compact_runner(cfg(), c1, c2), K, W, sampler)
+    if world > 1 and args.transport == "p2p":
+        p2p = shard.P2PCompactCA(plan_c, dist, device=local)
+        p2p.load(c1)
+        head_ms = timed(lambda: p2p.step(cfg(), nbb.CaRule(), s), K, W, sampler)
+        p2p.check(s)
+        p2p.close()
+    else:
+        head_ms = timed(compact_runner(cfg(), c1, c2), K, W, sampler)
     value = members * 1e3 / head_ms  # all ranks together update the 3^r cells per step
     results["ca_lambda_compact_i64"] = head_ms
     # ---- the same step on the reference's int64 embedded Grid layout --------------------
@@ -488,7 +502,7 @@ def main():
         "vs_baseline": None, "dtype": "int64",
         "data": f"synthetic: random_member_grid(gasket, {r}, seed=17, modulus=2) generated "
                 "bit-identically on device, B3/S23",
-        "config": config_block(r, 32, world),
+        "config": config_block(r, 32, world, args.transport),
         "gpu_launches": K * launches_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,

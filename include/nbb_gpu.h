@@ -246,6 +246,37 @@ int nbb_gpu_scatter_cells_dev(const nbb_config* cfg, void* d_grid, const int64_t
 /* Free the device buffers cached by the host-buffer entry points. */
 int nbb_gpu_release(void);
 
+/* ---- multi-GPU compact CA over peer memory (one process per GPU) ----------------------
+ * The reference splits block ordinals over worker threads sharing one Grid
+ * (dispatch.cpp:416-432); across GPUs the shared grid becomes CUDA IPC mappings of every
+ * rank's compact buffers. nbb_gpu_ca_compact_step_p2p_dev is nbb_gpu_ca_compact_step_dev
+ * for this rank's shard (cfg.shard_begin/shard_count over the compact tile order) in ONE
+ * kernel: it waits until every rank finished the previous step (flag barrier in peer
+ * memory, bounded by timeout_ms -> NBB_ERR_CUDA), reads the halo cells other ranks own
+ * straight from their buffers over NVLink, and announces its own completion to every rank.
+ * All device arrays below are device-resident; world <= 8. */
+typedef struct nbb_p2p {
+    int32_t world, rank;
+    const void* d_peer_src;      /* [world] const int64_t*: every rank's source buffer this step */
+    const void* d_halo_owner;    /* [tiles * 8] uint8: owner rank of each tile's halo cell     */
+    void* d_sync;                /* this rank's uint32[4] {arrivals, done, error, 0}, zeroed    */
+    const void* d_peer_flag;     /* [world] uint32*: every rank's d_sync (arrival counter)      */
+    uint32_t wait_target;        /* arrivals needed before this step starts (world * step)      */
+    uint32_t timeout_ms;         /* bound on the wait; 0 = 20000                                */
+} nbb_p2p;
+int nbb_gpu_ca_compact_step_p2p_dev(const nbb_config* cfg, const void* d_src, void* d_dst,
+                                    uint16_t birth, uint16_t survive, const nbb_p2p* p2p,
+                                    void* stream);
+/* error flag of d_sync after a step sequence (synchronises the stream): 0 ok, 1 timed out */
+int nbb_gpu_p2p_check(const nbb_p2p* p2p, void* stream);
+/* device memory that can be exported (cudaMalloc: the IPC handle names the allocation) */
+int nbb_gpu_malloc(int32_t device, uint64_t bytes, void** d_ptr);
+int nbb_gpu_free(int32_t device, void* d_ptr);
+/* CUDA IPC: 64-byte handle of an nbb_gpu_malloc allocation; open a peer's handle */
+int nbb_gpu_ipc_handle(int32_t device, const void* d_ptr, uint8_t handle[64]);
+int nbb_gpu_ipc_open(int32_t device, const uint8_t handle[64], void** d_ptr);
+int nbb_gpu_ipc_close(int32_t device, void* d_ptr);
+
 #ifdef __cplusplus
 }
 #endif

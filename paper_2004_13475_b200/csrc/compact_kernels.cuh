@@ -182,6 +182,55 @@ __device__ __forceinline__ uint64_t gasket_compact_offset(uint32_t x, uint32_t y
     return (uint64_t)oy * W + ox;
 }
 
+// ---- multi-GPU (P2P) step ordering -------------------------------------------------------
+constexpr int kMaxP2P = 8;
+struct P2PArgs {
+    const long long* const* peer_src;  // [world] each rank's source buffer of this step
+    const uint8_t* halo_owner;         // [tiles * 8] rank owning each halo cell
+    unsigned int* flag;                // this rank's arrival counter (peers add to it)
+    unsigned int* const* peer_flag;    // [world] every rank's arrival counter
+    unsigned int* done;                // CTAs of this launch that finished
+    int* error;                        // set to 1 if the wait timed out
+    unsigned int wait_target;          // arrivals required before the step may start
+    unsigned int timeout_ms;
+    int world, rank;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// one thread per CTA: spin (bounded) until every rank finished the previous step
+__device__ __forceinline__ void p2p_wait(const P2PArgs& p) {
+    const unsigned long long t0 = global_ns();
+    unsigned int v;
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p.flag) : "memory");
+        if (v >= p.wait_target) break;
+        if (global_ns() - t0 > 1000000ull * p.timeout_ms) {
+            atomicExch(p.error, 1);
+            break;
+        }
+        __nanosleep(200);
+    }
+}
+
+// after the CTA's last store: the last CTA of the launch announces the step to every rank
+__device__ __forceinline__ void p2p_arrive(const P2PArgs& p) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned int prev = atomicAdd(p.done, 1u);
+        if (prev == gridDim.x - 1) {
+            *p.done = 0u;  // stream order: the next launch starts after this one
+            __threadfence_system();
+            for (int r = 0; r < p.world; ++r) atomicAdd_system(p.peer_flag[r], 1u);
+        }
+    }
+}
+
 // The 8 halo cells of every ρ = 32 tile as compact offsets (-1: not a member / outside),
 // [tile u][k] for the tile-local positions (-1,-1) (0,-1) (1,-1) (-1,31) (32,30) (32,31)
 // (32,32) (0,32). Static per level; built once per device and level (5.7 MB at r = 16) so
@@ -214,14 +263,28 @@ __global__ void compact_halo_table_kernel(CompactCaArgs a, FastDiv div_hb, int32
 // hence the instruction diet. Tried and slower on B200 (profiles/r1_compact_ca_tuning.md):
 // a cp.async ring (8-byte copies), L2 bulk prefetch one tile ahead, 64/48-register budgets,
 // and cp.async.bulk row copies into an mbarrier ring.
+//
+// P2P = true is the multi-GPU form (one kernel per step, no separate exchange): each rank
+// owns a contiguous range of tiles in its own replica-sized buffers, the halo cells owned
+// by other ranks are read straight from their buffers over NVLink (CUDA IPC mappings,
+// ld.relaxed.sys), and a flag barrier in peer memory orders the steps: the kernel first
+// waits until every rank has finished the previous step (p.wait_target arrivals on this
+// rank's flag), and its last CTA to finish adds one arrival to every rank's flag.
+template <bool P2P>
 __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, FastDiv div_hb,
-                                                             const int32_t* __restrict__ halo_tab) {
+                                                             const int32_t* __restrict__ halo_tab,
+                                                             P2PArgs p) {
     __shared__ __align__(16) uint8_t s_cell[8][32 * 32];
     __shared__ uint32_t s_new[8][32];
     __shared__ uint16_t s_pos[256];  // c_local_pos (per-lane constant-bank reads serialise)
+    __shared__ const long long* s_peer[kMaxP2P];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint8_t* cell = s_cell[wib];
     s_pos[threadIdx.x] = threadIdx.x < 243 ? c_local_pos[threadIdx.x] : 0;
+    if (P2P) {
+        if (threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
+        if (threadIdx.x == 0 && p.wait_target) p2p_wait(p);
+    }
     __syncthreads();
     uint32_t sl_off[8], sl_pos[8];
 #pragma unroll
@@ -243,6 +306,7 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
 
     uint32_t u = a.tile_begin + warp_global;
     int32_t hoff = (u < a.tile_end && lane < 8) ? __ldg(halo_tab + 8ull * u + lane) : -1;
+    uint32_t hown = (P2P && u < a.tile_end && lane < 8) ? p.halo_owner[8ull * u + lane] : 0u;
     for (; u < a.tile_end; u += warp_stride) {
         const uint32_t wxb = fastdiv(u, div_hb), wyb = u - wxb * a.Hb;
         const uint64_t base = ((uint64_t)(9u * wxb) * a.W + 27u * wyb) * 8u;
@@ -252,9 +316,16 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
         for (int k = 0; k < 7; ++k) v[k] = __ldg(reinterpret_cast<const long long*>(src + sl_off[k]));
         v[7] = k7 ? __ldg(reinterpret_cast<const long long*>(src + sl_off[7])) : 0ll;
         // halo cell of lanes 0..7 (offset from the table; the next tile's entry prefetched)
-        const long long hv = hoff >= 0 ? __ldg(a.src + hoff) : 0ll;
+        long long hv = 0;
+        if (hoff >= 0) {
+            if (!P2P || hown == (uint32_t)p.rank)
+                hv = __ldg(a.src + hoff);
+            else  // a cell of another rank's tile: read its buffer over NVLink
+                asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(hv) : "l"(s_peer[hown] + hoff));
+        }
         const uint32_t un = u + warp_stride;
         hoff = (un < a.tile_end && lane < 8) ? __ldg(halo_tab + 8ull * un + lane) : -1;
+        if (P2P) hown = (un < a.tile_end && lane < 8) ? p.halo_owner[8ull * un + lane] : 0u;
 #pragma unroll
         for (int k = 0; k < 7; ++k) cell[sl_pos[k]] = v[k] != 0ll;
         if (k7) cell[sl_pos[7]] = v[7] != 0ll;
@@ -292,6 +363,7 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
                 (long long)((s_new[wib][sl_pos[7] >> 5] >> (sl_pos[7] & 31u)) & 1u);
         __syncwarp();
     }
+    if (P2P) p2p_arrive(p);
 }
 
 

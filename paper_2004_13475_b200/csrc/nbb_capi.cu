@@ -709,13 +709,13 @@ int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, vo
     NBB_CHECK(compact_halo_table(ctx, cfg, a, div_hb, &tab));
     static int occ = 0;
     if (occ == 0) {
-        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ca_compact_kernel, 256, 0));
+        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ca_compact_kernel<false>, 256, 0));
         if (occ < 1) occ = 1;
     }
     const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
     if (want == 0) return NBB_OK;
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
-    ca_compact_kernel<<<blocks, 256, 0, st>>>(a, div_hb, tab);
+    ca_compact_kernel<false><<<blocks, 256, 0, st>>>(a, div_hb, tab, P2PArgs{});
     NBB_CUDA(cudaGetLastError());
     return NBB_OK;
 }
@@ -1320,6 +1320,94 @@ int nbb_gpu_ca_compact_step_dev(const nbb_config* cfg, const void* d_src, void* 
     Timer t(cfg->timing != 0, (cudaStream_t)stream);
     NBB_CHECK(launch_ca_compact(ctx, cfg, d_src, d_dst, birth, survive, (cudaStream_t)stream));
     fill_report(cfg, report, t.stop_micros());
+    return NBB_OK;
+}
+
+int nbb_gpu_ca_compact_step_p2p_dev(const nbb_config* cfg, const void* d_src, void* d_dst, uint16_t birth,
+                                    uint16_t survive, const nbb_p2p* p2p, void* stream) {
+    if (!cfg || !p2p) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_CHECK(compact_workload_check(cfg));
+    if (p2p->world < 1 || p2p->world > kMaxP2P || p2p->rank < 0 || p2p->rank >= p2p->world)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: need 1 <= world <= 8 and 0 <= rank < world");
+    if (!p2p->d_peer_src || !p2p->d_halo_owner || !p2p->d_sync || !p2p->d_peer_flag)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: null device array");
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    FastDiv div_hb;
+    const CompactCaArgs a = compact_args(cfg, d_src, d_dst, birth, survive, &div_hb);
+    const int32_t* tab;
+    NBB_CHECK(compact_halo_table(ctx, cfg, a, div_hb, &tab));
+    P2PArgs p;
+    p.peer_src = (const long long* const*)p2p->d_peer_src;
+    p.halo_owner = (const uint8_t*)p2p->d_halo_owner;
+    unsigned int* sync = (unsigned int*)p2p->d_sync;
+    p.flag = sync;
+    p.done = sync + 1;
+    p.error = (int*)(sync + 2);
+    p.peer_flag = (unsigned int* const*)p2p->d_peer_flag;
+    p.wait_target = p2p->wait_target;
+    p.timeout_ms = p2p->timeout_ms ? p2p->timeout_ms : 20000u;
+    p.world = p2p->world;
+    p.rank = p2p->rank;
+    static int occ = 0;
+    if (occ == 0) {
+        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ca_compact_kernel<true>, 256, 0));
+        if (occ < 1) occ = 1;
+    }
+    // every rank launches (and arrives) even with an empty shard: one CTA at least
+    const uint64_t want = std::max<uint64_t>(1, (a.tile_end - a.tile_begin + 7) / 8);
+    const unsigned blocks = (unsigned)std::min<uint64_t>(want, (uint64_t)ctx->sms * occ);
+    ca_compact_kernel<true><<<blocks, 256, 0, (cudaStream_t)stream>>>(a, div_hb, tab, p);
+    NBB_CUDA(cudaGetLastError());
+    return NBB_OK;
+}
+
+int nbb_gpu_p2p_check(const nbb_p2p* p2p, void* stream) {
+    if (!p2p || !p2p->d_sync) return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: null sync buffer");
+    int err = 0;
+    NBB_CUDA(cudaMemcpyAsync(&err, (const unsigned int*)p2p->d_sync + 2, sizeof(int), cudaMemcpyDeviceToHost,
+                             (cudaStream_t)stream));
+    NBB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    if (err) return fail(NBB_ERR_CUDA, "p2p: a step timed out waiting for the other ranks");
+    return NBB_OK;
+}
+
+int nbb_gpu_malloc(int32_t device, uint64_t bytes, void** d_ptr) {
+    if (!d_ptr) return fail(NBB_ERR_INVALID_ARGUMENT, "null output pointer");
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(device, &ctx));
+    NBB_CUDA(cudaSetDevice(device));
+    NBB_CUDA(cudaMalloc(d_ptr, bytes));
+    NBB_CUDA(cudaMemset(*d_ptr, 0, bytes));
+    return NBB_OK;
+}
+
+int nbb_gpu_free(int32_t device, void* d_ptr) {
+    NBB_CUDA(cudaSetDevice(device));
+    NBB_CUDA(cudaFree(d_ptr));
+    return NBB_OK;
+}
+
+int nbb_gpu_ipc_handle(int32_t device, const void* d_ptr, uint8_t handle[64]) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    NBB_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    NBB_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+    std::memcpy(handle, &h, 64);
+    return NBB_OK;
+}
+
+int nbb_gpu_ipc_open(int32_t device, const uint8_t handle[64], void** d_ptr) {
+    NBB_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    NBB_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return NBB_OK;
+}
+
+int nbb_gpu_ipc_close(int32_t device, void* d_ptr) {
+    NBB_CUDA(cudaSetDevice(device));
+    NBB_CUDA(cudaIpcCloseMemHandle(d_ptr));
     return NBB_OK;
 }
 

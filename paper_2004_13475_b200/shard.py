@@ -130,6 +130,22 @@ class ShardPlan:
         t = np.arange(self.begin, self.begin + self.count, dtype=np.int64)
         return lambda_blocks(self.ordinal_of_tile(t), self.W)
 
+    def halo_owner_table(self) -> np.ndarray:
+        """uint8 [tiles * 8]: the rank owning each tile's k-th halo cell (0 where the cell is
+        not a member) — the table the P2P compact CA kernel selects peer buffers with."""
+        n, rho = 1 << self.r, self.rho
+        t = np.arange(self.total, dtype=np.int64)
+        bx, by = lambda_blocks(self.ordinal_of_tile(t), self.W)
+        off = _halo_offsets(rho)
+        cx = (bx * rho)[:, None] + off[None, :, 0]
+        cy = (by * rho)[:, None] + off[None, :, 1]
+        ok = (cx >= 0) & (cy >= 0) & (cx < n) & (cy < n)
+        ok &= (np.where(ok, cx, 0) & (n - 1 - np.where(ok, cy, 0))) == 0
+        own = np.zeros(cx.shape, dtype=np.int64)
+        own[ok] = self.owner(self.tile_of_ordinal(
+            lambda_inverse_blocks(cx[ok] // rho, cy[ok] // rho, self.r_b, self.W)))
+        return own.astype(np.uint8).ravel()
+
     def _build_halo_lists(self):
         n, rho = 1 << self.r, self.rho
         t = np.arange(self.total, dtype=np.int64)
@@ -237,3 +253,132 @@ def _kernel_scatter(flat, idx, vals):
                                             ctypes.c_void_p(idx.data_ptr()), idx.numel(),
                                             ctypes.c_void_p(vals.data_ptr()),
                                             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
+
+# ---- the compact CA over peer memory (one kernel per step, no separate exchange) ----------
+class _DevArray:
+    """A raw device allocation seen by torch (zero-copy, __cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, count: int, typestr: str = "<i8"):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3}
+
+
+class P2PCompactCA:
+    """Multi-GPU compact CA where the exchange lives inside the step kernel.
+
+    Every rank allocates its two compact buffers and a 16-byte sync word with cudaMalloc
+    (nbb_gpu_malloc), exports them as CUDA IPC handles, opens every peer's (one
+    all_gather_object at setup), and then runs each step as ONE launch of
+    nbb_gpu_ca_compact_step_p2p_dev: the kernel waits on its arrival counter until all ranks
+    finished the previous step, reads the ≤ 8 halo cells per tile that other ranks own
+    straight from their buffers (NVLink loads through the IPC mappings), writes its own tiles,
+    and its last CTA adds one arrival to every rank's counter. No host synchronisation and
+    no collective inside the step loop; the NCCL `exchange_halo` path is the baseline.
+    """
+
+    def __init__(self, plan: ShardPlan, dist, device: int = 0, timeout_ms: int = 20000):
+        import ctypes
+        import torch
+        from . import _abi
+        if plan.state != "compact":
+            raise ValueError("P2PCompactCA needs ShardPlan(state='compact')")
+        if plan.world > 8:
+            raise ValueError("P2PCompactCA supports up to 8 ranks")
+        self.plan, self.device, self.timeout_ms, self.dist = plan, device, timeout_ms, dist
+        self.lib = lib = _abi.load()
+        self.count = 3 ** plan.r
+        nbytes = self.count * 8
+
+        def alloc(b):
+            p = ctypes.c_void_p()
+            _check(lib.nbb_gpu_malloc(device, b, ctypes.byref(p)))
+            return p.value
+
+        self._own = [alloc(nbytes), alloc(nbytes), alloc(16)]   # buffer 0, buffer 1, sync
+        handles = []
+        for ptr in self._own:
+            h = (ctypes.c_uint8 * 64)()
+            _check(lib.nbb_gpu_ipc_handle(device, ctypes.c_void_p(ptr), h))
+            handles.append(bytes(h))
+        gathered = [None] * plan.world
+        dist.all_gather_object(gathered, handles)
+        self._opened = []
+        peers = []
+        for r, hs in enumerate(gathered):
+            if r == plan.rank:
+                peers.append(self._own)
+                continue
+            ptrs = []
+            for h in hs:
+                p = ctypes.c_void_p()
+                _check(lib.nbb_gpu_ipc_open(device, (ctypes.c_uint8 * 64).from_buffer_copy(h),
+                                            ctypes.byref(p)))
+                ptrs.append(p.value)
+                self._opened.append(p.value)
+            peers.append(ptrs)
+        dev = torch.device("cuda", device)
+        self._peer_src = [torch.tensor([peers[r][b] for r in range(plan.world)], dtype=torch.int64,
+                                       device=dev) for b in (0, 1)]
+        self._peer_flag = torch.tensor([peers[r][2] for r in range(plan.world)], dtype=torch.int64,
+                                       device=dev)
+        self._owner = torch.from_numpy(plan.halo_owner_table()).to(dev)
+        self.buffers = [torch.as_tensor(_DevArray(p, self.count), device=dev) for p in self._own[:2]]
+        self.step_index = 0
+
+    def load(self, compact_state) -> None:
+        """Set the state (a (3^r,) int64 tensor; this rank's tiles must be current). Collective:
+        every rank loads before any rank's first step reads a peer."""
+        import torch
+        self.buffers[0].copy_(compact_state.to(self.buffers[0].device).view(-1))
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier()
+        self.step_index = 0
+
+    def state(self):
+        """The current state buffer (this rank's tiles are current)."""
+        return self.buffers[self.step_index & 1]
+
+    def _p2p(self):
+        from . import _abi
+        i = self.step_index
+        return _abi.NbbP2P(self.plan.world, self.plan.rank, self._peer_src[i & 1].data_ptr(),
+                           self._owner.data_ptr(), self._own[2], self._peer_flag.data_ptr(),
+                           self.plan.world * i, self.timeout_ms)
+
+    def step(self, config, rule, stream) -> None:
+        import ctypes
+        i = self.step_index
+        p = self._p2p()
+        c = self.plan.local_config(config).to_c()
+        _check(self.lib.nbb_gpu_ca_compact_step_p2p_dev(
+            ctypes.byref(c), ctypes.c_void_p(self.buffers[i & 1].data_ptr()),
+            ctypes.c_void_p(self.buffers[(i + 1) & 1].data_ptr()), rule.birth, rule.survive,
+            ctypes.byref(p), ctypes.c_void_p(stream)))
+        self.step_index = i + 1
+
+    def check(self, stream) -> None:
+        """Raise if any step timed out waiting for the other ranks (synchronises)."""
+        import ctypes
+        p = self._p2p()
+        _check(self.lib.nbb_gpu_p2p_check(ctypes.byref(p), ctypes.c_void_p(stream)))
+
+    def close(self) -> None:
+        """Collective: no rank unmaps or frees while a peer's step may still read it."""
+        import ctypes
+        import torch
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier()
+        for p in self._opened:
+            self.lib.nbb_gpu_ipc_close(self.device, ctypes.c_void_p(p))
+        self._opened = []
+        self.buffers = []
+        self.dist.barrier()
+        for p in self._own:
+            self.lib.nbb_gpu_free(self.device, ctypes.c_void_p(p))
+        self._own = []
+
+
+def _check(rc: int) -> None:
+    from .nbb import _check as check
+    check(rc)

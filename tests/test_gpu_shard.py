@@ -88,3 +88,53 @@ def test_sharded_ca_on_gpu(world, r, rho, cw):
         assert p.exitcode == 0
     want = orc_ca(r, orc_random_member_grid(r, 4321, 2), steps)
     assert np.array_equal(got, want)
+
+
+def _p2p_worker(rank, world, port, r, steps, q):
+    """The P2P compact CA: ranks on one B200 share buffers through CUDA IPC mappings."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2004_13475_b200 import nbb
+    from paper_2004_13475_b200.shard import (P2PCompactCA, ShardPlan, lambda_blocks,
+                                             lambda_inverse_blocks)
+    n = 1 << r
+    plan = ShardPlan(r=r, rho=32, world=world, rank=rank, state="compact")
+    cx, cy = lambda_blocks(np.arange(3 ** r, dtype=np.int64), 3 ** ((r + 1) // 2))
+    tile = plan.tile_of_ordinal(lambda_inverse_blocks(cx >> 5, cy >> 5, plan.r_b, plan.W))
+    own = torch.from_numpy(plan.owner(tile) == rank)
+    init = torch.from_numpy(orc_random_member_grid(r, 4321, 2)[cy, cx].copy())
+    init[~own] = 7  # only this rank's tiles are trusted: remote cells must come from peers
+    ca = P2PCompactCA(plan, dist, device=0, timeout_ms=60000)
+    ca.load(init)
+    c = nbb.DispatchConfig(r=r, rho=32, max_cells=n * n)
+    s = torch.cuda.current_stream().cuda_stream
+    for _ in range(steps):
+        ca.step(c, nbb.CaRule(), s)
+    ca.check(s)
+    out = ca.state().cpu()
+    mine_c = torch.where(own, out, torch.zeros_like(out))
+    mine = torch.zeros(n, n, dtype=torch.int64)
+    mine[torch.from_numpy(cy), torch.from_numpy(cx)] = mine_c
+    ca.close()
+    dist.all_reduce(mine)
+    if rank == 0:
+        q.put(mine.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,r", [(2, 10), (3, 11)])
+def test_p2p_compact_ca_on_gpu(world, r):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    steps = 6
+    procs = [ctx.Process(target=_p2p_worker, args=(i, world, port, r, steps, q)) for i in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want = orc_ca(r, orc_random_member_grid(r, 4321, 2), steps)
+    assert np.array_equal(got, want)
