@@ -473,6 +473,11 @@ def main():
                                 for k in ("int64", "bit")}}
         del hin, hout
         nbb.release()
+    elif world > 1:
+        e2e = {"value": None, "unit": "cells/s",
+               "note": "measured at N = 1 only: the host-buffer call takes the reference's whole int64 "
+                       "Grid (32 GiB in + 32 GiB out pinned per process at n = 2^16), which N ranks "
+                       "on one host cannot each hold"}
 
     # ---- CPU baseline: the reference on this host's cores (bounded sample) ------------
     cpu = None
