@@ -1,0 +1,59 @@
+"""Small end-to-end exercise of every kernel family for compute-sanitizer
+(memcheck / racecheck / synccheck), checked against the C oracle:
+
+    compute-sanitizer --tool racecheck python tools/sanitize_run.py
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+
+from _oracle import orc_ca, orc_random_member_grid, orc_reduction, orc_single_write  # noqa: E402
+from paper_2004_13475_b200 import _abi, nbb  # noqa: E402
+
+G = nbb.FractalSpec.sierpinski()
+r = int(os.environ.get("SAN_R", "7"))
+g = orc_random_member_grid(r, 5, 2)
+want = orc_ca(r, g, 3)
+checks = 0
+for mode in (nbb.MapMode.Lambda, nbb.MapMode.BoundingBox):
+    for rho in (8, 32):
+        for kern in (nbb.KernelFamily.Tile, nbb.KernelFamily.PerCell):
+            for cw in (8, 1, 0):
+                if cw != 8 and (kern == nbb.KernelFamily.PerCell or rho != 32):
+                    continue
+                c = nbb.DispatchConfig(r=r, rho=rho, mode=mode, kernel=kern, cell_width=cw)
+                assert np.array_equal(nbb.run_ca(c, nbb.Grid(G, r, g), 3).grid.values, want), (mode, rho, kern, cw)
+                checks += 1
+            c = nbb.DispatchConfig(r=r, rho=rho, mode=mode, kernel=kern)
+            assert np.array_equal(nbb.run_single_write(c).grid.values, orc_single_write(r))
+            assert nbb.run_reduction(c, nbb.Grid(G, r, g)).value == orc_reduction(r, g)
+            checks += 2
+for be in (nbb.LambdaBackend.MmaV1, nbb.LambdaBackend.MmaV2):
+    c = nbb.DispatchConfig(r=r, rho=8, backend=be, kernel=nbb.KernelFamily.PerCell)
+    assert np.array_equal(nbb.run_ca(c, nbb.Grid(G, r, g), 3).grid.values, want)
+    checks += 1
+c = nbb.DispatchConfig(r=r, rho=32, flags=_abi.FLAG_COMPACT_STATE)
+assert np.array_equal(nbb.run_ca(c, nbb.Grid(G, r, g), 3).grid.values, want)
+comp = nbb.compact_store(G, r, g)
+assert np.array_equal(nbb.compact_load(G, comp, 0), g)
+xy = nbb.lambda_coords(nbb.DispatchConfig(r=r, rho=1), r)
+checks += 3
+# zero-copy host buffers (pinned): member sectors read / written in place over PCIe
+import ctypes  # noqa: E402
+import torch  # noqa: E402
+n = 1 << r
+h_in = torch.from_numpy(g.copy()).pin_memory()
+for fl, cw in ((_abi.FLAG_OUT_ZEROED, 8), (_abi.FLAG_OUT_ZEROED | _abi.FLAG_COMPACT_STATE, 8),
+               (_abi.FLAG_OUT_ZEROED, 0)):
+    h_out = torch.zeros((n, n), dtype=torch.int64).pin_memory()
+    cc = nbb.DispatchConfig(r=r, rho=32, cell_width=cw, flags=fl).to_c()
+    assert _abi.load().nbb_gpu_ca(ctypes.byref(cc), ctypes.c_void_p(h_in.data_ptr()), r, 3, 8, 12,
+                                  ctypes.c_void_p(h_out.data_ptr()), None) == 0
+    assert np.array_equal(h_out.numpy(), want), (fl, cw)
+    checks += 1
+print(f"sanitize_run ok: r={r}, {checks} checks")
