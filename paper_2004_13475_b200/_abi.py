@@ -12,7 +12,7 @@ from ctypes import (POINTER, Structure, c_char, c_char_p, c_double, c_int, c_int
                     c_size_t, c_uint16, c_uint64, c_void_p)
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libnbbgpu.so")
+LIB_PATH = os.environ.get("NBB_GPU_LIB") or os.path.join(PKG_DIR, "libnbbgpu.so")  # env: tuning builds
 
 MAX_REPLICAS = 9
 
