@@ -304,32 +304,64 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
     char* dst0 = reinterpret_cast<char*>(a.dst);
     __syncwarp();
 
-    uint32_t u = a.tile_begin + warp_global;
-    int32_t hoff = (u < a.tile_end && lane < 8) ? __ldg(halo_tab + 8ull * u + lane) : -1;
-    uint32_t hown = (P2P && u < a.tile_end && lane < 8) ? p.halo_owner[8ull * u + lane] : 0u;
-    for (; u < a.tile_end; u += warp_stride) {
-        const uint32_t wxb = fastdiv(u, div_hb), wyb = u - wxb * a.Hb;
-        const uint64_t base = ((uint64_t)(9u * wxb) * a.W + 27u * wyb) * 8u;
-        const char* src = src0 + base;
-        long long v[8];
+    // Software-pipelined over the warp's tiles: tile u+stride's loads (its 243 values and
+    // halo cells) are issued as soon as tile u's values are in the byte tile — into the same
+    // registers — so they fly while tile u's rule and stores run; the halo-table entries run
+    // one more tile ahead (the halo load depends on them).
+    auto tile_base = [&](uint32_t t) -> uint64_t {
+        const uint32_t wxb = fastdiv(t, div_hb), wyb = t - wxb * a.Hb;
+        return ((uint64_t)(9u * wxb) * a.W + 27u * wyb) * 8u;
+    };
+    long long v[8];
+    auto load_tile = [&](uint64_t b) {
+        const char* src = src0 + b;
 #pragma unroll
         for (int k = 0; k < 7; ++k) v[k] = __ldg(reinterpret_cast<const long long*>(src + sl_off[k]));
         v[7] = k7 ? __ldg(reinterpret_cast<const long long*>(src + sl_off[7])) : 0ll;
-        // halo cell of lanes 0..7 (offset from the table; the next tile's entry prefetched)
+    };
+    auto load_halo = [&](int32_t off, uint32_t own) -> long long {
         long long hv = 0;
-        if (hoff >= 0) {
-            if (!P2P || hown == (uint32_t)p.rank)
-                hv = __ldg(a.src + hoff);
+        if (off >= 0) {
+            if (!P2P || own == (uint32_t)p.rank)
+                hv = __ldg(a.src + off);
             else  // a cell of another rank's tile: read its buffer over NVLink
-                asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(hv) : "l"(s_peer[hown] + hoff));
+                asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(hv) : "l"(s_peer[own] + off));
         }
+        return hv;
+    };
+    auto halo_entry = [&](uint32_t t, int32_t& off, uint32_t& own) {
+        const bool ok = t < a.tile_end && lane < 8;
+        off = ok ? __ldg(halo_tab + 8ull * t + lane) : -1;
+        own = (P2P && ok) ? p.halo_owner[8ull * t + lane] : 0u;
+    };
+
+    uint32_t u = a.tile_begin + warp_global;
+    uint64_t base = 0;
+    long long hv = 0;
+    int32_t hoff_n = -1;
+    uint32_t hown_n = 0;
+    if (u < a.tile_end) {
+        base = tile_base(u);
+        load_tile(base);
+        int32_t off;
+        uint32_t own;
+        halo_entry(u, off, own);
+        hv = load_halo(off, own);
+        halo_entry(u + warp_stride, hoff_n, hown_n);
+    }
+    for (; u < a.tile_end; u += warp_stride) {
         const uint32_t un = u + warp_stride;
-        hoff = (un < a.tile_end && lane < 8) ? __ldg(halo_tab + 8ull * un + lane) : -1;
-        if (P2P) hown = (un < a.tile_end && lane < 8) ? p.halo_owner[8ull * un + lane] : 0u;
 #pragma unroll
         for (int k = 0; k < 7; ++k) cell[sl_pos[k]] = v[k] != 0ll;
         if (k7) cell[sl_pos[7]] = v[7] != 0ll;
         const uint32_t h = __ballot_sync(0xFFFFFFFFu, hv != 0ll) & 0xFFu;
+        uint64_t base_n = 0;
+        if (un < a.tile_end) {  // warp-uniform
+            base_n = tile_base(un);
+            load_tile(base_n);
+            hv = load_halo(hoff_n, hown_n);
+            halo_entry(un + warp_stride, hoff_n, hown_n);
+        }
         __syncwarp();
         uint32_t R = 0;
         {
@@ -354,6 +386,7 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
                            submask_bits((uint32_t)lane);
         __syncwarp();
         char* dst = dst0 + base;
+        base = base_n;
 #pragma unroll
         for (int k = 0; k < 7; ++k)
             *reinterpret_cast<long long*>(dst + sl_off[k]) =
