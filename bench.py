@@ -16,7 +16,10 @@ reference's int64 Grid in and out; transfers inside the timed region).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N > 1 runs under torchrun (one process per GPU): the tile range is split in contiguous
-chunks (dispatch.cpp:419-427) and CA halo cells cross ranks via NCCL.
+chunks (dispatch.cpp:419-427); the headline's halo cells are read from the owning rank's
+buffer over peer memory inside the step kernel (--transport p2p, default) or exchanged by
+NCCL between steps (--transport nccl). `c5_r17` = the same step at n = 2^17 (BASELINE
+configs[4]) at every N.
 """
 from __future__ import annotations
 
@@ -289,23 +292,28 @@ def main():
             state["i"] = i + 1
         return step
 
-    def timed(step, K, W, sampler=None):
-        for _ in range(W):
-            step()
+    def timed_run(run, K, W, sampler=None):
+        """run(k) issues k steps on `stream`; W warm-up steps, then K timed with CUDA events."""
+        run(W)
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         if sampler:
             sampler.__enter__()
         e0.record(stream)
-        for _ in range(K):
-            step()
+        run(K)
         e1.record(stream)
         e1.synchronize()
         if sampler:
             sampler.__exit__()
         barrier()
         return max_over_ranks(e0.elapsed_time(e1)) / K  # ms per step
+
+    def timed(step, K, W, sampler=None):
+        def run(k):
+            for _ in range(k):
+                step()
+        return timed_run(run, K, W, sampler)
 
     # the compact CA state (λ-ordered CompactGrid): every byte a member value (int64)
     c1 = torch.empty(members, dtype=torch.int64, device="cuda")
@@ -329,16 +337,51 @@ def main():
     results = {}
 
     # ---- headline: λ(ω) CA step on the compact state, ρ = 32 tiles ---------------------
+    # the step loop runs in the library (C++; one kernel per step, PDL between steps)
     if world > 1 and args.transport == "p2p":
         p2p = shard.P2PCompactCA(plan_c, dist, device=local)
         p2p.load(c1)
-        head_ms = timed(lambda: p2p.step(cfg(), nbb.CaRule(), s), K, W, sampler)
+        head_ms = timed_run(lambda k: p2p.run(cfg(), nbb.CaRule(), k, s), K, W, sampler)
         p2p.check(s)
         p2p.close()
-    else:
+    elif world > 1:
         head_ms = timed(compact_runner(cfg(), c1, c2), K, W, sampler)
+    else:
+        head_ms = timed_run(lambda k: dev.ca_compact_run_dev(cfg(), c1.data_ptr(), c2.data_ptr(), k,
+                                                             nbb.CaRule(), s), K, W, sampler)
     value = members * 1e3 / head_ms  # all ranks together update the 3^r cells per step
     results["ca_lambda_compact_i64"] = head_ms
+    # ---- C5: the same step on the gasket at n = 2^17 (BASELINE configs[4]), sharded by
+    # contiguous compact tile ranges at N > 1 (halos over peer memory inside the kernel) ------
+    c5 = None
+    if world == 1 or args.transport == "p2p":
+        r5 = args.level + 1
+        m5 = 3 ** r5
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(18)
+        d1 = torch.randint(0, 2, (m5,), dtype=torch.int64, device="cuda", generator=gen)
+        cfg5 = nbb.DispatchConfig(r=r5, rho=32, max_cells=(1 << r5) ** 2, device=local)
+        if world > 1:
+            plan5 = shard.ShardPlan(r=r5, rho=32, world=world, rank=rank, state="compact")
+            p5 = shard.P2PCompactCA(plan5, dist, device=local)
+            p5.load(d1)
+            ms5 = timed_run(lambda k: p5.run(cfg5, nbb.CaRule(), k, s), K, W)
+            p5.check(s)
+            p5.close()
+        else:
+            d2 = torch.empty_like(d1)
+            ms5 = timed_run(lambda k: dev.ca_compact_run_dev(cfg5, d1.data_ptr(), d2.data_ptr(), k,
+                                                             nbb.CaRule(), s), K, W)
+            del d2
+        del d1
+        ach5 = 16 * m5 / (ms5 * 1e-3) / 1e9
+        c5 = {"workload": f"C5: gasket n=2^{r5} CA step (B3/S23), compact state, rho=32 tiles, "
+                          f"{world} rank(s), contiguous compact tile ranges",
+              "data": "synthetic: iid alive values (torch.randint(0, 2), seed 18) over the 3^r member "
+                      "cells of the compact state",
+              "r": r5, "cells_per_step": m5, "ms_per_step": ms5, "value": m5 * 1e3 / ms5,
+              "unit": "cells/s", "per_gpu_GBps": ach5 / world,
+              "per_gpu_roofline_frac": ach5 / world / measured_peaks()[0]}
     # ---- the same step on the reference's int64 embedded Grid layout --------------------
     emb_ms = timed(ca_runner(cfg(), a, b), K, W)
     results["ca_lambda_tile_rho32_i64"] = emb_ms
@@ -541,6 +584,7 @@ def main():
         "workloads_ms": results,
         "workloads_cells_per_s": {k: cells(k) for k in results},
         "map_sweep_C4": sweep,
+        "c5_r17": c5,
         "cpu_baseline": cpu,
         "e2e": e2e,
     }

@@ -231,6 +231,11 @@ int nbb_gpu_compact_read(const char* path, const nbb_spec* spec, int32_t* level,
  * rows), so each rank of the multi-GPU path updates one slab of the compact array. */
 int nbb_gpu_ca_compact_step_dev(const nbb_config* cfg, const void* d_src, void* d_dst,
                                 uint16_t birth, uint16_t survive, void* stream, nbb_report* report);
+/* `steps` compact CA steps ping-ponging between d_a and d_b (step i reads d_a when i is even),
+ * issued back to back from C++ (the reference's run_ca step loop, dispatch.cpp:517-557);
+ * the result is in d_a when steps is even, else in d_b. */
+int nbb_gpu_ca_compact_run_dev(const nbb_config* cfg, void* d_a, void* d_b, int32_t steps,
+                               uint16_t birth, uint16_t survive, void* stream);
 int nbb_gpu_reduction_compact_dev(const nbb_config* cfg, const void* d_compact, void* d_value,
                                   void* stream, nbb_report* report);
 int nbb_gpu_single_write_compact_dev(const nbb_config* cfg, void* d_compact, void* stream,
@@ -249,24 +254,26 @@ int nbb_gpu_release(void);
 /* ---- multi-GPU compact CA over peer memory (one process per GPU) ----------------------
  * The reference splits block ordinals over worker threads sharing one Grid
  * (dispatch.cpp:416-432); across GPUs the shared grid becomes CUDA IPC mappings of every
- * rank's compact buffers. nbb_gpu_ca_compact_step_p2p_dev is nbb_gpu_ca_compact_step_dev
- * for this rank's shard (cfg.shard_begin/shard_count over the compact tile order) in ONE
- * kernel: it waits until every rank finished the previous step (flag barrier in peer
- * memory, bounded by timeout_ms -> NBB_ERR_CUDA), reads the halo cells other ranks own
- * straight from their buffers over NVLink, and announces its own completion to every rank.
- * All device arrays below are device-resident; world <= 8. */
+ * rank's compact buffers. nbb_gpu_ca_compact_p2p_dev runs `steps` steps of
+ * nbb_gpu_ca_compact_step_dev for this rank's shard (cfg.shard_begin/shard_count over the
+ * compact tile order), ONE kernel per step issued back to back from C++: each kernel waits
+ * until every rank finished the previous step (flag barrier in peer memory: world x i arrivals
+ * before step i, bounded by timeout_ms -> error flag), reads the
+ * halo cells other ranks own straight from their buffers over NVLink, and announces its own
+ * completion to every rank. Step i (first_step <= i < first_step + steps) reads d_buf[i & 1]
+ * and writes d_buf[(i + 1) & 1]; first_step must equal the number of steps this d_sync has
+ * already run. All d_* arrays are device-resident; world <= 8. */
 typedef struct nbb_p2p {
     int32_t world, rank;
-    const void* d_peer_src;      /* [world] const int64_t*: every rank's source buffer this step */
+    void* d_buf[2];              /* this rank's two compact buffers (3^r int64 each)            */
+    const void* d_peer_buf[2];   /* [world] const int64_t*: every rank's buffer 0 / buffer 1   */
     const void* d_halo_owner;    /* [tiles * 8] uint8: owner rank of each tile's halo cell     */
     void* d_sync;                /* this rank's uint32[4] {arrivals, done, error, 0}, zeroed    */
     const void* d_peer_flag;     /* [world] uint32*: every rank's d_sync (arrival counter)      */
-    uint32_t wait_target;        /* arrivals needed before this step starts (world * step)      */
-    uint32_t timeout_ms;         /* bound on the wait; 0 = 20000                                */
+    uint32_t timeout_ms;         /* bound on each wait; 0 = 20000                               */
 } nbb_p2p;
-int nbb_gpu_ca_compact_step_p2p_dev(const nbb_config* cfg, const void* d_src, void* d_dst,
-                                    uint16_t birth, uint16_t survive, const nbb_p2p* p2p,
-                                    void* stream);
+int nbb_gpu_ca_compact_p2p_dev(const nbb_config* cfg, int64_t first_step, int32_t steps,
+                               uint16_t birth, uint16_t survive, const nbb_p2p* p2p, void* stream);
 /* error flag of d_sync after a step sequence (synchronises the stream): 0 ok, 1 timed out */
 int nbb_gpu_p2p_check(const nbb_p2p* p2p, void* stream);
 /* device memory that can be exported (cudaMalloc: the IPC handle names the allocation) */

@@ -91,11 +91,11 @@ class NbbP2P(Structure):
     _fields_ = [
         ("world", c_int32),
         ("rank", c_int32),
-        ("d_peer_src", c_void_p),
+        ("d_buf", c_void_p * 2),
+        ("d_peer_buf", c_void_p * 2),
         ("d_halo_owner", c_void_p),
         ("d_sync", c_void_p),
         ("d_peer_flag", c_void_p),
-        ("wait_target", ctypes.c_uint32),
         ("timeout_ms", ctypes.c_uint32),
     ]
 
@@ -147,8 +147,9 @@ SIGNATURES = {
     "nbb_gpu_ca_compact_step_dev": (c_int, [CP, c_void_p, c_void_p, c_uint16, c_uint16, c_void_p, RP]),
     "nbb_gpu_reduction_compact_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p, RP]),
     "nbb_gpu_single_write_compact_dev": (c_int, [CP, c_void_p, c_void_p, RP]),
-    "nbb_gpu_ca_compact_step_p2p_dev": (c_int, [CP, c_void_p, c_void_p, c_uint16, c_uint16,
-                                                POINTER(NbbP2P), c_void_p]),
+    "nbb_gpu_ca_compact_run_dev": (c_int, [CP, c_void_p, c_void_p, c_int32, c_uint16, c_uint16, c_void_p]),
+    "nbb_gpu_ca_compact_p2p_dev": (c_int, [CP, ctypes.c_int64, c_int32, c_uint16, c_uint16,
+                                           POINTER(NbbP2P), c_void_p]),
     "nbb_gpu_p2p_check": (c_int, [POINTER(NbbP2P), c_void_p]),
     "nbb_gpu_malloc": (c_int, [c_int32, c_uint64, POINTER(c_void_p)]),
     "nbb_gpu_free": (c_int, [c_int32, c_void_p]),

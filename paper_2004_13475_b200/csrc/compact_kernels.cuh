@@ -187,11 +187,9 @@ constexpr int kMaxP2P = 8;
 struct P2PArgs {
     const long long* const* peer_src;  // [world] each rank's source buffer of this step
     const uint8_t* halo_owner;         // [tiles * 8] rank owning each halo cell
-    unsigned int* flag;                // this rank's arrival counter (peers add to it)
-    unsigned int* const* peer_flag;    // [world] every rank's arrival counter
-    unsigned int* done;                // CTAs of this launch that finished
-    int* error;                        // set to 1 if the wait timed out
-    unsigned int wait_target;          // arrivals required before the step may start
+    unsigned int* sync;                // this rank's {arrivals, done CTAs, error, unused}
+    unsigned int* const* peer_flag;    // [world] every rank's sync word (arrival counter first)
+    unsigned int wait_target;          // arrivals required before the step may start (world x step)
     unsigned int timeout_ms;
     int world, rank;
 };
@@ -202,34 +200,51 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-// one thread per CTA: spin (bounded) until every rank finished the previous step
+// One thread per CTA: spin (bounded) until every rank finished the previous step. Every rank's
+// last CTA of step i-1 adds one arrival here after its CTAs' stores, so world x i arrivals mean
+// every peer's step i-1 output (this step's halo source) is complete AND no peer still reads the
+// buffer this step overwrites (their step i-1 source). This rank's own arrival is included,
+// which orders the step after this rank's previous kernel even when it was launched early (PDL).
 __device__ __forceinline__ void p2p_wait(const P2PArgs& p) {
+    if (p.wait_target == 0u) return;
     const unsigned long long t0 = global_ns();
     unsigned int v;
     for (;;) {
-        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p.flag) : "memory");
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sync) : "memory");
         if (v >= p.wait_target) break;
         if (global_ns() - t0 > 1000000ull * p.timeout_ms) {
-            atomicExch(p.error, 1);
+            atomicExch(p.sync + 2, 1u);
             break;
         }
-        __nanosleep(200);
+        __nanosleep(64);
     }
 }
 
-// after the CTA's last store: the last CTA of the launch announces the step to every rank
+// After the CTA's last store: each CTA counts itself done with an acq_rel atomic at GPU scope
+// (releasing its stores; peers read this GPU's memory through its L2); the last CTA — which has
+// acquired every other CTA's release through that counter — fences once at system scope
+// (cumulative over what it acquired) and announces the step to every rank with relaxed
+// system-scope reductions: one GPU-scope atomic per CTA, one system fence per step.
 __device__ __forceinline__ void p2p_arrive(const P2PArgs& p) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence_system();
-        const unsigned int prev = atomicAdd(p.done, 1u);
+        unsigned int prev;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.sync + 1) : "memory");
         if (prev == gridDim.x - 1) {
-            *p.done = 0u;  // stream order: the next launch starts after this one
-            __threadfence_system();
-            for (int r = 0; r < p.world; ++r) atomicAdd_system(p.peer_flag[r], 1u);
+            // the next step's CTAs count only after they pass their wait (which needs this
+            // CTA's own arrival below, released after this store)
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(p.sync + 1) : "memory");
+            asm volatile("fence.acq_rel.sys;" ::: "memory");
+            for (int r = 0; r < p.world; ++r)
+                asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(p.peer_flag[r]) : "memory");
         }
     }
 }
+
+// Programmatic dependent launch (the next step's CTAs are scheduled while this step drains
+// and run their prologue; griddepcontrol.wait orders them after this grid's stores).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // The 8 halo cells of every ρ = 32 tile as compact offsets (-1: not a member / outside),
 // [tile u][k] for the tile-local positions (-1,-1) (0,-1) (1,-1) (-1,31) (32,30) (32,31)
@@ -268,8 +283,8 @@ __global__ void compact_halo_table_kernel(CompactCaArgs a, FastDiv div_hb, int32
 // owns a contiguous range of tiles in its own replica-sized buffers, the halo cells owned
 // by other ranks are read straight from their buffers over NVLink (CUDA IPC mappings,
 // ld.relaxed.sys), and a flag barrier in peer memory orders the steps: the kernel first
-// waits until every rank has finished the previous step (p.wait_target arrivals on this
-// rank's flag), and its last CTA to finish adds one arrival to every rank's flag.
+// waits until every rank has finished the previous step (world x steps-done arrivals on this
+// rank's counter), and its last CTA to finish adds one arrival to every rank's flag.
 template <bool P2P>
 __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, FastDiv div_hb,
                                                              const int32_t* __restrict__ halo_tab,
@@ -280,10 +295,13 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
     __shared__ const long long* s_peer[kMaxP2P];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint8_t* cell = s_cell[wib];
+    pdl_trigger();
     s_pos[threadIdx.x] = threadIdx.x < 243 ? c_local_pos[threadIdx.x] : 0;
     if (P2P) {
         if (threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
-        if (threadIdx.x == 0 && p.wait_target) p2p_wait(p);
+        if (threadIdx.x == 0) p2p_wait(p);  // subsumes pdl_wait: this rank's own arrival is in it
+    } else {
+        pdl_wait();
     }
     __syncthreads();
     uint32_t sl_off[8], sl_pos[8];

@@ -701,6 +701,24 @@ int compact_halo_table(DeviceCtx* ctx, const nbb_config* cfg, const CompactCaArg
     return NBB_OK;
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may start while the previous
+// kernel on the stream drains; kernels launched this way call griddepcontrol.wait before
+// touching memory the previous kernel writes (ca_compact_kernel: pdl_wait()).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t c = {};
+    c.gridDim = dim3(grid);
+    c.blockDim = dim3(block);
+    c.dynamicSmemBytes = 0;
+    c.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    c.attrs = at;
+    c.numAttrs = 1;
+    return cudaLaunchKernelEx(&c, k, std::forward<Args>(args)...);
+}
+
 int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* dst, uint16_t birth,
                       uint16_t survive, cudaStream_t st) {
     FastDiv div_hb;
@@ -715,8 +733,7 @@ int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, vo
     const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
     if (want == 0) return NBB_OK;
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
-    ca_compact_kernel<false><<<blocks, 256, 0, st>>>(a, div_hb, tab, P2PArgs{});
-    NBB_CUDA(cudaGetLastError());
+    NBB_CUDA(launch_pdl(ca_compact_kernel<false>, blocks, 256, st, a, div_hb, tab, P2PArgs{}));
     return NBB_OK;
 }
 }  // namespace
@@ -1323,29 +1340,40 @@ int nbb_gpu_ca_compact_step_dev(const nbb_config* cfg, const void* d_src, void* 
     return NBB_OK;
 }
 
-int nbb_gpu_ca_compact_step_p2p_dev(const nbb_config* cfg, const void* d_src, void* d_dst, uint16_t birth,
-                                    uint16_t survive, const nbb_p2p* p2p, void* stream) {
+int nbb_gpu_ca_compact_run_dev(const nbb_config* cfg, void* d_a, void* d_b, int32_t steps, uint16_t birth,
+                               uint16_t survive, void* stream) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    if (steps < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "run_ca: steps must be non-negative");
+    NBB_CHECK(compact_workload_check(cfg));
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    for (int32_t i = 0; i < steps; ++i)
+        NBB_CHECK(launch_ca_compact(ctx, cfg, (i & 1) ? d_b : d_a, (i & 1) ? d_a : d_b, birth, survive,
+                                    (cudaStream_t)stream));
+    return NBB_OK;
+}
+
+int nbb_gpu_ca_compact_p2p_dev(const nbb_config* cfg, int64_t first_step, int32_t steps, uint16_t birth,
+                               uint16_t survive, const nbb_p2p* p2p, void* stream) {
     if (!cfg || !p2p) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    if (steps < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "run_ca: steps must be non-negative");
+    if (first_step < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: first_step must be non-negative");
     NBB_CHECK(compact_workload_check(cfg));
     if (p2p->world < 1 || p2p->world > kMaxP2P || p2p->rank < 0 || p2p->rank >= p2p->world)
         return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: need 1 <= world <= 8 and 0 <= rank < world");
-    if (!p2p->d_peer_src || !p2p->d_halo_owner || !p2p->d_sync || !p2p->d_peer_flag)
+    if (!p2p->d_buf[0] || !p2p->d_buf[1] || !p2p->d_peer_buf[0] || !p2p->d_peer_buf[1] ||
+        !p2p->d_halo_owner || !p2p->d_sync || !p2p->d_peer_flag)
         return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: null device array");
     DeviceCtx* ctx;
     NBB_CHECK(ensure_device(cfg->device, &ctx));
     FastDiv div_hb;
-    const CompactCaArgs a = compact_args(cfg, d_src, d_dst, birth, survive, &div_hb);
+    CompactCaArgs a = compact_args(cfg, p2p->d_buf[0], p2p->d_buf[1], birth, survive, &div_hb);
     const int32_t* tab;
     NBB_CHECK(compact_halo_table(ctx, cfg, a, div_hb, &tab));
     P2PArgs p;
-    p.peer_src = (const long long* const*)p2p->d_peer_src;
     p.halo_owner = (const uint8_t*)p2p->d_halo_owner;
-    unsigned int* sync = (unsigned int*)p2p->d_sync;
-    p.flag = sync;
-    p.done = sync + 1;
-    p.error = (int*)(sync + 2);
+    p.sync = (unsigned int*)p2p->d_sync;
     p.peer_flag = (unsigned int* const*)p2p->d_peer_flag;
-    p.wait_target = p2p->wait_target;
     p.timeout_ms = p2p->timeout_ms ? p2p->timeout_ms : 20000u;
     p.world = p2p->world;
     p.rank = p2p->rank;
@@ -1354,11 +1382,20 @@ int nbb_gpu_ca_compact_step_p2p_dev(const nbb_config* cfg, const void* d_src, vo
         NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ca_compact_kernel<true>, 256, 0));
         if (occ < 1) occ = 1;
     }
-    // every rank launches (and arrives) even with an empty shard: one CTA at least
+    // every rank launches (and arrives) even with an empty shard: one CTA at least; at most one
+    // resident wave, so CTAs spinning in the wait never keep a CTA of the same step off an SM
     const uint64_t want = std::max<uint64_t>(1, (a.tile_end - a.tile_begin + 7) / 8);
     const unsigned blocks = (unsigned)std::min<uint64_t>(want, (uint64_t)ctx->sms * occ);
-    ca_compact_kernel<true><<<blocks, 256, 0, (cudaStream_t)stream>>>(a, div_hb, tab, p);
-    NBB_CUDA(cudaGetLastError());
+    // the step loop lives here, not in the caller: one launch per step, back to back on the
+    // stream, no per-step host arguments beyond the ping-pong parity
+    for (int64_t i = first_step; i < first_step + steps; ++i) {
+        const int par = (int)(i & 1);
+        a.src = (const long long*)p2p->d_buf[par];
+        a.dst = (long long*)p2p->d_buf[par ^ 1];
+        p.peer_src = (const long long* const*)p2p->d_peer_buf[par];
+        p.wait_target = (unsigned int)((uint64_t)p2p->world * (uint64_t)i);
+        NBB_CUDA(launch_pdl(ca_compact_kernel<true>, blocks, 256, (cudaStream_t)stream, a, div_hb, tab, p));
+    }
     return NBB_OK;
 }
 

@@ -222,9 +222,25 @@ __global__ void scatter_cells_kernel(Cell* grid, const long long* idx, long long
 }
 
 // ---- K0: λ map of a whole orthotope (scalar closed form) ----------------------
-// 4 ordinals per thread; int32 pairs -> one 32-byte store, int64 pairs -> two.
+// 4 consecutive ordinals per thread (consecutive lanes -> consecutive 32-byte sectors);
+// int32 pairs -> one 32-byte store, int64 pairs -> two. λ is separable:
+// λx = X(ωx) | X(ωy) << 1, λy = Y(ωx) | Y(ωy) << 1, and X/Y of ωx = its low 6 base-3 digits
+// (table entry lo = ωx mod 729) OR its high digits (entry ωx / 729) << 12. Per quad the
+// ωy part and the high digits are folded into two constants, so each ω costs one shared-
+// memory lookup and two logic ops; the rare carries (lo reaching 729, ωx reaching the row
+// end) recompute the constants.
+__device__ __forceinline__ void k0_consts(const uint32_t* s_tab, uint32_t hi, uint32_t oy, uint32_t& kx,
+                                          uint32_t& ky) {
+    uint32_t Xy, Yy;
+    xy_from_table(s_tab, oy, Xy, Yy);
+    const uint32_t b = s_tab[hi];
+    kx = ((b & 0xFFFFu) << 12) | (Xy << 1);
+    ky = ((b >> 16) << 12) | (Yy << 1);
+}
+
 template <typename Coord>
-__global__ void lambda_map_kernel(Coord* xy, uint64_t total, uint32_t gw, FastDiv div_gw) {
+__global__ void __launch_bounds__(256) lambda_map_kernel(Coord* xy, uint64_t total, uint32_t gw,
+                                                         FastDiv div_gw) {
     __shared__ uint32_t s_tab[729];
     for (int i = threadIdx.x; i < 729; i += blockDim.x) s_tab[i] = c_xy729[i];
     __syncthreads();
@@ -234,20 +250,29 @@ __global__ void lambda_map_kernel(Coord* xy, uint64_t total, uint32_t gw, FastDi
         const uint64_t o0 = q * 4;
         uint32_t oy = fastdiv((uint32_t)o0, div_gw);
         uint32_t ox = (uint32_t)o0 - oy * gw;
-        uint32_t Xy, Yy;
-        xy_from_table(s_tab, oy, Xy, Yy);
+        uint32_t hi = __umulhi(ox, 0x59E60383u) >> 8;  // ωx / 729
+        uint32_t lo = ox - hi * 729u;
+        uint32_t kx, ky;
+        k0_consts(s_tab, hi, oy, kx, ky);
         uint32_t lxs[4], lys[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             if (ox == gw) {  // carry into the next orthotope row
                 ox = 0;
+                lo = 0;
+                hi = 0;
                 ++oy;
-                xy_from_table(s_tab, oy, Xy, Yy);
+                k0_consts(s_tab, 0, oy, kx, ky);
+            } else if (lo == 729u) {
+                lo = 0;
+                ++hi;
+                k0_consts(s_tab, hi, oy, kx, ky);
             }
-            uint32_t Xx, Yx;
-            xy_from_table(s_tab, ox, Xx, Yx);
-            lambda_from_xy(Xx, Yx, Xy, Yy, lxs[i], lys[i]);
+            const uint32_t a = s_tab[lo];
+            lxs[i] = (a & 0xFFFFu) | kx;
+            lys[i] = (a >> 16) | ky;
             ++ox;
+            ++lo;
         }
         if (o0 + 4 <= total) {
             if (sizeof(Coord) == 4) {
@@ -275,10 +300,12 @@ __global__ void lambda_map_kernel(Coord* xy, uint64_t total, uint32_t gw, FastDi
                 stg_sector(xy + 2 * o0 + 4, v1);
             }
         } else {
-            for (uint64_t i = 0; o0 + i < total; ++i) {
-                xy[2 * (o0 + i)] = (Coord)lxs[i];
-                xy[2 * (o0 + i) + 1] = (Coord)lys[i];
-            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)  // fixed indices: keeps lxs/lys in registers
+                if (o0 + i < total) {
+                    xy[2 * (o0 + i)] = (Coord)lxs[i];
+                    xy[2 * (o0 + i) + 1] = (Coord)lys[i];
+                }
         }
     }
 }

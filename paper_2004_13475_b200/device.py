@@ -78,6 +78,14 @@ def ca_compact_step_dev(config: DispatchConfig, d_src: int, d_dst: int, rule: Ca
     return WorkReport.from_c(rep)
 
 
+def ca_compact_run_dev(config: DispatchConfig, d_a: int, d_b: int, steps: int, rule: CaRule = CaRule(),
+                       stream: int = 0) -> None:
+    """`steps` steps ping-ponging d_a <-> d_b, issued by the library (result in d_a if steps
+    is even, else d_b)."""
+    _check(_lib().nbb_gpu_ca_compact_run_dev(ctypes.byref(config.to_c()), _vp(d_a), _vp(d_b), steps,
+                                             rule.birth, rule.survive, _vp(stream)))
+
+
 def reduction_compact_dev(config: DispatchConfig, d_compact: int, d_value: int, stream: int = 0) -> WorkReport:
     rep = _abi.NbbReport()
     _check(_lib().nbb_gpu_reduction_compact_dev(ctypes.byref(config.to_c()), _vp(d_compact),

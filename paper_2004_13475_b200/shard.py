@@ -270,7 +270,7 @@ class P2PCompactCA:
     Every rank allocates its two compact buffers and a 16-byte sync word with cudaMalloc
     (nbb_gpu_malloc), exports them as CUDA IPC handles, opens every peer's (one
     all_gather_object at setup), and then runs each step as ONE launch of
-    nbb_gpu_ca_compact_step_p2p_dev: the kernel waits on its arrival counter until all ranks
+    nbb_gpu_ca_compact_p2p_dev (the step loop in C++): each kernel waits until all ranks
     finished the previous step, reads the ≤ 8 halo cells per tile that other ranks own
     straight from their buffers (NVLink loads through the IPC mappings), writes its own tiles,
     and its last CTA adds one arrival to every rank's counter. No host synchronisation and
@@ -318,50 +318,49 @@ class P2PCompactCA:
                 self._opened.append(p.value)
             peers.append(ptrs)
         dev = torch.device("cuda", device)
-        self._peer_src = [torch.tensor([peers[r][b] for r in range(plan.world)], dtype=torch.int64,
+        self._peer_buf = [torch.tensor([peers[r][b] for r in range(plan.world)], dtype=torch.int64,
                                        device=dev) for b in (0, 1)]
         self._peer_flag = torch.tensor([peers[r][2] for r in range(plan.world)], dtype=torch.int64,
                                        device=dev)
         self._owner = torch.from_numpy(plan.halo_owner_table()).to(dev)
         self.buffers = [torch.as_tensor(_DevArray(p, self.count), device=dev) for p in self._own[:2]]
+        self._args = _abi.NbbP2P(plan.world, plan.rank, (ctypes.c_void_p * 2)(*self._own[:2]),
+                                 (ctypes.c_void_p * 2)(*(t.data_ptr() for t in self._peer_buf)),
+                                 self._owner.data_ptr(), self._own[2], self._peer_flag.data_ptr(),
+                                 timeout_ms)
         self.step_index = 0
 
     def load(self, compact_state) -> None:
         """Set the state (a (3^r,) int64 tensor; this rank's tiles must be current). Collective:
-        every rank loads before any rank's first step reads a peer."""
+        every rank loads before any rank's first step reads a peer. Call once, before the
+        first step (the device step counter starts at 0)."""
         import torch
+        if self.step_index:
+            raise RuntimeError("P2PCompactCA.load: the step sequence has already started")
         self.buffers[0].copy_(compact_state.to(self.buffers[0].device).view(-1))
         torch.cuda.synchronize(self.device)
         self.dist.barrier()
-        self.step_index = 0
 
     def state(self):
         """The current state buffer (this rank's tiles are current)."""
         return self.buffers[self.step_index & 1]
 
-    def _p2p(self):
-        from . import _abi
-        i = self.step_index
-        return _abi.NbbP2P(self.plan.world, self.plan.rank, self._peer_src[i & 1].data_ptr(),
-                           self._owner.data_ptr(), self._own[2], self._peer_flag.data_ptr(),
-                           self.plan.world * i, self.timeout_ms)
+    def run(self, config, rule, steps: int, stream) -> None:
+        """`steps` steps, one kernel per step issued back to back by the library."""
+        import ctypes
+        c = self.plan.local_config(config).to_c()
+        _check(self.lib.nbb_gpu_ca_compact_p2p_dev(
+            ctypes.byref(c), self.step_index, steps, rule.birth, rule.survive,
+            ctypes.byref(self._args), ctypes.c_void_p(stream)))
+        self.step_index += steps
 
     def step(self, config, rule, stream) -> None:
-        import ctypes
-        i = self.step_index
-        p = self._p2p()
-        c = self.plan.local_config(config).to_c()
-        _check(self.lib.nbb_gpu_ca_compact_step_p2p_dev(
-            ctypes.byref(c), ctypes.c_void_p(self.buffers[i & 1].data_ptr()),
-            ctypes.c_void_p(self.buffers[(i + 1) & 1].data_ptr()), rule.birth, rule.survive,
-            ctypes.byref(p), ctypes.c_void_p(stream)))
-        self.step_index = i + 1
+        self.run(config, rule, 1, stream)
 
     def check(self, stream) -> None:
         """Raise if any step timed out waiting for the other ranks (synchronises)."""
         import ctypes
-        p = self._p2p()
-        _check(self.lib.nbb_gpu_p2p_check(ctypes.byref(p), ctypes.c_void_p(stream)))
+        _check(self.lib.nbb_gpu_p2p_check(ctypes.byref(self._args), ctypes.c_void_p(stream)))
 
     def close(self) -> None:
         """Collective: no rank unmaps or frees while a peer's step may still read it."""

@@ -239,6 +239,22 @@ def test_lambda_coords_map_kernels(golden):
     assert np.array_equal(nbb.lambda_coords(cfg(), 9), orc_lambda_coords(9))
 
 
+@pytest.mark.parametrize("level", [11, 13, 16, 17])
+def test_lambda_map_full_levels(level):
+    """K0 over whole orthotopes up to the C4 sweep's top level (row carries at W = 3^⌈L/2⌉,
+    the 729-entry digit carries, a quad tail when 3^L is odd): int32 pairs on the device and
+    int64 pairs through the host call, bit-exact against the C oracle."""
+    import torch
+    from paper_2004_13475_b200 import device as dev
+    want = orc_lambda_coords(level)
+    s = torch.cuda.current_stream().cuda_stream
+    xy = torch.empty((3 ** level, 2), dtype=torch.int32, device="cuda")
+    dev.lambda_coords_dev(cfg(), level, xy.data_ptr(), 4, s)
+    assert np.array_equal(xy.cpu().numpy().astype(np.int64), want)
+    del xy
+    assert np.array_equal(nbb.lambda_coords(cfg(), level), want)
+
+
 def test_workers_shard_the_ordinal_range():
     """Contiguous ordinal chunks (dispatch.cpp:419-427) give identical results for any count."""
     r = 9

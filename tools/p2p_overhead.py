@@ -1,0 +1,80 @@
+"""Per-rank cost of one compact CA step at N ranks, measured on ONE GPU (gpurun has 1 GPU).
+
+For each level r in {16, 17} and N in {1, 2, 4, 8}, rank 0's shard (chunk = ceil(tiles / N),
+dispatch.cpp:419-427) is stepped K times back to back by the library's C++ step loop:
+  plain : ca_compact_kernel<false> on the shard (nbb_gpu_ca_compact_run_dev, no exchange) —
+          the compute floor of one rank;
+  p2p   : ca_compact_kernel<true> on the shard with world = 1 (nbb_gpu_ca_compact_p2p_dev: the
+          flag wait / arrive protocol and the peer-table halo path run; the barrier partner is
+          this GPU itself — what a real N-GPU run adds is one NVLink round trip per step).
+Prints one JSON line; ms per step = CUDA-event time / K.
+"""
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2004_13475_b200 import _abi, nbb, shard  # noqa: E402
+from paper_2004_13475_b200 import device as dev  # noqa: E402
+
+K = int(os.environ.get("K", "400"))
+s = torch.cuda.current_stream().cuda_stream
+lib = _abi.load()
+out = {}
+
+
+def timed(run):
+    run(6)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    run(K)
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / K
+
+
+for r in (16, 17):
+    members = 3 ** r
+    c1 = torch.zeros(members, dtype=torch.int64, device="cuda")
+    c1.random_(0, 2)
+    c2 = torch.zeros_like(c1)
+    base = nbb.DispatchConfig(r=r, rho=32, max_cells=(1 << r) ** 2)
+    for N in (1, 2, 4, 8):
+        plan = shard.ShardPlan(r=r, rho=32, world=N, rank=0, state="compact")
+        lc = plan.local_config(base)
+        t_plain = timed(lambda k: dev.ca_compact_run_dev(lc, c1.data_ptr(), c2.data_ptr(), k, nbb.CaRule(), s))
+
+        sync = torch.zeros(4, dtype=torch.int32, device="cuda")
+        peer = [torch.tensor([b.data_ptr()], dtype=torch.int64, device="cuda") for b in (c1, c2)]
+        peer_flag = torch.tensor([sync.data_ptr()], dtype=torch.int64, device="cuda")
+        owner = torch.zeros(plan.total * 8, dtype=torch.uint8, device="cuda")
+        args = _abi.NbbP2P(1, 0, (ctypes.c_void_p * 2)(c1.data_ptr(), c2.data_ptr()),
+                           (ctypes.c_void_p * 2)(peer[0].data_ptr(), peer[1].data_ptr()),
+                           owner.data_ptr(), sync.data_ptr(), peer_flag.data_ptr(), 20000)
+        cc = lc.to_c()
+        st = {"i": 0}
+
+        def p2p(k):
+            rc = lib.nbb_gpu_ca_compact_p2p_dev(ctypes.byref(cc), st["i"], k, 8, 12, ctypes.byref(args),
+                                                ctypes.c_void_p(s))
+            assert rc == 0, lib.nbb_gpu_last_error()
+            st["i"] += k
+        t_p2p = timed(p2p)
+        torch.cuda.synchronize()
+        assert int(sync[2].item()) == 0, "a wait timed out"
+        assert int(sync[0].item()) == st["i"], (int(sync[0].item()), st["i"])
+        out[f"r{r}_N{N}"] = {"tiles": plan.count, "plain_ms": t_plain, "p2p_world1_ms": t_p2p}
+    one = out[f"r{r}_N1"]["plain_ms"]
+    for N in (1, 2, 4, 8):
+        d = out[f"r{r}_N{N}"]
+        d["ideal_ms"] = one / N
+        d["efficiency_plain"] = one / N / d["plain_ms"]
+        d["efficiency_p2p_world1"] = one / N / d["p2p_world1_ms"]
+    del c1, c2
+print(json.dumps(out))
