@@ -123,7 +123,7 @@ def _p2p_worker(rank, world, port, r, steps, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,r", [(2, 10), (3, 11)])
+@pytest.mark.parametrize("world,r", [(2, 10), (3, 11), (4, 12)])
 def test_p2p_compact_ca_on_gpu(world, r):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -4,9 +4,11 @@ For each level r in {16, 17} and N in {1, 2, 4, 8}, rank 0's shard (chunk = ceil
 dispatch.cpp:419-427) is stepped K times back to back by the library's C++ step loop:
   plain : ca_compact_kernel<false> on the shard (nbb_gpu_ca_compact_run_dev, no exchange) —
           the compute floor of one rank;
-  p2p   : ca_compact_kernel<true> on the shard with world = 1 (nbb_gpu_ca_compact_p2p_dev: the
-          flag wait / arrive protocol and the peer-table halo path run; the barrier partner is
-          this GPU itself — what a real N-GPU run adds is one NVLink round trip per step).
+  p2p   : ca_compact_kernel<true> on the shard (nbb_gpu_ca_compact_p2p_dev) with the real
+          owner table and phase split of world N, every peer mapped to this process (peer
+          buffers and flags = ours, N arrivals per step): the interior/boundary phases, the
+          wait / arrive protocol and the remote-halo path all run; what a real N-GPU run adds
+          is NVLink latency on the remote halo loads and the arrivals.
 Prints one JSON line; ms per step = CUDA-event time / K.
 """
 import ctypes
@@ -51,10 +53,12 @@ for r in (16, 17):
         t_plain = timed(lambda k: dev.ca_compact_run_dev(lc, c1.data_ptr(), c2.data_ptr(), k, nbb.CaRule(), s))
 
         sync = torch.zeros(4, dtype=torch.int32, device="cuda")
-        peer = [torch.tensor([b.data_ptr()], dtype=torch.int64, device="cuda") for b in (c1, c2)]
-        peer_flag = torch.tensor([sync.data_ptr()], dtype=torch.int64, device="cuda")
-        owner = torch.zeros(plan.total * 8, dtype=torch.uint8, device="cuda")
-        args = _abi.NbbP2P(1, 0, (ctypes.c_void_p * 2)(c1.data_ptr(), c2.data_ptr()),
+        # every "peer" is this process: N entries pointing at our own buffers and sync word, so
+        # the real owner table, phase split and barrier target (N arrivals per step) all run
+        peer = [torch.tensor([b.data_ptr()] * N, dtype=torch.int64, device="cuda") for b in (c1, c2)]
+        peer_flag = torch.tensor([sync.data_ptr()] * N, dtype=torch.int64, device="cuda")
+        owner = torch.from_numpy(plan.halo_owner_table()).cuda()
+        args = _abi.NbbP2P(N, 0, (ctypes.c_void_p * 2)(c1.data_ptr(), c2.data_ptr()),
                            (ctypes.c_void_p * 2)(peer[0].data_ptr(), peer[1].data_ptr()),
                            owner.data_ptr(), sync.data_ptr(), peer_flag.data_ptr(), 20000)
         cc = lc.to_c()
@@ -68,7 +72,7 @@ for r in (16, 17):
         t_p2p = timed(p2p)
         torch.cuda.synchronize()
         assert int(sync[2].item()) == 0, "a wait timed out"
-        assert int(sync[0].item()) == st["i"], (int(sync[0].item()), st["i"])
+        assert int(sync[0].item()) == N * st["i"], (int(sync[0].item()), st["i"])
         out[f"r{r}_N{N}"] = {"tiles": plan.count, "plain_ms": t_plain, "p2p_world1_ms": t_p2p}
     one = out[f"r{r}_N1"]["plain_ms"]
     for N in (1, 2, 4, 8):
