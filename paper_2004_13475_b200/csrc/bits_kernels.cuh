@@ -34,7 +34,22 @@ __global__ void __launch_bounds__(256) ca_bits_kernel(TileArgs a) {
     const int hx = (hk == 0 || hk == 3) ? -1 : (hk == 1 || hk == 7) ? 0 : (hk == 2) ? 1 : 32;
     const int hy = (hk <= 2) ? -1 : (hk == 3 || hk == 5) ? 31 : (hk == 4) ? 30 : 32;
 
-    for (uint32_t u = warp_global; u < units; u += warp_stride) {
+    // BB: odd warp stride (see tile_kernel) and whole-tile culling: a bounding-box tile holds a
+    // member iff bx ⊆ (n/32 - 1 - by); a unit without one is skipped (warp-uniform)
+    const uint32_t ustride = BB ? (warp_stride | 1u) - ((warp_stride & 1u) ? 0u : 2u) : warp_stride;
+    const uint32_t ustart = (BB && warp_global >= ustride) ? units : warp_global;
+    for (uint32_t u = ustart; u < units; u += ustride) {
+        if (BB) {
+            bool any = false;
+#pragma unroll
+            for (int i = 0; i < ILP; ++i) {
+                const uint32_t tl = u * ILP + i;
+                const uint32_t t = a.tile_begin + tl;
+                const uint32_t gy = fastdiv(t, a.div_gw), gx = t - gy * a.gw;
+                any |= tl < a.tiles && (gx & ((nm1 >> 5) - gy)) == 0u;
+            }
+            if (!any) continue;
+        }
         uint32_t X0[ILP], Y0[ILP], memb[ILP], R[ILP], hw[ILP];
         bool ok[ILP], hact[ILP];
         uint32_t hbitpos[ILP];

@@ -966,7 +966,11 @@ int nbb_gpu_lambda_coords_dev(const nbb_config* cfg, int32_t level, void* d_xy, 
     f.d = (uint32_t)w;
     nbbhost::fastdiv_magic(f.d, &f.m, &f.s);
     cudaStream_t s = (cudaStream_t)stream;
-    const int blocks = ctx->sms * 8;
+    // one wave at most, no more blocks than the work needs (small levels are launch-bound:
+    // every block stages the 729-entry digit table)
+    const uint64_t per_block = tc ? 16ull * 8 : 4ull * 256;  // ω per block and pass
+    const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sms * 8,
+                                                                      (total + per_block - 1) / per_block));
     if (tc) {
         if (coord_bytes == 4)
             lambda_map_tc_kernel<int32_t><<<blocks, 256, 0, s>>>((int32_t*)d_xy, total, (uint32_t)w, f, level);

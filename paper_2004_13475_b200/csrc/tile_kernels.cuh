@@ -144,7 +144,13 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs a) {
     const char* src = static_cast<const char*>(a.src);
     char* dst = static_cast<char*>(a.dst);
 
-    for (uint32_t u = warp_global; u < units; u += warp_stride) {
+    // BB: an odd warp stride (one warp idles when the grid's warp count is even). The bounding
+    // box's member tiles are bx ⊆ (n/ρ - 1 - by); with an even stride (a multiple of a large
+    // power of two) a warp would always see the same low bits of bx and the members would
+    // pile onto a few warps (ncu: 11-15% warps active); an odd stride cycles every residue.
+    const uint32_t ustride = BB ? (warp_stride | 1u) - ((warp_stride & 1u) ? 0u : 2u) : warp_stride;
+    const uint32_t ustart = (BB && warp_global >= ustride) ? units : warp_global;
+    for (uint32_t u = ustart; u < units; u += ustride) {
         // ---- tile origins (lane computes its own tile j = lane / RHO) ----------
         const uint32_t t_local = u * TPW + my_j;
         const bool my_tile_ok = t_local < a.tiles;
@@ -160,7 +166,12 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs a) {
         }
         const uint32_t X0 = bx * RHO, Y0 = by * RHO;
         const int64_t my_base = ((int64_t)Y0 * n + X0) * (int64_t)sizeof(Cell);
-        const uint32_t tiles_ok = __ballot_sync(0xFFFFFFFFu, my_tile_ok && my_y == 0);
+        // BB: a tile of the bounding box holds a member iff bx ⊆ (n/ρ - 1 - by) (its cell
+        // (X0, Y0 + ρ - 1) is then one); the reference's threads of such a block all fail
+        // their membership test and return, so the warp skips the tile outright
+        const bool has_member = !BB || (bx & ((nm1 >> (31 - __clz(RHO))) - by)) == 0u;
+        const uint32_t tiles_ok = __ballot_sync(0xFFFFFFFFu, my_tile_ok && has_member && my_y == 0);
+        if (BB && tiles_ok == 0u) continue;
 
         // ---- stage 1: loads / stores of the slots ----------------------------
         uint32_t slot_nib[SLOTS];
@@ -194,12 +205,16 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs a) {
             continue;
         }
         if (OP == OP_RD) {
+            // all of the unit's loads in flight before the first add (the predicated
+            // load-add pairs would otherwise serialise one DRAM round trip per slot)
+            Sector v[SLOTS];
 #pragma unroll
             for (int k = 0; k < SLOTS; ++k) {
-                if (slot_nib[k]) {
-                    const Sector v = ldg_sector(src + slot_base[k] + sl_off[k]);
-                    acc += masked_sum4(v, slot_nib[k]);
-                }
+                if (slot_nib[k]) v[k] = ldg_sector(src + slot_base[k] + sl_off[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < SLOTS; ++k) {
+                if (slot_nib[k]) acc += masked_sum4(v[k], slot_nib[k]);
             }
             continue;
         }
