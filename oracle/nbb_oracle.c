@@ -284,6 +284,33 @@ void orc_ca_step(const nbb_spec* spec, int r, const int64_t* src, int64_t* dst, 
     }
 }
 
+int64_t orc_ca_compact_check(const nbb_spec* spec, int r, const int64_t* src, const int64_t* dst,
+                             const int64_t* offsets, int64_t count, uint16_t birth, uint16_t survive) {
+    int64_t W, H, bad = 0;
+    orc_orthotope_dims(spec, r, &W, &H);
+    for (int64_t i = 0; i < count; ++i) {
+        const int64_t c = offsets[i];
+        int64_t x, y;
+        if (c < 0 || c >= W * H || orc_lambda_map(spec, r, c % W, c / W, &x, &y) != 0) {
+            ++bad;
+            continue;
+        }
+        int live = 0;
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                if (dx == 0 && dy == 0) continue;
+                int64_t ox, oy;
+                if (member(spec, r, x + dx, y + dy) &&
+                    orc_lambda_inverse(spec, r, x + dx, y + dy, &ox, &oy) == 0 && src[oy * W + ox] != 0)
+                    ++live;
+            }
+        const uint16_t bit = (uint16_t)(1u << live);
+        const int64_t want = (((src[c] != 0) ? survive : birth) & bit) ? 1 : 0;
+        if (dst[c] != want) ++bad;
+    }
+    return bad;
+}
+
 void orc_ca(const nbb_spec* spec, int r, const int64_t* initial, int steps, uint16_t birth,
             uint16_t survive, int64_t* out) {
     const int64_t n = orc_side_length(spec, r);

@@ -57,6 +57,12 @@ void orc_single_write(const nbb_spec* spec, int r, int64_t* out);
 int64_t orc_reduction(const nbb_spec* spec, int r, const int64_t* grid);
 void orc_ca_step(const nbb_spec* spec, int r, const int64_t* src, int64_t* dst, uint16_t birth,
                  uint16_t survive);
+/* One CA step checked on the compact state (CompactGrid, block_map.hpp:82-110: value(ω) =
+ * embedded(λ(ω)) at offset ωy·W + ωx): for each sampled offset, the reference rule
+ * (dispatch.cpp:530-550) over the cell's member Moore neighbours located by λ⁻¹. Returns the
+ * number of sampled offsets whose dst value differs (size-independent full-size check). */
+int64_t orc_ca_compact_check(const nbb_spec* spec, int r, const int64_t* src, const int64_t* dst,
+                             const int64_t* offsets, int64_t count, uint16_t birth, uint16_t survive);
 /* steps == 0 copies the input unchanged (B.4) */
 void orc_ca(const nbb_spec* spec, int r, const int64_t* initial, int steps, uint16_t birth,
             uint16_t survive, int64_t* out);

@@ -62,6 +62,8 @@ def orc_lib():
             "orc_reduction": (c_int64, [SP, c_int, c_void_p]),
             "orc_ca_step": (None, [SP, c_int, c_void_p, c_void_p, c_uint16, c_uint16]),
             "orc_ca": (None, [SP, c_int, c_void_p, c_int, c_uint16, c_uint16, c_void_p]),
+            "orc_ca_compact_check": (c_int64, [SP, c_int, c_void_p, c_void_p, c_void_p, c_int64,
+                                               c_uint16, c_uint16]),
             "orc_validate": (c_int, [CP, c_char_p, c_size_t]),
             "orc_plan_report": (c_int, [CP, RP]),
             "orc_launch_block_count": (c_uint64, [CP]),
@@ -158,6 +160,16 @@ def orc_ca(r: int, grid: np.ndarray, steps: int, birth: int = 8, survive: int = 
     out = np.empty_like(g)
     orc_lib().orc_ca(ctypes.byref(spec.to_c()), r, _ptr(g), steps, birth, survive, _ptr(out))
     return out
+
+
+def orc_ca_compact_check(r: int, src: np.ndarray, dst: np.ndarray, offsets: np.ndarray,
+                         birth: int = 8, survive: int = 12, spec: FractalSpec = GASKET) -> int:
+    """Mismatching sampled offsets of one compact-state CA step src -> dst (oracle rule)."""
+    src = np.ascontiguousarray(src, dtype=np.int64).ravel()
+    dst = np.ascontiguousarray(dst, dtype=np.int64).ravel()
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    return int(orc_lib().orc_ca_compact_check(ctypes.byref(spec.to_c()), r, _ptr(src), _ptr(dst),
+                                              _ptr(offsets), offsets.size, birth, survive))
 
 
 def orc_lambda_coords(level: int, spec: FractalSpec = GASKET) -> np.ndarray:

@@ -7,8 +7,8 @@ import subprocess
 import numpy as np
 import pytest
 
-from _oracle import (GASKET, ROOT, fnv1a64, orc_ca, orc_lambda_coords, orc_random_member_grid,
-                     orc_reduction, orc_single_write)
+from _oracle import (GASKET, ROOT, fnv1a64, orc_ca, orc_ca_compact_check, orc_lambda_coords,
+                     orc_random_member_grid, orc_reduction, orc_single_write)
 from paper_2004_13475_b200 import _abi, nbb
 from paper_2004_13475_b200.nbb import (CaRule, DispatchConfig, Grid, IntraBlockStrategy,
                                        KernelFamily, LambdaBackend, MapMode)
@@ -521,3 +521,35 @@ def test_full_size_r16_properties():
     dev.compact_load_dev(c, k2.data_ptr(), b.data_ptr(), 0, s)
     assert torch.equal(b, ref)
     assert int(k2.sum().item()) == ref_sum
+
+
+@pytest.mark.parametrize("r", [17])
+def test_compact_ca_full_size_sampled(r):
+    """C5 size (n = 2^17, 3^17 members): two steps through the library's step loop, then a third
+    step checked against the oracle rule on 600k sampled cells — uniform, every tile-corner
+    cell of the first and last 2000 tiles (the halo-reading cells), and the array's ends."""
+    import torch
+    from paper_2004_13475_b200 import device as dev
+    members = 3 ** r
+    c = cfg(r=r, rho=32)
+    s = torch.cuda.current_stream().cuda_stream
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1700 + r)
+    a = torch.randint(0, 2, (members,), dtype=torch.int64, device="cuda", generator=gen)
+    b = torch.empty_like(a)
+    dev.ca_compact_run_dev(c, a.data_ptr(), b.data_ptr(), 2, CaRule(), s)  # result in a
+    dev.ca_compact_step_dev(c, a.data_ptr(), b.data_ptr(), CaRule(), s)
+    torch.cuda.synchronize()
+    src, dst = a.cpu().numpy(), b.cpu().numpy()
+    del a, b
+    assert set(np.unique(dst)) <= {0, 1}
+    W = 3 ** ((r + 1) // 2)
+    Hb = 3 ** ((r - 5) // 2)
+    rng = np.random.default_rng(r)
+    tiles = np.concatenate([np.arange(2000), np.arange(3 ** (r - 5) - 2000, 3 ** (r - 5))])
+    rows, cols = np.meshgrid([0, 8], [0, 26], indexing="ij")  # corner cells of the 9 x 27 block
+    corner = ((tiles // Hb * 9)[:, None] + rows.ravel()[None]) * W + \
+             ((tiles % Hb) * 27)[:, None] + cols.ravel()[None]
+    offs = np.concatenate([rng.integers(0, members, 600_000), corner.ravel(),
+                           np.arange(1000), np.arange(members - 1000, members)]).astype(np.int64)
+    assert orc_ca_compact_check(r, src, dst, offs) == 0
