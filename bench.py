@@ -445,7 +445,9 @@ def main():
         sweep = {}
         for lvl in (10, 12, 14, 16, 17):
             row = {"omegas": 3 ** lvl}
-            for label, be in (("scalar", nbb.LambdaBackend.Direct), ("tensor_core", nbb.LambdaBackend.MmaV2)):
+            for label, be in (("scalar", nbb.LambdaBackend.Direct),
+                              ("tensor_core_tcgen05", nbb.LambdaBackend.MmaV2),
+                              ("tensor_core_mma_sync", nbb.LambdaBackend.MmaV1)):
                 if be != nbb.LambdaBackend.Direct and lvl > 16:
                     continue
                 c = cfg(backend=be)

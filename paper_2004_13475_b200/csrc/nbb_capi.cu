@@ -971,7 +971,18 @@ int nbb_gpu_lambda_coords_dev(const nbb_config* cfg, int32_t level, void* d_xy, 
     const uint64_t per_block = tc ? 16ull * 8 : 4ull * 256;  // ω per block and pass
     const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)ctx->sms * 8,
                                                                       (total + per_block - 1) / per_block));
-    if (tc) {
+    if (tc && cfg->backend == NBB_BACKEND_MMA2) {
+        // K0-TC on tcgen05 (5th-gen tensor core, accumulator in TMEM): 128 ω per CTA tile,
+        // 16 CTAs per SM (32 of the 512 TMEM columns and 13 KB smem each): the per-tile
+        // build -> MMA -> tcgen05.ld chain is latency-bound, other CTAs fill the gaps
+        const unsigned tc_blocks = (unsigned)std::max<uint64_t>(
+            1, std::min<uint64_t>((uint64_t)ctx->sms * 16, (total + 127) / 128));
+        if (coord_bytes == 4)
+            lambda_map_tc5_kernel<int32_t><<<tc_blocks, 128, 0, s>>>((int32_t*)d_xy, total, (uint32_t)w, f);
+        else
+            lambda_map_tc5_kernel<long long><<<tc_blocks, 128, 0, s>>>((long long*)d_xy, total, (uint32_t)w, f);
+    } else if (tc) {
+        // K0-TC on the warp-level mma.sync path (the paper's 16 x 16 fragment product)
         if (coord_bytes == 4)
             lambda_map_tc_kernel<int32_t><<<blocks, 256, 0, s>>>((int32_t*)d_xy, total, (uint32_t)w, f, level);
         else

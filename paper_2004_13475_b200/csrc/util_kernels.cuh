@@ -15,6 +15,8 @@
 #include "common.cuh"
 #include "percell_kernels.cuh"
 
+#include <cuda_bf16.h>
+
 namespace nbbgpu {
 
 // ---- sanitize ---------------------------------------------------------------
@@ -378,6 +380,137 @@ __global__ void lambda_map_tc_kernel(Coord* xy, uint64_t total, uint32_t gw, Fas
             }
         }
     }
+}
+
+// ---- K0-TC on the 5th-generation tensor core (tcgen05 + TMEM) ----------------------
+// The paper's MMA λ (mma.cpp:34-118, variant 1) as one tcgen05.mma per 128 ordinals and 16
+// levels: D[128 ω x 16] (fp32, TMEM) = A[128 x 32] (bf16, smem) · B[32 x 16] (bf16, smem) with
+// A[i][k] = τx(β_{k+1}(ω_i)) for k < 16 and τy(β_{k-15}(ω_i)) for k >= 16, B[k][0] = 2^k (k < 16),
+// B[k][1] = 2^(k-16) (k >= 16), other columns 0, so D[i][0..1] = λ(ω_i). τx(β) = [β == 2] and
+// τy(β) = [β >= 1] of the level's base-3 digit are bit μ-1 of X(ωx) | X(ωy) << 1 and
+// Y(ωx) | Y(ωy) << 1, read from the 729-entry digit table. Exact: 0/1 and
+// powers of two <= 2^15 are exact in bf16, sums < 2^16 in fp32.
+//
+// One CTA = 4 warps = 128 ordinals per tile (thread i builds A row i), persistent over tiles:
+// build A -> fence.proxy.async -> one elected thread issues 2 x tcgen05.mma (M=128, N=16,
+// K=16) and commits to an mbarrier -> every warp tcgen05.ld's its 32 TMEM lanes (2 columns)
+// -> 8-byte stores. Operands in the canonical no-swizzle K-major layout: 8-row x 16-byte core
+// matrices, K-adjacent core matrices 128 B apart (LBO), 8-row groups 512 B apart (SBO).
+__device__ __forceinline__ uint64_t umma_smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100)
+    return d;                // base offset 0, legacy LBO mode, layout SWIZZLE_NONE (0)
+}
+
+template <typename Coord>
+__global__ void __launch_bounds__(128) lambda_map_tc5_kernel(Coord* xy, uint64_t total, uint32_t gw,
+                                                             FastDiv div_gw) {
+    constexpr uint32_t IDESC = (1u << 4)      // D format f32
+                             | (1u << 7)      // A format bf16
+                             | (1u << 10)     // B format bf16
+                             | (2u << 17)     // N = 16 (>> 3)
+                             | (8u << 24);    // M = 128 (>> 4); A, B K-major
+    __shared__ __align__(128) uint8_t s_a[128 * 64];  // [16 row groups][4 k chunks][8 rows][16 B]
+    __shared__ __align__(128) uint8_t s_b[16 * 64];   // [2 col groups][4 k chunks][8 cols][16 B]
+    __shared__ uint32_t s_tab[729];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ uint32_t s_tmem;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    for (uint32_t i = tid; i < 729; i += 128) s_tab[i] = c_xy729[i];
+    // B: column n (= "row" of the K-major B), k chunk c holds k = 8c..8c+7
+    for (uint32_t e = tid; e < 16 * 32; e += 128) {
+        const uint32_t n = e >> 5, k = e & 31;
+        float v = 0.f;
+        if (n == 0 && k < 16) v = (float)(1u << k);
+        if (n == 1 && k >= 16) v = (float)(1u << (k - 16));
+        const uint32_t off = (n >> 3) * 512 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
+        *reinterpret_cast<__nv_bfloat16*>(s_b + off) = __float2bfloat16_rn(v);
+    }
+    if (warp == 0) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_tmem);
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(dst));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = s_tmem;
+    const uint32_t a_base = (uint32_t)__cvta_generic_to_shared(s_a);
+    const uint32_t b_base = (uint32_t)__cvta_generic_to_shared(s_b);
+    // this thread's A row: row group tid >> 3, row tid & 7
+    uint8_t* my_row = s_a + (tid >> 3) * 512 + (tid & 7) * 16;
+    uint32_t phase = 0;
+    const uint64_t tiles = (total + 127) / 128;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const uint64_t o = t * 128 + tid;
+        uint32_t lx = 0, ly = 0;
+        if (o < total) {
+            const uint32_t oy = fastdiv((uint32_t)o, div_gw), ox = (uint32_t)o - oy * gw;
+            uint32_t Xx, Yx, Xy, Yy;
+            xy_from_table(s_tab, ox, Xx, Yx);
+            xy_from_table(s_tab, oy, Xy, Yy);
+            lambda_from_xy(Xx, Yx, Xy, Yy, lx, ly);  // bit μ-1: τx / τy of level μ
+        }
+        // A row: k < 16 -> τx bits, k >= 16 -> τy bits, as bf16 1.0 (0x3F80) or 0
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t bits = (c < 2 ? lx : ly) >> (8 * (c & 1));
+            uint32_t w[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+                w[h] = (((bits >> (2 * h)) & 1u) ? 0x3F80u : 0u) | (((bits >> (2 * h + 1)) & 1u) ? 0x3F800000u : 0u);
+            *reinterpret_cast<uint4*>(my_row + c * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const uint64_t da = umma_smem_desc(a_base + ks * 256, 128, 512);
+                const uint64_t db = umma_smem_desc(b_base + ks * 256, 128, 512);
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                    "l"(da), "l"(db), "r"(IDESC), "r"(ks));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                         : "memory");
+        }
+        // wait for the MMAs (they also finished reading s_a)
+        {
+            uint32_t done = 0;
+            while (!done)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                    "selp.u32 %0, 1, 0, p;\n\t}\n"
+                    : "=r"(done) : "r"(bar), "r"(phase) : "memory");
+            phase ^= 1u;
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        uint32_t d0, d1;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                     : "=r"(d0), "=r"(d1) : "r"(tmem + ((warp * 32u) << 16)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (o < total) {
+            xy[2 * o] = (Coord)__float2uint_rn(__uint_as_float(d0));
+            xy[2 * o + 1] = (Coord)__float2uint_rn(__uint_as_float(d1));
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();  // TMEM and s_a are rewritten by the next tile
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
 }
 
 }  // namespace nbbgpu

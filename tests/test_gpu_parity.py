@@ -233,9 +233,10 @@ def test_lambda_coords_map_kernels(golden):
     for level in range(0, 16):
         want = golden["lambda_digests"][str(level)]
         assert fnv1a64(nbb.lambda_coords(cfg(r=level), level)) == want, level
-        if level <= 16:
-            got = nbb.lambda_coords(cfg(r=level, backend=LambdaBackend.MmaV2), level)
-            assert fnv1a64(got) == want, ("tc", level)
+        if level <= 16:  # K0-TC: mma.sync (MmaV1) and tcgen05 + TMEM (MmaV2)
+            for be in (LambdaBackend.MmaV1, LambdaBackend.MmaV2):
+                got = nbb.lambda_coords(cfg(r=level, backend=be), level)
+                assert fnv1a64(got) == want, ("tc", be, level)
     assert np.array_equal(nbb.lambda_coords(cfg(), 9), orc_lambda_coords(9))
 
 
@@ -251,6 +252,9 @@ def test_lambda_map_full_levels(level):
     xy = torch.empty((3 ** level, 2), dtype=torch.int32, device="cuda")
     dev.lambda_coords_dev(cfg(), level, xy.data_ptr(), 4, s)
     assert np.array_equal(xy.cpu().numpy().astype(np.int64), want)
+    if level <= 16:  # the tcgen05 K0-TC at full size too (int32 pairs)
+        dev.lambda_coords_dev(cfg(backend=LambdaBackend.MmaV2), level, xy.data_ptr(), 4, s)
+        assert np.array_equal(xy.cpu().numpy().astype(np.int64), want)
     del xy
     assert np.array_equal(nbb.lambda_coords(cfg(), level), want)
 
