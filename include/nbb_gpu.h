@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define NBB_GPU_ABI_VERSION 1
+#define NBB_GPU_ABI_VERSION 2
 #define NBB_MAX_REPLICAS 9
 
 /* Status codes; the C++ shim (nbb_gpu.hpp) rethrows the matching std:: type. */

@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol():
     for name in names:
         assert hasattr(lib, name), name
         assert name in _abi.SIGNATURES, f"{name} missing from _abi.SIGNATURES"
-    assert lib.nbb_gpu_abi_version() == 1
+    assert lib.nbb_gpu_abi_version() == 2
 
 
 def test_library_is_sm100a_and_native():
@@ -183,6 +183,31 @@ def test_cpp_shim_compiles():
     r = subprocess.run([out, "--host-only"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "sierpinski,8,1,lambda,subbox,direct,6561,6561,6561,0,59049,0" in r.stdout
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors (_abi.py) have the header's sizes and field offsets (gcc -> offsetof)."""
+    structs = {"nbb_spec": _abi.NbbSpec, "nbb_config": _abi.NbbConfig, "nbb_report": _abi.NbbReport,
+               "nbb_p2p": _abi.NbbP2P}
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "nbb_gpu.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for f in py._fields_:
+            lines.append(f'printf("{cname} {f[0]} %zu\\n", offsetof({cname}, {f[0]}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["/usr/bin/gcc", "-std=c11", f"-I{os.path.join(ROOT, 'include')}", str(src), "-o", str(exe)],
+                   check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        c, f, v = line.split()
+        got[(c, f)] = int(v)
+    for cname, py in structs.items():
+        assert got[(cname, "sizeof")] == ctypes.sizeof(py), cname
+        for f in py._fields_:
+            assert got[(cname, f[0])] == getattr(py, f[0]).offset, (cname, f[0])
 
 
 def test_nbbmap_quotient_format_matches_cpp():
