@@ -56,4 +56,38 @@ for fl, cw in ((_abi.FLAG_OUT_ZEROED, 8), (_abi.FLAG_OUT_ZEROED | _abi.FLAG_COMP
                                   ctypes.c_void_p(h_out.data_ptr()), None) == 0
     assert np.array_equal(h_out.numpy(), want), (fl, cw)
     checks += 1
+# λ map kernels: scalar K0, tcgen05 K0-TC, mma.sync K0-TC
+from _oracle import orc_lambda_coords  # noqa: E402
+for be in (nbb.LambdaBackend.Direct, nbb.LambdaBackend.MmaV2, nbb.LambdaBackend.MmaV1):
+    assert np.array_equal(nbb.lambda_coords(nbb.DispatchConfig(r=r, rho=1, backend=be), r),
+                          orc_lambda_coords(r)), be
+    checks += 1
+# compact CA: the library's multi-step loop (PDL launches) and the P2P kernel (2-rank owner
+# table and phase of rank 0, every peer mapped to this process)
+from paper_2004_13475_b200 import device as dev, shard  # noqa: E402
+cx, cy = orc_lambda_coords(r)[:, 0], orc_lambda_coords(r)[:, 1]
+comp0 = torch.from_numpy(g[cy, cx].copy()).cuda()
+ca, cb = comp0.clone(), torch.empty_like(comp0)
+s = torch.cuda.current_stream().cuda_stream
+cfg = nbb.DispatchConfig(r=r, rho=32)
+dev.ca_compact_run_dev(cfg, ca.data_ptr(), cb.data_ptr(), 3, nbb.CaRule(), s)
+assert np.array_equal(cb.cpu().numpy(), want[cy, cx])
+checks += 1
+plan = shard.ShardPlan(r=r, rho=32, world=2, rank=0, state="compact")
+ca, cb = comp0.clone(), torch.zeros_like(comp0)  # rank 0 writes only its tiles
+sync = torch.zeros(4, dtype=torch.int32, device="cuda")
+peers = [torch.tensor([t.data_ptr()] * 2, dtype=torch.int64, device="cuda") for t in (ca, cb)]
+flags = torch.tensor([sync.data_ptr()] * 2, dtype=torch.int64, device="cuda")
+owner = torch.from_numpy(plan.halo_owner_table()).cuda()
+args = _abi.NbbP2P(2, 0, (ctypes.c_void_p * 2)(ca.data_ptr(), cb.data_ptr()),
+                   (ctypes.c_void_p * 2)(peers[0].data_ptr(), peers[1].data_ptr()), owner.data_ptr(),
+                   sync.data_ptr(), flags.data_ptr(), 20000)
+cc = plan.local_config(cfg).to_c()
+assert _abi.load().nbb_gpu_ca_compact_p2p_dev(ctypes.byref(cc), 0, 1, 8, 12, ctypes.byref(args),
+                                              ctypes.c_void_p(s)) == 0
+torch.cuda.synchronize()
+own = plan.owner(plan.tile_of_ordinal(shard.lambda_inverse_blocks(cx >> 5, cy >> 5, plan.r_b, plan.W))) == 0
+assert np.array_equal(cb.cpu().numpy()[own], orc_ca(r, g, 1)[cy, cx][own])
+assert int(sync[0].item()) == 2 and int(sync[2].item()) == 0
+checks += 1
 print(f"sanitize_run ok: r={r}, {checks} checks")
