@@ -292,22 +292,28 @@ def main():
             state["i"] = i + 1
         return step
 
-    def timed_run(run, K, W, sampler=None):
-        """run(k) issues k steps on `stream`; W warm-up steps, then K timed with CUDA events."""
+    def timed_run(run, K, W, sampler=None, groups=None):
+        """run(k) issues k steps on `stream`; W warm-up steps, then K timed with CUDA events.
+        groups (a list) receives the per-step means of G equal sub-runs (events between them)."""
         run(W)
         barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        G = 10 if (groups is not None and K >= 10) else 1
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(G + 1)]
         if sampler:
             sampler.__enter__()
-        e0.record(stream)
-        run(K)
-        e1.record(stream)
-        e1.synchronize()
+        ev[0].record(stream)
+        for gi in range(G):
+            k = K // G + (1 if gi < K % G else 0)
+            run(k)
+            ev[gi + 1].record(stream)
+        ev[G].synchronize()
         if sampler:
             sampler.__exit__()
         barrier()
-        return max_over_ranks(e0.elapsed_time(e1)) / K  # ms per step
+        if groups is not None and G > 1:
+            groups.extend(ev[gi].elapsed_time(ev[gi + 1]) / (K // G + (1 if gi < K % G else 0))
+                          for gi in range(G))
+        return max_over_ranks(ev[0].elapsed_time(ev[G])) / K  # ms per step
 
     def timed(step, K, W, sampler=None):
         def run(k):
@@ -337,6 +343,7 @@ def main():
     results = {}
 
     # ---- headline: λ(ω) CA step on the compact state, ρ = 32 tiles ---------------------
+    head_groups = []  # per-step means of 10 sub-runs (N = 1): median / paper-style mean
     # the step loop runs in the library (C++; one kernel per step, PDL between steps)
     if world > 1 and args.transport == "p2p":
         p2p = shard.P2PCompactCA(plan_c, dist, device=local)
@@ -348,7 +355,7 @@ def main():
         head_ms = timed(compact_runner(cfg(), c1, c2), K, W, sampler)
     else:
         head_ms = timed_run(lambda k: dev.ca_compact_run_dev(cfg(), c1.data_ptr(), c2.data_ptr(), k,
-                                                             nbb.CaRule(), s), K, W, sampler)
+                                                             nbb.CaRule(), s), K, W, sampler, head_groups)
     value = members * 1e3 / head_ms  # all ranks together update the 3^r cells per step
     results["ca_lambda_compact_i64"] = head_ms
     # ---- C5: the same step on the gasket at n = 2^17 (BASELINE configs[4]), sharded by
@@ -570,6 +577,13 @@ def main():
                 "hw_min_bytes_per_step": 1088391168 + 612220032,
                 "achieved_GBps_vs_hw_min": (1088391168 + 612220032) / (emb_ms * 1e-3) / 1e9},
         },
+        "timing": {"ms_per_step_mean": head_ms,
+                   "sub_runs": len(head_groups),
+                   "ms_per_step_median_of_sub_runs": statistics.median(head_groups) if head_groups else None,
+                   "ms_per_step_mean_of_sub_averages": statistics.mean(head_groups) if head_groups else None,
+                   "ms_per_step_min_max_sub_run": [min(head_groups), max(head_groups)] if head_groups else None,
+                   "note": "CUDA events on the launching stream; K steps split into equal sub-runs "
+                           "(SURVEY 8(d): median and the paper's mean of sub-averages)"},
         "clocks": sampler.summary(),
         "speedup_vs_bb": {
             "ca_lambda_compact_over_bb_tile_i64": ratio("ca_bb_tile_rho32_i64", "ca_lambda_compact_i64"),
