@@ -175,7 +175,7 @@ def config_block(r, rho, world=1, transport="p2p"):
                            f"{world} ranks: contiguous tile-range shards; " + (
                                "halo cells read over peer memory (CUDA IPC) inside the step kernel"
                                if transport == "p2p" else
-                               "halo cells exchanged by gather + NCCL all_to_all + scatter"),
+                               f"halo cells exchanged by gather + NCCL all_to_all + scatter ({transport})"),
             "l2": "no flush: each step moves 689 MB compact / 1.7 GB embedded (> 126 MB L2)"}
 
 
@@ -345,8 +345,15 @@ def main():
     # ---- headline: λ(ω) CA step on the compact state, ρ = 32 tiles ---------------------
     head_groups = []  # per-step means of 10 sub-runs (N = 1): median / paper-style mean
     # the step loop runs in the library (C++; one kernel per step, PDL between steps)
+    p2p = None
     if world > 1 and args.transport == "p2p":
-        p2p = shard.P2PCompactCA(plan_c, dist, device=local)
+        try:
+            p2p = shard.P2PCompactCA(plan_c, dist, device=local)
+        except shard.P2PUnavailable as e:  # every rank agrees; run the NCCL exchange instead
+            print(f"bench: {e}; falling back to --transport nccl", file=sys.stderr)
+            args.transport = "nccl (p2p unavailable)"
+            launches_per_step = 3
+    if p2p is not None:
         p2p.load(c1)
         head_ms = timed_run(lambda k: p2p.run(cfg(), nbb.CaRule(), k, s), K, W, sampler)
         p2p.check(s)

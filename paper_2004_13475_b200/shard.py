@@ -264,6 +264,10 @@ class _DevArray:
                                          "data": (ptr, False), "version": 3}
 
 
+class P2PUnavailable(RuntimeError):
+    """CUDA IPC peer mappings could not be opened on every rank (raised on all ranks alike)."""
+
+
 class P2PCompactCA:
     """Multi-GPU compact CA where the exchange lives inside the step kernel.
 
@@ -305,18 +309,33 @@ class P2PCompactCA:
         dist.all_gather_object(gathered, handles)
         self._opened = []
         peers = []
-        for r, hs in enumerate(gathered):
-            if r == plan.rank:
-                peers.append(self._own)
-                continue
-            ptrs = []
-            for h in hs:
-                p = ctypes.c_void_p()
-                _check(lib.nbb_gpu_ipc_open(device, (ctypes.c_uint8 * 64).from_buffer_copy(h),
-                                            ctypes.byref(p)))
-                ptrs.append(p.value)
-                self._opened.append(p.value)
-            peers.append(ptrs)
+        err = None
+        try:
+            for r, hs in enumerate(gathered):
+                if r == plan.rank:
+                    peers.append(self._own)
+                    continue
+                ptrs = []
+                for h in hs:
+                    p = ctypes.c_void_p()
+                    _check(lib.nbb_gpu_ipc_open(device, (ctypes.c_uint8 * 64).from_buffer_copy(h),
+                                                ctypes.byref(p)))
+                    ptrs.append(p.value)
+                    self._opened.append(p.value)
+                peers.append(ptrs)
+        except Exception as e:  # noqa: BLE001 - agreed on below, raised on every rank
+            err = e
+        # every rank must agree, or one rank would wait in a step kernel for a peer that gave up
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32,
+                          device=torch.device("cuda", device) if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            for ptr in self._opened:
+                lib.nbb_gpu_ipc_close(device, ctypes.c_void_p(ptr))
+            for ptr in self._own:
+                lib.nbb_gpu_free(device, ctypes.c_void_p(ptr))
+            self._opened, self._own = [], []
+            raise P2PUnavailable(f"peer mappings unavailable on some rank ({err or 'another rank'})")
         dev = torch.device("cuda", device)
         self._peer_buf = [torch.tensor([peers[r][b] for r in range(plan.world)], dtype=torch.int64,
                                        device=dev) for b in (0, 1)]
