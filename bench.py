@@ -443,10 +443,12 @@ def main():
             return lambda: dev.reduction_dev(c, a.data_ptr(), out.data_ptr(), s)
         for name, c in {"sw_lambda_tile_rho32": cfg(), "sw_bb_tile_rho32": cfg(mode=nbb.MapMode.BoundingBox),
                         "sw_bb_percell_rho32": cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell),
+                        "sw_lambda_percell_rho32": cfg(kernel=nbb.KernelFamily.PerCell),
                         "sw_lambda_percell_rho16": cfg(rho=16, kernel=nbb.KernelFamily.PerCell)}.items():
             results[name] = timed(sw(c), K if "tile" in name else max(5, K // 10), W)
         for name, c in {"rd_lambda_tile_rho32": cfg(), "rd_bb_tile_rho32": cfg(mode=nbb.MapMode.BoundingBox),
                         "rd_bb_percell_rho32": cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell),
+                        "rd_lambda_percell_rho32": cfg(kernel=nbb.KernelFamily.PerCell),
                         "rd_lambda_percell_rho16": cfg(rho=16, kernel=nbb.KernelFamily.PerCell)}.items():
             results[name] = timed(rd(c), K if "tile" in name else max(5, K // 10), W)
         results["rd_lambda_compact_i64"] = timed(
@@ -603,6 +605,12 @@ def main():
             "sw_bb_tile_over_lambda_tile": ratio("sw_bb_tile_rho32", "sw_lambda_tile_rho32"),
             "rd_bb_tile_over_lambda_tile": ratio("rd_bb_tile_rho32", "rd_lambda_tile_rho32"),
             "rd_bb_tile_over_lambda_compact": ratio("rd_bb_tile_rho32", "rd_lambda_compact_i64"),
+            # the paper's own comparison (one thread per cell, ρ = 32 blocks; PAPER.md:548-549
+            # reports 6x-12x at n = 2^16 on Titan V / Titan RTX)
+            "paper_percell_rho32": {
+                "sw": ratio("sw_bb_percell_rho32", "sw_lambda_percell_rho32"),
+                "rd": ratio("rd_bb_percell_rho32", "rd_lambda_percell_rho32"),
+                "ca": ratio("ca_bb_percell_rho32_i64", "ca_lambda_percell_rho32_i64")},
         },
         "workloads_ms": results,
         "workloads_cells_per_s": {k: cells(k) for k in results},
