@@ -63,18 +63,33 @@ __global__ void compact_load_kernel(DevSpec sp, const long long* comp, long long
     }
 }
 
-// Σ of a dense int64 array (every compact value is a member), wrap-around like int64 +
-__global__ void __launch_bounds__(256) dense_sum_kernel(const long long* p, uint64_t count,
-                                                        unsigned long long* out) {
+// A shard of the compact state as memory segments: tiles u in [b, e) of the order
+// u = ωx_b·H_b + ωy_b (a tile = 9 compact rows x 27 columns, a tile row = 9 full compact rows):
+// a partial tile row at each end (9 segments of 27·k values each) and the full tile rows between
+// (one contiguous segment) — at most 19 segments; the whole array is the single segment (0, 3^r).
+constexpr int kMaxSegs = 20;
+struct Segs {
+    uint64_t off[kMaxSegs];
+    uint64_t cnt[kMaxSegs];
+    int n;
+};
+
+// Σ of the segments' values (int64, wrapping like the reference's accumulation): per segment
+// an unaligned head, 32-byte sector loads, a tail; warp shuffle + block reduction, one atomic
+// per block.
+__global__ void __launch_bounds__(256) segment_sum_kernel(const long long* p, Segs sg, unsigned long long* out) {
     unsigned long long acc = 0;
-    const uint64_t vec = count / 4;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < vec; i += stride) {
-        const Sector s = ldg_sector(p + 4 * i);
-        acc += masked_sum4(s, 0xFu);
+    for (int k = 0; k < sg.n; ++k) {
+        const uint64_t o = sg.off[k], c = sg.cnt[k];
+        const uint64_t head = min(c, (4u - (o & 3u)) & 3u);
+        const uint64_t vec = (c - head) / 4, body = o + head;
+        for (uint64_t i = tid; i < head; i += stride) acc += (unsigned long long)p[o + i];
+#pragma unroll 4
+        for (uint64_t i = tid; i < vec; i += stride) acc += masked_sum4(ldg_sector(p + body + 4 * i), 0xFu);
+        for (uint64_t i = body + 4 * vec + tid; i < o + c; i += stride) acc += (unsigned long long)p[i];
     }
-    for (uint64_t i = 4 * vec + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride)
-        acc += (unsigned long long)p[i];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
     __shared__ unsigned long long s[8];
@@ -84,6 +99,26 @@ __global__ void __launch_bounds__(256) dense_sum_kernel(const long long* p, uint
         unsigned long long t = 0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
         if (t) atomicAdd(out, t);
+    }
+}
+
+// SW on the segments: every member value <- v (32-byte sector stores in the aligned body)
+__global__ void __launch_bounds__(256) segment_fill_kernel(long long* p, Segs sg, long long v) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    Sector sv;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        sv.w[2 * i] = (uint32_t)(unsigned long long)v;
+        sv.w[2 * i + 1] = (uint32_t)((unsigned long long)v >> 32);
+    }
+    for (int k = 0; k < sg.n; ++k) {
+        const uint64_t o = sg.off[k], c = sg.cnt[k];
+        const uint64_t head = min(c, (4u - (o & 3u)) & 3u);
+        const uint64_t vec = (c - head) / 4, body = o + head;
+        for (uint64_t i = tid; i < head; i += stride) p[o + i] = v;
+        for (uint64_t i = tid; i < vec; i += stride) stg_sector(p + body + 4 * i, sv);
+        for (uint64_t i = body + 4 * vec + tid; i < o + c; i += stride) p[i] = v;
     }
 }
 

@@ -620,6 +620,39 @@ int compact_shape(const nbb_config* cfg, CompactShape* s) {
     if (s->n > (int64_t(1) << 20)) return fail(NBB_ERR_RESOURCE, "embedding too large for the device path");
     return NBB_OK;
 }
+// The compact-state memory of cfg's shard (all of it without a shard): Segs (compact_kernels.cuh)
+int compact_segments(const nbb_config* cfg, Segs* sg) {
+    CompactShape cs;
+    NBB_CHECK(compact_shape(cfg, &cs));
+    int64_t wb, hb;
+    NBB_TRY(nbbhost::orthotope_dims(cfg->spec, cfg->r - 5, &wb, &hb));
+    const uint64_t tiles = (uint64_t)wb * (uint64_t)hb, Hb = (uint64_t)hb, W = cs.W;
+    uint64_t b = 0, e = tiles;
+    if (cfg->shard_count > 0) {
+        b = std::min<uint64_t>(cfg->shard_begin, tiles);
+        e = std::min<uint64_t>(b + cfg->shard_count, tiles);
+    }
+    sg->n = 0;
+    for (uint64_t u = b; u < e;) {
+        const uint64_t wxb = u / Hb, c0 = u % Hb;
+        if (c0 == 0 && e - u >= Hb) {  // whole tile rows: one contiguous run of compact rows
+            const uint64_t k = (e - u) / Hb;
+            sg->off[sg->n] = 9 * wxb * W;
+            sg->cnt[sg->n] = 9 * W * k;
+            ++sg->n;
+            u += k * Hb;
+        } else {  // part of one tile row: 9 row pieces of 27 values per tile
+            const uint64_t c1 = std::min<uint64_t>(Hb, c0 + (e - u));
+            for (uint64_t row = 0; row < 9; ++row) {
+                sg->off[sg->n] = (9 * wxb + row) * W + 27 * c0;
+                sg->cnt[sg->n] = 27 * (c1 - c0);
+                ++sg->n;
+            }
+            u += c1 - c0;
+        }
+    }  // at most: a partial tile row (9) + whole tile rows (1) + a partial tile row (9) = 19
+    return NBB_OK;
+}
 unsigned grid_for(const DeviceCtx* c, uint64_t work) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, (uint64_t)c->sms * 16));
 }
@@ -1467,14 +1500,14 @@ int nbb_gpu_reduction_compact_dev(const nbb_config* cfg, const void* d_compact, 
                                   nbb_report* report) {
     if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
     NBB_CHECK(compact_workload_check(cfg));
-    CompactShape s;
-    NBB_CHECK(compact_shape(cfg, &s));
+    Segs sg;
+    NBB_CHECK(compact_segments(cfg, &sg));
     DeviceCtx* ctx;
     NBB_CHECK(ensure_device(cfg->device, &ctx));
     Timer t(cfg->timing != 0, (cudaStream_t)stream);
     NBB_CUDA(cudaMemsetAsync(d_value, 0, 8, (cudaStream_t)stream));
-    dense_sum_kernel<<<ctx->sms * 4, 256, 0, (cudaStream_t)stream>>>((const long long*)d_compact, s.total,
-                                                                      (unsigned long long*)d_value);
+    segment_sum_kernel<<<ctx->sms * 4, 256, 0, (cudaStream_t)stream>>>((const long long*)d_compact, sg,
+                                                                        (unsigned long long*)d_value);
     NBB_CUDA(cudaGetLastError());
     fill_report(cfg, report, t.stop_micros());
     return NBB_OK;
@@ -1483,12 +1516,12 @@ int nbb_gpu_reduction_compact_dev(const nbb_config* cfg, const void* d_compact, 
 int nbb_gpu_single_write_compact_dev(const nbb_config* cfg, void* d_compact, void* stream, nbb_report* report) {
     if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
     NBB_CHECK(compact_workload_check(cfg));
-    CompactShape s;
-    NBB_CHECK(compact_shape(cfg, &s));
+    Segs sg;
+    NBB_CHECK(compact_segments(cfg, &sg));
     DeviceCtx* ctx;
     NBB_CHECK(ensure_device(cfg->device, &ctx));
     Timer t(cfg->timing != 0, (cudaStream_t)stream);
-    fill_kernel<<<ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>((long long*)d_compact, s.total, 1);
+    segment_fill_kernel<<<ctx->sms * 8, 256, 0, (cudaStream_t)stream>>>((long long*)d_compact, sg, 1);
     NBB_CUDA(cudaGetLastError());
     fill_report(cfg, report, t.stop_micros());
     return NBB_OK;

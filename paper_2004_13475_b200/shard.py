@@ -181,6 +181,24 @@ class ShardPlan:
     def halo_cells_received(self) -> int:
         return int(sum(self.recv_counts))
 
+    def compact_segments(self):
+        """(offset, count) runs of the compact state holding this rank's tiles (state="compact"):
+        the same decomposition the library's compact RD / SW use (nbb_capi.cu compact_segments):
+        a tile u = ωx_b·H_b + ωy_b is 9 compact rows x 27 columns, a tile row 9 full rows."""
+        W = 27 * self.Hb
+        segs, u, e = [], self.begin, self.begin + self.count
+        while u < e:
+            wxb, c0 = divmod(u, self.Hb)
+            if c0 == 0 and e - u >= self.Hb:
+                k = (e - u) // self.Hb
+                segs.append((9 * wxb * W, 9 * W * k))
+                u += k * self.Hb
+            else:
+                c1 = min(self.Hb, c0 + (e - u))
+                segs += [((9 * wxb + row) * W + 27 * c0, 27 * (c1 - c0)) for row in range(9)]
+                u += c1 - c0
+        return segs
+
     def local_config(self, config):
         """The launch config restricted to this rank's chunk of block ordinals."""
         import copy
@@ -220,6 +238,40 @@ class ShardPlan:
             dist.all_to_all_single(recv, send, output_split_sizes=self.recv_counts,
                                    input_split_sizes=self.send_counts, group=group)
         scatter(flat, ridx, recv)
+
+
+def sharded_reduction(plan: ShardPlan, config, d_state: int, dist, stream: int = 0,
+                      device: int = 0) -> int:
+    """run_reduction over the shards (dispatch.cpp:490-515): each rank sums its own tiles on its
+    GPU (embedded grid: the tile kernels on cfg.shard_*; compact state: the segments of its
+    tiles), then ONE int64 all-reduce (NCCL; gloo when ranks share a GPU) — the final reduction.
+    int64 addition wraps like the reference's, so the partial sums add up exactly."""
+    import torch
+    from . import device as dev
+    c = plan.local_config(config)
+    part = torch.zeros(1, dtype=torch.int64, device=torch.device("cuda", device))
+    if plan.state == "compact":
+        dev.reduction_compact_dev(c, d_state, part.data_ptr(), stream)
+    else:
+        dev.reduction_dev(c, d_state, part.data_ptr(), stream)
+    if plan.world > 1:
+        if dist.get_backend() == "nccl":
+            dist.all_reduce(part)
+        else:
+            h = part.cpu()
+            dist.all_reduce(h)
+            part = h
+    return int(part.item())
+
+
+def sharded_single_write(plan: ShardPlan, config, d_state: int, stream: int = 0) -> None:
+    """run_single_write over the shards: each rank writes its own tiles; no exchange."""
+    from . import device as dev
+    c = plan.local_config(config)
+    if plan.state == "compact":
+        dev.single_write_compact_dev(c, d_state, stream)
+    else:
+        dev.single_write_dev(c, d_state, stream)
 
 
 def _cfg_for(t):

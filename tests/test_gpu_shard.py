@@ -138,3 +138,60 @@ def test_p2p_compact_ca_on_gpu(world, r):
         assert p.exitcode == 0
     want = orc_ca(r, orc_random_member_grid(r, 4321, 2), steps)
     assert np.array_equal(got, want)
+
+
+def _rd_worker(rank, world, port, r, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2004_13475_b200 import nbb
+    from paper_2004_13475_b200.shard import (ShardPlan, lambda_blocks, sharded_reduction,
+                                             sharded_single_write)
+    n = 1 << r
+    # values near 2^62 so the int64 sum wraps, as the reference's accumulation does
+    g = orc_random_member_grid(r, 99, 1 << 62)
+    c = nbb.DispatchConfig(r=r, rho=32, max_cells=n * n)
+    out = {}
+    for state in ("embedded", "compact"):
+        plan = ShardPlan(r=r, rho=32, world=world, rank=rank, state=state)
+        if state == "compact":
+            cx, cy = lambda_blocks(np.arange(3 ** r, dtype=np.int64), 3 ** ((r + 1) // 2))
+            a = torch.from_numpy(g[cy, cx].copy()).cuda()
+        else:
+            a = torch.from_numpy(g.copy()).cuda()
+        out[state] = sharded_reduction(plan, c, a.data_ptr(), dist,
+                                       torch.cuda.current_stream().cuda_stream)
+        b = torch.zeros_like(a)
+        sharded_single_write(plan, c, b.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        bh = b.cpu()
+        dist.all_reduce(bh)  # every rank wrote only its own tiles: the sum is the full write
+        out[state + "_sw"] = bh.numpy()
+    if rank == 0:
+        q.put(out)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,r", [(2, 10), (3, 11)])
+def test_sharded_reduction_and_single_write(world, r):
+    """RD = per-rank partial sums over each rank's tiles + ONE all-reduce; SW = each rank writes
+    its own tiles. Both states, values that make the int64 sum wrap."""
+    from _oracle import orc_reduction, orc_single_write
+    from paper_2004_13475_b200.shard import lambda_blocks
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rd_worker, args=(i, world, port, r, q)) for i in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    g = orc_random_member_grid(r, 99, 1 << 62)
+    want = orc_reduction(r, g)
+    assert got["embedded"] == want and got["compact"] == want
+    sw = orc_single_write(r)
+    assert np.array_equal(got["embedded_sw"], sw)
+    cx, cy = lambda_blocks(np.arange(3 ** r, dtype=np.int64), 3 ** ((r + 1) // 2))
+    assert np.array_equal(got["compact_sw"], sw[cy, cx])

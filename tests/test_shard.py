@@ -157,3 +157,25 @@ def test_lambda_inverse_blocks_round_trip():
         t = np.arange(3 ** r_b, dtype=np.int64)
         bx, by = lambda_blocks(t, W)
         assert np.array_equal(lambda_inverse_blocks(bx, by, r_b, W), t)
+
+
+@pytest.mark.parametrize("r", [8, 10, 11])
+def test_compact_segments_partition_the_state(r):
+    """The compact RD / SW shard decomposition: each rank's (offset, count) runs are exactly the
+    cells of its tiles (tile u = 9 compact rows x 27 columns at (9·u // H_b, 27·u % H_b)), and
+    over the ranks they cover the 3^r values once."""
+    W = 3 ** ((r + 1) // 2)
+    for world in (1, 2, 3, 5, 8):
+        cover = np.zeros(3 ** r, dtype=np.int64)
+        for k in range(world):
+            plan = ShardPlan(r=r, rho=32, world=world, rank=k, state="compact")
+            segs = plan.compact_segments()
+            assert len(segs) <= 19
+            mine = np.concatenate([np.arange(o, o + c) for o, c in segs]) if segs else np.zeros(0, int)
+            u = np.arange(plan.begin, plan.begin + plan.count)
+            rows = (9 * (u // plan.Hb))[:, None] + np.arange(9)[None, :]
+            want = (rows[:, :, None] * W + (27 * (u % plan.Hb))[:, None, None] +
+                    np.arange(27)[None, None, :]).ravel()
+            assert np.array_equal(np.sort(mine), np.sort(want)), (world, k)
+            cover[mine] += 1
+        assert np.all(cover == 1), world
