@@ -342,6 +342,15 @@ def main():
     sampler = ClockSampler(local)
     results = {}
 
+    # ---- RD (the global reduction) on the compact state: each rank sums its own tiles, then
+    # one int64 all-reduce (NCCL) — the value back on the host every call ----------------
+    rd_val = shard.sharded_reduction(plan_c, cfg(), c1.data_ptr(), dist, s, local)
+    rd_ms = timed(lambda: shard.sharded_reduction(plan_c, cfg(), c1.data_ptr(), dist, s, local),
+                  max(10, K // 4), W)
+    rd_line = {"workload": f"run_reduction on the compact state at n=2^{r}: per-rank partial over its "
+                           f"tiles (segment_sum_kernel) + one int64 all-reduce, value read back on the host; state = the initial random_member_grid",
+               "ms_per_call": rd_ms, "value": members * 1e3 / rd_ms, "unit": "cells/s",
+               "GBps_per_gpu": 8 * members / world / (rd_ms * 1e-3) / 1e9, "sum": rd_val}
     # ---- headline: λ(ω) CA step on the compact state, ρ = 32 tiles ---------------------
     head_groups = []  # per-step means of 10 sub-runs (N = 1): median / paper-style mean
     # the step loop runs in the library (C++; one kernel per step, PDL between steps)
@@ -616,6 +625,7 @@ def main():
         "workloads_cells_per_s": {k: cells(k) for k in results},
         "map_sweep_C4": sweep,
         "c5_r17": c5,
+        "rd_compact": rd_line,
         "cpu_baseline": cpu,
         "e2e": e2e,
     }
