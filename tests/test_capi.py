@@ -210,6 +210,23 @@ def test_struct_layouts_match_header(tmp_path):
             assert got[(cname, f[0])] == getattr(py, f[0]).offset, (cname, f[0])
 
 
+def build_launch_example(out="/tmp/nbb_launch_example"):
+    """tests/cuda/launch_example.cu: include/nbb_launch.cuh (the reference's launch(config,
+    kernel) for device functors) compiled by nvcc into the caller's own binary."""
+    src = os.path.join(ROOT, "tests", "cuda", "launch_example.cu")
+    lib_dir = os.path.dirname(_abi.LIB_PATH)
+    subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2",
+                    "-std=c++17", f"-I{os.path.join(ROOT, 'include')}", src, "-o", out,
+                    f"-L{lib_dir}", "-lnbbgpu", "-Xlinker", "-rpath", "-Xlinker", lib_dir], check=True)
+    return out
+
+
+def test_device_functor_launch_compiles_and_fails_loudly_without_gpu():
+    exe = build_launch_example()
+    r = subprocess.run([exe, "--host-only"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 def test_nbbmap_quotient_format_matches_cpp():
     """nbbmap prints the quotient with std::ostream defaults (%g, 6 significant)."""
     from _oracle import ref_available, ref_lib

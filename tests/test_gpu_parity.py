@@ -557,3 +557,20 @@ def test_compact_ca_full_size_sampled(r):
     offs = np.concatenate([rng.integers(0, members, 600_000), corner.ravel(),
                            np.arange(1000), np.arange(members - 1000, members)]).astype(np.int64)
     assert orc_ca_compact_check(r, src, dst, offs) == 0
+
+
+@pytest.mark.parametrize("rho,mode", [(1, "lambda"), (4, "lambda"), (32, "lambda"), (8, "bb"), (32, "bb")])
+def test_device_functor_launch(rho, mode):
+    """include/nbb_launch.cuh — launch(config, kernel) with device functors: run_single_write and
+    run_reduction written as functors give the oracle's grid and sum, over λ and BB launches."""
+    import subprocess
+    from test_capi import build_launch_example
+    r, seed = 10, 31
+    exe = build_launch_example("/tmp/nbb_launch_example_gpu")
+    out = subprocess.run([exe, str(r), str(rho), mode, str(seed)], capture_output=True, text=True,
+                         timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    f = out.stdout.split()
+    assert f[1] == fnv1a64(orc_single_write(r))
+    assert int(f[3]) == orc_reduction(r, orc_random_member_grid(r, seed, 1000))
+    assert int(f[7]) == 3 ** r  # active threads = the members (closed-form counters)
