@@ -574,3 +574,23 @@ def test_device_functor_launch(rho, mode):
     assert f[1] == fnv1a64(orc_single_write(r))
     assert int(f[3]) == orc_reduction(r, orc_random_member_grid(r, seed, 1000))
     assert int(f[7]) == 3 ** r  # active threads = the members (closed-form counters)
+
+
+def test_host_buffer_compact_ca_pinned_zero_copy():
+    """nbb_gpu_ca on pinned host Grids with FLAG_OUT_ZEROED | FLAG_COMPACT_STATE: member sectors
+    read and written zero-copy (the e2e path of the bench) — bit-exact with the oracle at
+    n = 2^13, twice (cached device buffers)."""
+    import ctypes
+    import torch
+    r, steps = 13, 3
+    n = 1 << r
+    g = orc_random_member_grid(r, 2024, 2)
+    want = orc_ca(r, g, steps)
+    hin = torch.from_numpy(g.copy()).pin_memory()
+    for trial in range(2):  # the second call reuses the cached device buffers
+        hout = torch.zeros((n, n), dtype=torch.int64).pin_memory()
+        cc = cfg(r=r, rho=32, flags=_abi.FLAG_OUT_ZEROED | _abi.FLAG_COMPACT_STATE).to_c()
+        rc = _abi.load().nbb_gpu_ca(ctypes.byref(cc), ctypes.c_void_p(hin.data_ptr()), r, steps, 8, 12,
+                                    ctypes.c_void_p(hout.data_ptr()), None)
+        assert rc == 0, _abi.load().nbb_gpu_last_error()
+        assert np.array_equal(hout.numpy(), want), trial
