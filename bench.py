@@ -473,7 +473,7 @@ def main():
             for label, be in (("scalar", nbb.LambdaBackend.Direct),
                               ("tensor_core_tcgen05", nbb.LambdaBackend.MmaV2),
                               ("tensor_core_mma_sync", nbb.LambdaBackend.MmaV1)):
-                if be != nbb.LambdaBackend.Direct and lvl > 16:
+                if be == nbb.LambdaBackend.MmaV1 and lvl > 16:  # the paper's V1: r_b <= 16
                     continue
                 c = cfg(backend=be)
                 ms = timed(lambda: dev.lambda_coords_dev(c, lvl, xy.data_ptr(), 4, s), max(5, K // 4), W)

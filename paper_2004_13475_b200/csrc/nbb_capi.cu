@@ -987,7 +987,7 @@ int nbb_gpu_lambda_coords_dev(const nbb_config* cfg, int32_t level, void* d_xy, 
     if (coord_bytes != 4 && coord_bytes != 8)
         return fail(NBB_ERR_INVALID_ARGUMENT, "coord_bytes must be 4 or 8");
     const bool tc = cfg->backend == NBB_BACKEND_MMA1 || cfg->backend == NBB_BACKEND_MMA2;
-    if (tc && level > 16)
+    if (cfg->backend == NBB_BACKEND_MMA1 && level > 16)  // the paper's 16 x 16 fragment
         return fail(NBB_ERR_INVALID_ARGUMENT, "variant 1 encodes at most 16 levels, r_b = " +
                                                   std::to_string(level));
     DeviceCtx* ctx;

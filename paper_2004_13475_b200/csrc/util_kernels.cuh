@@ -383,19 +383,19 @@ __global__ void lambda_map_tc_kernel(Coord* xy, uint64_t total, uint32_t gw, Fas
 }
 
 // ---- K0-TC on the 5th-generation tensor core (tcgen05 + TMEM) ----------------------
-// The paper's MMA λ (mma.cpp:34-118, variant 1) as one tcgen05.mma per 128 ordinals and 16
-// levels: D[128 ω x 16] (fp32, TMEM) = A[128 x 32] (bf16, smem) · B[32 x 16] (bf16, smem) with
-// A[i][k] = τx(β_{k+1}(ω_i)) for k < 16 and τy(β_{k-15}(ω_i)) for k >= 16, B[k][0] = 2^k (k < 16),
-// B[k][1] = 2^(k-16) (k >= 16), other columns 0, so D[i][0..1] = λ(ω_i). τx(β) = [β == 2] and
+// The paper's MMA λ (mma.cpp:34-118, variant 1) as three tcgen05.mma per 128 ordinals and up to
+// 24 levels: D[128 ω x 16] (fp32, TMEM) = A[128 x 48] (bf16, smem) · B[48 x 16] (bf16, smem) with
+// A[i][k] = τx(β_{k+1}(ω_i)) for k < 24 and τy(β_{k-23}(ω_i)) for k >= 24, B[k][0] = 2^k (k < 24),
+// B[k][1] = 2^(k-24) (k >= 24), other columns 0, so D[i][0..1] = λ(ω_i). τx(β) = [β == 2] and
 // τy(β) = [β >= 1] of the level's base-3 digit are bit μ-1 of X(ωx) | X(ωy) << 1 and
 // Y(ωx) | Y(ωy) << 1, read from the 729-entry digit table. Exact: 0/1 and
-// powers of two <= 2^15 are exact in bf16, sums < 2^16 in fp32.
+// powers of two <= 2^23 are exact in bf16, sums < 2^24 in fp32 (the map covers levels <= 17).
 //
 // One CTA = 4 warps = 128 ordinals per tile (thread i builds A row i), persistent over tiles:
-// build A -> fence.proxy.async -> one elected thread issues 2 x tcgen05.mma (M=128, N=16,
+// build A -> fence.proxy.async -> one elected thread issues 3 x tcgen05.mma (M=128, N=16,
 // K=16) and commits to an mbarrier -> every warp tcgen05.ld's its 32 TMEM lanes (2 columns)
 // -> 8-byte stores. Operands in the canonical no-swizzle K-major layout: 8-row x 16-byte core
-// matrices, K-adjacent core matrices 128 B apart (LBO), 8-row groups 512 B apart (SBO).
+// matrices, K-adjacent core matrices 128 B apart (LBO), 8-row groups 768 B apart (SBO).
 __device__ __forceinline__ uint64_t umma_smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
@@ -413,20 +413,22 @@ __global__ void __launch_bounds__(128) lambda_map_tc5_kernel(Coord* xy, uint64_t
                              | (1u << 10)     // B format bf16
                              | (2u << 17)     // N = 16 (>> 3)
                              | (8u << 24);    // M = 128 (>> 4); A, B K-major
-    __shared__ __align__(128) uint8_t s_a[128 * 64];  // [16 row groups][4 k chunks][8 rows][16 B]
-    __shared__ __align__(128) uint8_t s_b[16 * 64];   // [2 col groups][4 k chunks][8 cols][16 B]
+    constexpr uint32_t KC = 6;                // 16-byte k chunks per row (K = 48)
+    constexpr uint32_t SBO = KC * 128;        // bytes between 8-row groups
+    __shared__ __align__(128) uint8_t s_a[128 * KC * 16];  // [16 row groups][KC][8 rows][16 B]
+    __shared__ __align__(128) uint8_t s_b[16 * KC * 16];   // [2 col groups][KC][8 cols][16 B]
     __shared__ uint32_t s_tab[729];
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint32_t s_tmem;
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     for (uint32_t i = tid; i < 729; i += 128) s_tab[i] = c_xy729[i];
     // B: column n (= "row" of the K-major B), k chunk c holds k = 8c..8c+7
-    for (uint32_t e = tid; e < 16 * 32; e += 128) {
-        const uint32_t n = e >> 5, k = e & 31;
+    for (uint32_t e = tid; e < 16 * 48; e += 128) {
+        const uint32_t n = e / 48, k = e % 48;
         float v = 0.f;
-        if (n == 0 && k < 16) v = (float)(1u << k);
-        if (n == 1 && k >= 16) v = (float)(1u << (k - 16));
-        const uint32_t off = (n >> 3) * 512 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
+        if (n == 0 && k < 24) v = (float)(1u << k);
+        if (n == 1 && k >= 24) v = (float)(1u << (k - 24));
+        const uint32_t off = (n >> 3) * SBO + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
         *reinterpret_cast<__nv_bfloat16*>(s_b + off) = __float2bfloat16_rn(v);
     }
     if (warp == 0) {
@@ -447,7 +449,7 @@ __global__ void __launch_bounds__(128) lambda_map_tc5_kernel(Coord* xy, uint64_t
     const uint32_t a_base = (uint32_t)__cvta_generic_to_shared(s_a);
     const uint32_t b_base = (uint32_t)__cvta_generic_to_shared(s_b);
     // this thread's A row: row group tid >> 3, row tid & 7
-    uint8_t* my_row = s_a + (tid >> 3) * 512 + (tid & 7) * 16;
+    uint8_t* my_row = s_a + (tid >> 3) * SBO + (tid & 7) * 16;
     uint32_t phase = 0;
     const uint64_t tiles = (total + 127) / 128;
     for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -460,10 +462,10 @@ __global__ void __launch_bounds__(128) lambda_map_tc5_kernel(Coord* xy, uint64_t
             xy_from_table(s_tab, oy, Xy, Yy);
             lambda_from_xy(Xx, Yx, Xy, Yy, lx, ly);  // bit μ-1: τx / τy of level μ
         }
-        // A row: k < 16 -> τx bits, k >= 16 -> τy bits, as bf16 1.0 (0x3F80) or 0
+        // A row: chunks 0-2 -> τx bits 0-23, chunks 3-5 -> τy bits 0-23, as bf16 1.0 (0x3F80) or 0
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const uint32_t bits = (c < 2 ? lx : ly) >> (8 * (c & 1));
+        for (int c = 0; c < (int)KC; ++c) {
+            const uint32_t bits = (c < 3 ? lx : ly) >> (8 * (c % 3));
             uint32_t w[4];
 #pragma unroll
             for (int h = 0; h < 4; ++h)
@@ -476,9 +478,9 @@ __global__ void __launch_bounds__(128) lambda_map_tc5_kernel(Coord* xy, uint64_t
         if (tid == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-                const uint64_t da = umma_smem_desc(a_base + ks * 256, 128, 512);
-                const uint64_t db = umma_smem_desc(b_base + ks * 256, 128, 512);
+            for (int ks = 0; ks < (int)KC / 2; ++ks) {
+                const uint64_t da = umma_smem_desc(a_base + ks * 256, 128, SBO);
+                const uint64_t db = umma_smem_desc(b_base + ks * 256, 128, SBO);
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),

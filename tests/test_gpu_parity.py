@@ -252,9 +252,9 @@ def test_lambda_map_full_levels(level):
     xy = torch.empty((3 ** level, 2), dtype=torch.int32, device="cuda")
     dev.lambda_coords_dev(cfg(), level, xy.data_ptr(), 4, s)
     assert np.array_equal(xy.cpu().numpy().astype(np.int64), want)
-    if level <= 16:  # the tcgen05 K0-TC at full size too (int32 pairs)
-        dev.lambda_coords_dev(cfg(backend=LambdaBackend.MmaV2), level, xy.data_ptr(), 4, s)
-        assert np.array_equal(xy.cpu().numpy().astype(np.int64), want)
+    # the tcgen05 K0-TC at full size too (int32 pairs, levels <= 17)
+    dev.lambda_coords_dev(cfg(backend=LambdaBackend.MmaV2), level, xy.data_ptr(), 4, s)
+    assert np.array_equal(xy.cpu().numpy().astype(np.int64), want)
     del xy
     assert np.array_equal(nbb.lambda_coords(cfg(), level), want)
 
