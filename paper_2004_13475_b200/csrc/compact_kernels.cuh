@@ -332,10 +332,15 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
     uint8_t* cell = s_cell[wib];
     pdl_trigger();
     s_pos[threadIdx.x] = threadIdx.x < 243 ? c_local_pos[threadIdx.x] : 0;
-    if (P2P) {
+    if (P2P && p.wait_target != 0u) {
+        // the arrival wait subsumes pdl_wait: this rank's own arrival for the previous step is
+        // in it (its last CTA's stores released before it), so no grid-completion wait
         if (threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
-        if (threadIdx.x == 0) p2p_wait(p);  // subsumes pdl_wait: this rank's own arrival is in it
+        if (threadIdx.x == 0) p2p_wait(p);
     } else {
+        // plain steps, and the first P2P step of a sequence (its predecessor on the stream is
+        // whatever produced the state, not a P2P step)
+        if (P2P && threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
         pdl_wait();
     }
     __syncthreads();
