@@ -199,7 +199,12 @@ def main():
     args.warmup = max(args.warmup, 3)
 
     if args.impl == "reference":
-        run_reference_arm(args)
+        try:
+            run_reference_arm(args)
+        except Exception as e:  # e.g. oracle/_ref not built on this box: say so, don't crash
+            if int(os.environ.get("RANK", "0")) == 0:
+                print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}),
+                      flush=True)
         return
 
     import torch
