@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -202,6 +203,27 @@ struct Timer {
     }
 };
 
+// ---- occupancy (resident CTAs per SM), cached per kernel and device -------------------
+// Kern is the kernel itself (a non-type template parameter, so every kernel instantiation has
+// its own cache even when two share a signature); dynamic_smem > 0 also raises the kernel's
+// dynamic shared-memory limit on the device (an attribute that is per device).
+template <auto Kern>
+int occupancy(int threads, int dynamic_smem, int* out) {
+    static std::atomic<int> cache[64];  // by device ordinal; 0 = not yet queried
+    int dev = 0;
+    NBB_CUDA(cudaGetDevice(&dev));
+    int v = cache[dev & 63].load(std::memory_order_relaxed);
+    if (v == 0) {
+        if (dynamic_smem > 0)
+            NBB_CUDA(cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dynamic_smem));
+        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, Kern, threads, dynamic_smem));
+        if (v < 1) return fail(NBB_ERR_RESOURCE, "kernel does not fit on an SM");
+        cache[dev & 63].store(v, std::memory_order_relaxed);
+    }
+    *out = v;
+    return NBB_OK;
+}
+
 // ---- launch helpers -----------------------------------------------------------------
 struct Launch {
     const nbb_config* cfg;
@@ -227,11 +249,8 @@ bool tile_supported(const nbb_config& c, int op, int cell_width) {
 template <bool BB, int ILP>
 int run_ca_bits_ilp(const Launch& L, const TileArgs& a) {
     auto kern = ca_bits_kernel<BB, ILP>;
-    static int occ = 0;
-    if (occ == 0) {
-        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0));
-        if (occ < 1) occ = 1;
-    }
+    int occ;
+    NBB_CHECK(occupancy<ca_bits_kernel<BB, ILP>>(256, 0, &occ));
     const uint64_t units = (a.tiles + ILP - 1) / ILP;
     const uint64_t want = (units + 7) / 8;
     const uint64_t cap = (uint64_t)L.ctx->sms * (uint64_t)occ;
@@ -280,12 +299,8 @@ template <typename Cell, int RHO, bool BB, int STAGES, int WARPS>
 int run_ca_pipe(const Launch& L, const TileArgs& a) {
     using P = CaPipeShape<Cell, RHO, BB, STAGES, WARPS>;
     auto kern = ca_pipe_kernel<Cell, RHO, BB, STAGES, WARPS>;
-    static int occ = 0;
-    if (occ == 0) {
-        NBB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM));
-        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, P::SMEM));
-        if (occ < 1) return fail(NBB_ERR_RESOURCE, "ca pipeline kernel does not fit on an SM");
-    }
+    int occ;
+    NBB_CHECK((occupancy<ca_pipe_kernel<Cell, RHO, BB, STAGES, WARPS>>(WARPS * 32, P::SMEM, &occ)));
     constexpr int TPW = 32 / RHO;
     const uint64_t units = (a.tiles + TPW - 1) / TPW;
     const uint64_t want = (units + WARPS - 1) / WARPS;
@@ -331,11 +346,8 @@ int run_tile_rule(const Launch& L, const void* src, void* dst, unsigned long lon
         }
     }
     auto kern = tile_kernel<Cell, RHO, OP, BB>;
-    static int occ = 0;
-    if (occ == 0) {
-        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0));
-        if (occ < 1) occ = 1;
-    }
+    int occ;
+    NBB_CHECK((occupancy<tile_kernel<Cell, RHO, OP, BB>>(256, 0, &occ)));
     TileArgs a;
     a.src = src;
     a.dst = dst;
@@ -758,11 +770,8 @@ int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, vo
     const CompactCaArgs a = compact_args(cfg, src, dst, birth, survive, &div_hb);
     const int32_t* tab;
     NBB_CHECK(compact_halo_table(ctx, cfg, a, div_hb, &tab));
-    static int occ = 0;
-    if (occ == 0) {
-        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ca_compact_kernel<false>, 256, 0));
-        if (occ < 1) occ = 1;
-    }
+    int occ;
+    NBB_CHECK(occupancy<ca_compact_kernel<false>>(256, 0, &occ));
     const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
     if (want == 0) return NBB_OK;
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
@@ -1425,11 +1434,8 @@ int nbb_gpu_ca_compact_p2p_dev(const nbb_config* cfg, int64_t first_step, int32_
     p.timeout_ms = p2p->timeout_ms ? p2p->timeout_ms : 20000u;
     p.world = p2p->world;
     p.rank = p2p->rank;
-    static int occ = 0;
-    if (occ == 0) {
-        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ca_compact_kernel<true>, 256, 0));
-        if (occ < 1) occ = 1;
-    }
+    int occ;
+    NBB_CHECK(occupancy<ca_compact_kernel<true>>(256, 0, &occ));
     // every rank launches (and arrives) even with an empty shard: one CTA at least; at most one
     // resident wave, so CTAs spinning in the wait never keep a CTA of the same step off an SM
     const uint64_t want = std::max<uint64_t>(1, (a.tile_end - a.tile_begin + 7) / 8);
