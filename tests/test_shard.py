@@ -179,3 +179,29 @@ def test_compact_segments_partition_the_state(r):
             assert np.array_equal(np.sort(mine), np.sort(want)), (world, k)
             cover[mine] += 1
         assert np.all(cover == 1), world
+
+
+def test_more_ranks_than_tiles_and_owner_table():
+    """Empty shards (world > tiles) launch nothing and own nothing; the P2P owner table names,
+    for every member halo cell of every tile, the rank whose tile range holds that cell."""
+    for r, world in ((5, 3), (6, 5)):
+        plans = [ShardPlan(r=r, rho=32, world=world, rank=k, state="compact") for k in range(world)]
+        assert sum(p.count for p in plans) == 3 ** (r - 5)
+        for p in plans:
+            if p.count == 0:
+                assert p.compact_segments() == []
+    r, world = 10, 3
+    plan = ShardPlan(r=r, rho=32, world=world, rank=1, state="compact")
+    own = plan.halo_owner_table().reshape(-1, 8)
+    n = 1 << r
+    t = np.arange(plan.total, dtype=np.int64)
+    bx, by = lambda_blocks(plan.ordinal_of_tile(t), plan.W)
+    offs = np.array([(-1, -1), (0, -1), (1, -1), (-1, 31), (32, 30), (32, 31), (32, 32), (0, 32)])
+    for k, (dx, dy) in enumerate(offs):
+        cx, cy = bx * 32 + dx, by * 32 + dy
+        ok = (cx >= 0) & (cy >= 0) & (cx < n) & (cy < n)
+        ok &= (np.where(ok, cx, 0) & (n - 1 - np.where(ok, cy, 0))) == 0
+        where = {(int(x), int(y)): int(u) for u, x, y in zip(t, bx, by)}  # tile at each λ block
+        tile = np.array([where[(int(x) // 32, int(y) // 32)] for x, y in zip(cx[ok], cy[ok])], dtype=np.int64)
+        assert np.array_equal(own[ok, k], plan.owner(tile)), k
+        assert np.all(own[~ok, k] == 0)
