@@ -568,4 +568,56 @@ __global__ void __launch_bounds__(256) compact_to_sectors_kernel(const long long
     }
 }
 
+// ---- embedded Grid <-> compact state in embedded ROW order (the host boundary) ----------------
+// Warp per embedded row y: its member sectors s ⊆ (y >> 2) in increasing address order, member
+// cells i ⊆ (y & 3) inside each. Used for the pinned host Grid of nbb_gpu_ca: walking the Grid
+// row by row keeps consecutive zero-copy accesses on the same host pages, which the tile walk
+// does not (a tile spans 32 rows 512 KB apart) — tools/probe_zero_copy.cu: member-sector reads
+// 19.5 ms row-major vs 29 ms in tile order, writes 20.7 vs 27.4 ms, at n = 2^16. The compact
+// side takes scattered 8-byte accesses in HBM (λ⁻¹ of each cell, gasket_compact_offset).
+__global__ void __launch_bounds__(256) compact_from_rows_kernel(const long long* emb, long long* comp, int64_t n,
+                                                                uint32_t W) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t y = warp; y < (uint32_t)n; y += nwarps) {
+        const uint32_t m = y >> 2, cnt = 1u << __popc(m);
+        const uint32_t nib = submask_bits(y & 3u) & 0xFu;
+#pragma unroll 4
+        for (uint32_t j = (uint32_t)lane; j < cnt; j += 32u) {
+            const uint32_t sx = pdep32(j, m);
+            const Sector v = ld_sector(emb + (int64_t)y * n + 4 * (int64_t)sx);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if ((nib >> c) & 1u)
+                    comp[gasket_compact_offset(4u * sx + c, y, W)] =
+                        (long long)(((unsigned long long)v.w[2 * c + 1] << 32) | v.w[2 * c]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) compact_to_rows_kernel(const long long* comp, long long* emb, int64_t n,
+                                                              uint32_t W) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t y = warp; y < (uint32_t)n; y += nwarps) {
+        const uint32_t m = y >> 2, cnt = 1u << __popc(m);
+        const uint32_t nib = submask_bits(y & 3u) & 0xFu;
+#pragma unroll 4
+        for (uint32_t j = (uint32_t)lane; j < cnt; j += 32u) {
+            const uint32_t sx = pdep32(j, m);
+            Sector v;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const unsigned long long q =
+                    ((nib >> c) & 1u) ? (unsigned long long)__ldg(comp + gasket_compact_offset(4u * sx + c, y, W)) : 0ull;
+                v.w[2 * c] = (uint32_t)q;
+                v.w[2 * c + 1] = (uint32_t)(q >> 32);
+            }
+            stg_sector(emb + (int64_t)y * n + 4 * (int64_t)sx, v);
+        }
+    }
+}
+
 }  // namespace nbbgpu

@@ -1124,7 +1124,10 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
             NBB_CUDA(cudaMemcpyAsync(stage, initial, b64, cudaMemcpyHostToDevice, L.stream));
             src = stage;
         }
-        NBB_CHECK(compact_from_sectors(L.ctx, cfg, src, ca, L.stream));
+        // member sectors -> compact in embedded row order (host pages stay sequential)
+        compact_from_rows_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)src, (long long*)ca,
+                                                                        (int64_t)cs.n, (uint32_t)cs.W);
+        NBB_CUDA(cudaGetLastError());
         for (int s = 0; s < steps; ++s) {
             Timer t(cfg->timing != 0, L.stream);
             NBB_CHECK(launch_ca_compact(L.ctx, cfg, ca, cb, birth, survive, L.stream));
@@ -1132,8 +1135,10 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
             if (per_step) fill_report(cfg, &per_step[s], us);
             std::swap(ca, cb);
         }
-        if (h_out) {  // member sectors straight into the zeroed pinned output
-            NBB_CHECK(compact_to_sectors(L.ctx, cfg, ca, h_out, L.stream));
+        if (h_out) {  // member sectors straight into the zeroed pinned output, row by row
+            compact_to_rows_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)ca, h_out,
+                                                                          (int64_t)cs.n, (uint32_t)cs.W);
+            NBB_CUDA(cudaGetLastError());
         } else {
             if (!stage) NBB_CHECK(device_buffer(*L.ctx, 0, b64, &stage));
             NBB_CUDA(cudaMemsetAsync(stage, 0, b64, L.stream));
