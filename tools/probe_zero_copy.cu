@@ -10,8 +10,12 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o probe_zero_copy probe_zero_copy.cu
 #include <cuda_runtime.h>
 
+#include <sys/mman.h>
+
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 __constant__ uint32_t c_slot[128];  // per granularity: (row y, unit index) packed y | u << 5
@@ -120,7 +124,17 @@ int main() {
     const uint32_t tiles = 729u * 243u;
     const size_t bytes = (size_t)n * n * 8;
     long long *h, *d;
-    if (cudaHostAlloc((void**)&h, bytes, cudaHostAllocMapped) != cudaSuccess) return 1;
+    const bool huge = getenv("PROBE_HUGE") != nullptr;  // THP-backed mmap + cudaHostRegister
+    if (huge) {
+        void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (p == MAP_FAILED) return 1;
+        madvise(p, bytes, MADV_HUGEPAGE);
+        std::memset(p, 0, bytes);
+        if (cudaHostRegister(p, bytes, cudaHostRegisterMapped) != cudaSuccess) return 2;
+        h = (long long*)p;
+    } else if (cudaHostAlloc((void**)&h, bytes, cudaHostAllocMapped) != cudaSuccess) {
+        return 1;
+    }
     for (size_t i = 0; i < bytes / 8; i += 512) h[i] = (long long)i;
     cudaHostGetDevicePointer((void**)&d, h, 0);
     unsigned long long* sink;
@@ -128,7 +142,7 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    printf("{");
+    printf("{\"host_alloc\": \"%s\", ", huge ? "mmap+MADV_HUGEPAGE+cudaHostRegister" : "cudaHostAlloc");
     const char* names[3] = {"sector", "chunk", "line"};
     for (int g = 0; g < 3; ++g) {
         const int unit = 32 << g, per_row = 256 / unit;  // units per 256-byte tile row
