@@ -32,7 +32,7 @@ def call(steps):
 
 
 call(1)
-res = {"mode": "sectors" if os.environ.get("NBB_E2E_SECTORS") else "lines",
+res = {
        "one_step_s": min(call(1) for _ in range(5)), "k200_s": min(call(200) for _ in range(3))}
 res["cells_per_s_k200"] = 3 ** r * 200 / res["k200_s"]
 print(json.dumps(res))
