@@ -195,3 +195,58 @@ def test_sharded_reduction_and_single_write(world, r):
     assert np.array_equal(got["embedded_sw"], sw)
     cx, cy = lambda_blocks(np.arange(3 ** r, dtype=np.int64), 3 ** ((r + 1) // 2))
     assert np.array_equal(got["compact_sw"], sw[cy, cx])
+
+
+def _p2p_full_worker(rank, world, port, r, steps, q):
+    """C5 at full size: ranks share one B200; the compact state is generated on the device
+    (seeded), non-owned cells poisoned; returns this rank's tiles' result digest parts."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2004_13475_b200 import nbb
+    from paper_2004_13475_b200.shard import P2PCompactCA, ShardPlan
+    plan = ShardPlan(r=r, rho=32, world=world, rank=rank, state="compact")
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1700 + r)
+    init = torch.randint(0, 2, (3 ** r,), dtype=torch.int64, device="cuda", generator=gen)
+    own = torch.zeros(3 ** r, dtype=torch.bool, device="cuda")
+    for o, c in plan.compact_segments():
+        own[o:o + c] = True
+    init[~own] = 7
+    ca = P2PCompactCA(plan, dist, device=0, timeout_ms=120000)
+    ca.load(init)
+    ca.run(nbb.DispatchConfig(r=r, rho=32, max_cells=(1 << r) ** 2), nbb.CaRule(), steps,
+           torch.cuda.current_stream().cuda_stream)
+    ca.check(torch.cuda.current_stream().cuda_stream)
+    out = torch.where(own, ca.state(), torch.zeros_like(ca.state())).cpu()
+    ca.close()
+    dist.all_reduce(out)
+    if rank == 0:
+        q.put(out.numpy())
+    dist.destroy_process_group()
+
+
+def test_p2p_compact_ca_full_size_r17():
+    """C5 (n = 2^17) through the multi-rank P2P step loop (2 ranks time-sharing one B200, their
+    non-owned cells poisoned) equals the single-GPU compact step loop bit for bit."""
+    from paper_2004_13475_b200 import device as dev
+    from paper_2004_13475_b200 import nbb
+    r, steps, world = 17, 3, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_full_worker, args=(i, world, port, r, steps, q)) for i in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=900)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1700 + r)
+    a = torch.randint(0, 2, (3 ** r,), dtype=torch.int64, device="cuda", generator=gen)
+    b = torch.empty_like(a)
+    dev.ca_compact_run_dev(nbb.DispatchConfig(r=r, rho=32, max_cells=(1 << r) ** 2), a.data_ptr(),
+                           b.data_ptr(), steps, nbb.CaRule(), torch.cuda.current_stream().cuda_stream)
+    want = (b if steps % 2 else a).cpu().numpy()
+    assert np.array_equal(got, want)
