@@ -458,7 +458,13 @@ def main():
         for name, c in {"sw_lambda_tile_rho32": cfg(), "sw_bb_tile_rho32": cfg(mode=nbb.MapMode.BoundingBox),
                         "sw_bb_percell_rho32": cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell),
                         "sw_lambda_percell_rho32": cfg(kernel=nbb.KernelFamily.PerCell),
-                        "sw_lambda_percell_rho16": cfg(rho=16, kernel=nbb.KernelFamily.PerCell)}.items():
+                        "sw_lambda_percell_rho16": cfg(rho=16, kernel=nbb.KernelFamily.PerCell),
+                        # the paper's tensor-core λ (mma.cpp variants 1 and 2)
+                        # in the per-cell launch, against its direct backend above
+                        "sw_lambda_percell_rho16_mma1": cfg(rho=16, kernel=nbb.KernelFamily.PerCell,
+                                                            backend=nbb.LambdaBackend.MmaV1),
+                        "sw_lambda_percell_rho16_mma2": cfg(rho=16, kernel=nbb.KernelFamily.PerCell,
+                                                            backend=nbb.LambdaBackend.MmaV2)}.items():
             results[name] = timed(sw(c), K if "tile" in name else max(5, K // 10), W)
         for name, c in {"rd_lambda_tile_rho32": cfg(), "rd_bb_tile_rho32": cfg(mode=nbb.MapMode.BoundingBox),
                         "rd_bb_percell_rho32": cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell),
@@ -621,6 +627,9 @@ def main():
             "rd_bb_tile_over_lambda_compact": ratio("rd_bb_tile_rho32", "rd_lambda_compact_i64"),
             # the paper's own comparison (one thread per cell, ρ = 32 blocks; PAPER.md:548-549
             # reports 6x-12x at n = 2^16 on Titan V / Titan RTX)
+            "paper_tc_percell_rho16_sw": {  # V2 ~20-40% faster than scalar
+                "mma1_over_direct": ratio("sw_lambda_percell_rho16", "sw_lambda_percell_rho16_mma1"),
+                "mma2_over_direct": ratio("sw_lambda_percell_rho16", "sw_lambda_percell_rho16_mma2")},
             "paper_percell_rho32": {
                 "sw": ratio("sw_bb_percell_rho32", "sw_lambda_percell_rho32"),
                 "rd": ratio("rd_bb_percell_rho32", "rd_lambda_percell_rho32"),

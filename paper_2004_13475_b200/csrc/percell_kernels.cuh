@@ -139,14 +139,22 @@ __global__ void percell_kernel(PercellArgs a) {
         }
         int64_t ox = 0, oy = 0;
         if (BACKEND == NBB_BACKEND_DIRECT) {
-            if (!GEN) {
-                uint32_t lx, ly;
-                lambda_arith((uint32_t)gx, (uint32_t)gy, lx, ly);
-                ox = lx;
-                oy = ly;
-            } else {
-                lambda_spec(a.spec, gx, gy, a.map_level, ox, oy);
+            // λ(ω) once per block, as launch_impl resolves the origin once per ordinal
+            // (dispatch.cpp:307-311), broadcast through shared memory: per-thread evaluation
+            // made this path issue-bound (1.44 -> 0.70 ms for SW at n = 2^16, ρ = 16)
+            if (tid == 0) {
+                if (!GEN) {
+                    uint32_t lx, ly;
+                    lambda_arith((uint32_t)gx, (uint32_t)gy, lx, ly);
+                    s_origin[0] = lx;
+                    s_origin[1] = ly;
+                } else {
+                    lambda_spec(a.spec, gx, gy, a.map_level, s_origin[0], s_origin[1]);
+                }
             }
+            __syncthreads();
+            ox = s_origin[0];
+            oy = s_origin[1];
         } else if (BACKEND == NBB_BACKEND_MMA1 && GEN) {
             // s = 3: powers 3^(μ-1) are not bf16-exact beyond 3^5 — variant 1 on the FP64
             // tensor pipe (DMMA m8n8k4): A row 0 = s^(μ-1), B cols 0/1 = τx/τy; K = 16 in 4 steps
