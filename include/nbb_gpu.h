@@ -85,7 +85,10 @@ typedef struct nbb_config {
     int32_t mode;       /* NBB_MODE_*                                          */
     int32_t strategy;   /* NBB_STRATEGY_*                                      */
     int32_t backend;    /* NBB_BACKEND_*                                       */
-    int32_t workers;    /* reference: host threads; here: devices (>= 1)        */
+    int32_t workers;    /* reference: host threads (>= 1); here the ordinal range is
+                         * split into that many contiguous chunks (dispatch.cpp:419-427),
+                         * launched in order on `device` — results identical for any
+                         * count; across GPUs: one process per GPU with shard_* below */
     int32_t timing;     /* nonzero: fill report.micros from CUDA events         */
     int32_t cell_width; /* device cell bytes: 8 (int64, drop-in) or 1 (uint8)   */
     int32_t kernel;     /* NBB_KERNEL_*                                        */
