@@ -415,13 +415,22 @@ __global__ void __launch_bounds__(128) lambda_map_tc5_kernel(Coord* xy, uint64_t
                              | (8u << 24);    // M = 128 (>> 4); A, B K-major
     constexpr uint32_t KC = 6;                // 16-byte k chunks per row (K = 48)
     constexpr uint32_t SBO = KC * 128;        // bytes between 8-row groups
-    __shared__ __align__(128) uint8_t s_a[128 * KC * 16];  // [16 row groups][KC][8 rows][16 B]
-    __shared__ __align__(128) uint8_t s_b[16 * KC * 16];   // [2 col groups][KC][8 cols][16 B]
+    constexpr uint32_t A_BYTES = 128 * KC * 16;
+    __shared__ __align__(128) uint8_t s_a[2][A_BYTES];  // two stages of [16 row groups][KC][8 rows][16 B]
+    __shared__ __align__(128) uint8_t s_b[16 * KC * 16];  // [2 col groups][KC][8 cols][16 B]
     __shared__ uint32_t s_tab[729];
-    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ uint4 s_bits[256];  // byte b -> its 8 bits as 8 bf16 values (1.0 or 0), K-chunk ready
+    __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ uint32_t s_tmem;
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     for (uint32_t i = tid; i < 729; i += 128) s_tab[i] = c_xy729[i];
+    for (uint32_t bb = tid; bb < 256; bb += 128) {
+        uint32_t w[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+            w[h] = (((bb >> (2 * h)) & 1u) ? 0x3F80u : 0u) | (((bb >> (2 * h + 1)) & 1u) ? 0x3F800000u : 0u);
+        s_bits[bb] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
     // B: column n (= "row" of the K-major B), k chunk c holds k = 8c..8c+7
     for (uint32_t e = tid; e < 16 * 48; e += 128) {
         const uint32_t n = e / 48, k = e % 48;
@@ -431,14 +440,15 @@ __global__ void __launch_bounds__(128) lambda_map_tc5_kernel(Coord* xy, uint64_t
         const uint32_t off = (n >> 3) * SBO + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
         *reinterpret_cast<__nv_bfloat16*>(s_b + off) = __float2bfloat16_rn(v);
     }
-    if (warp == 0) {
+    if (warp == 0) {  // two 16-column accumulators (stages) in one 32-column allocation
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_tmem);
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(dst));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&s_bar[0]);
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -446,13 +456,37 @@ __global__ void __launch_bounds__(128) lambda_map_tc5_kernel(Coord* xy, uint64_t
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = s_tmem;
-    const uint32_t a_base = (uint32_t)__cvta_generic_to_shared(s_a);
+    const uint32_t a_base0 = (uint32_t)__cvta_generic_to_shared(s_a[0]);
     const uint32_t b_base = (uint32_t)__cvta_generic_to_shared(s_b);
-    // this thread's A row: row group tid >> 3, row tid & 7
-    uint8_t* my_row = s_a + (tid >> 3) * SBO + (tid & 7) * 16;
-    uint32_t phase = 0;
+    const uint32_t row_off = (tid >> 3) * SBO + (tid & 7) * 16;  // this thread's A row
+    uint32_t phase[2] = {0u, 0u};
+
+    // wait for tile (stage st)'s MMAs, read its accumulator lanes, store the λ pairs
+    auto drain = [&](uint32_t st, uint64_t o) {
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}\n"
+                : "=r"(done) : "r"(bar0 + 8u * st), "r"(phase[st]) : "memory");
+        phase[st] ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        uint32_t d0, d1;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                     : "=r"(d0), "=r"(d1) : "r"(tmem + ((warp * 32u) << 16) + 16u * st));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (o < total) {
+            xy[2 * o] = (Coord)__float2uint_rn(__uint_as_float(d0));
+            xy[2 * o + 1] = (Coord)__float2uint_rn(__uint_as_float(d1));
+        }
+    };
+
+    // two-stage pipeline: build tile i's A while the tensor core runs tile i-1, then drain i-1
     const uint64_t tiles = (total + 127) / 128;
-    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    uint64_t o_prev = 0;
+    uint32_t i = 0;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const uint32_t st = i & 1u;
         const uint64_t o = t * 128 + tid;
         uint32_t lx = 0, ly = 0;
         if (o < total) {
@@ -462,55 +496,38 @@ __global__ void __launch_bounds__(128) lambda_map_tc5_kernel(Coord* xy, uint64_t
             xy_from_table(s_tab, oy, Xy, Yy);
             lambda_from_xy(Xx, Yx, Xy, Yy, lx, ly);  // bit μ-1: τx / τy of level μ
         }
-        // A row: chunks 0-2 -> τx bits 0-23, chunks 3-5 -> τy bits 0-23, as bf16 1.0 (0x3F80) or 0
+        // A row (stage st; its previous MMA, tile i-2, was drained last iteration): chunks 0-2 ->
+        // τx bits 0-23, chunks 3-5 -> τy bits 0-23, one byte of λ per chunk via s_bits
+        uint8_t* my_row = s_a[st] + row_off;
 #pragma unroll
         for (int c = 0; c < (int)KC; ++c) {
-            const uint32_t bits = (c < 3 ? lx : ly) >> (8 * (c % 3));
-            uint32_t w[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h)
-                w[h] = (((bits >> (2 * h)) & 1u) ? 0x3F80u : 0u) | (((bits >> (2 * h + 1)) & 1u) ? 0x3F800000u : 0u);
-            *reinterpret_cast<uint4*>(my_row + c * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+            const uint32_t byte = ((c < 3 ? lx : ly) >> (8 * (c % 3))) & 0xFFu;
+            *reinterpret_cast<uint4*>(my_row + c * 128) = s_bits[byte];
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();
+        __syncthreads();  // A[st] complete; every thread has drained tile i-2's accumulator
         if (tid == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
             for (int ks = 0; ks < (int)KC / 2; ++ks) {
-                const uint64_t da = umma_smem_desc(a_base + ks * 256, 128, SBO);
+                const uint64_t da = umma_smem_desc(a_base0 + st * A_BYTES + ks * 256, 128, SBO);
                 const uint64_t db = umma_smem_desc(b_base + ks * 256, 128, SBO);
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + 16u * st),
                     "l"(da), "l"(db), "r"(IDESC), "r"(ks));
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                         : "memory");
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                         ::"r"(bar0 + 8u * st) : "memory");
         }
-        // wait for the MMAs (they also finished reading s_a)
-        {
-            uint32_t done = 0;
-            while (!done)
-                asm volatile(
-                    "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                    "selp.u32 %0, 1, 0, p;\n\t}\n"
-                    : "=r"(done) : "r"(bar), "r"(phase) : "memory");
-            phase ^= 1u;
-        }
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        uint32_t d0, d1;
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
-                     : "=r"(d0), "=r"(d1) : "r"(tmem + ((warp * 32u) << 16)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (o < total) {
-            xy[2 * o] = (Coord)__float2uint_rn(__uint_as_float(d0));
-            xy[2 * o + 1] = (Coord)__float2uint_rn(__uint_as_float(d1));
-        }
+        if (i > 0) drain(st ^ 1u, o_prev);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();  // TMEM and s_a are rewritten by the next tile
+        o_prev = o;
     }
+    if (i > 0) drain((i - 1) & 1u, o_prev);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
 }
