@@ -410,6 +410,11 @@ def main():
               "r": r5, "cells_per_step": m5, "ms_per_step": ms5, "value": m5 * 1e3 / ms5,
               "unit": "cells/s", "per_gpu_GBps": ach5 / world,
               "per_gpu_roofline_frac": ach5 / world / measured_peaks()[0]}
+    # ---- the bounding-box launch over the SAME compact state (culled box tiles, λ⁻¹ addressing)
+    if world == 1:
+        results["ca_bb_compact_i64"] = timed_run(
+            lambda k: dev.ca_compact_run_dev(cfg(mode=nbb.MapMode.BoundingBox), c1.data_ptr(), c2.data_ptr(), k,
+                                             nbb.CaRule(), s), K, W)
     # ---- the same step on the reference's int64 embedded Grid layout --------------------
     emb_ms = timed(ca_runner(cfg(), a, b), K, W)
     results["ca_lambda_tile_rho32_i64"] = emb_ms
@@ -616,6 +621,7 @@ def main():
         "clocks": sampler.summary(),
         "speedup_vs_bb": {
             "ca_lambda_compact_over_bb_tile_i64": ratio("ca_bb_tile_rho32_i64", "ca_lambda_compact_i64"),
+            "ca_lambda_compact_over_bb_compact_i64": ratio("ca_bb_compact_i64", "ca_lambda_compact_i64"),
             "ca_lambda_compact_over_bb_percell_i64": ratio("ca_bb_percell_rho32_i64", "ca_lambda_compact_i64"),
             "ca_embedded_i64_bb_tile_over_lambda_tile": ratio("ca_bb_tile_rho32_i64", "ca_lambda_tile_rho32_i64"),
             "ca_embedded_i64_bb_percell_over_lambda_percell": ratio("ca_bb_percell_rho32_i64",

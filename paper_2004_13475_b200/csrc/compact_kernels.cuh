@@ -458,6 +458,174 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
 }
 
 
+// The BOUNDING-BOX launch of the compact-state CA step (the comparison for ca_compact_kernel on
+// the same storage): identical per-tile work, but the warps walk all (n/32)^2 box tiles, cull
+// the non-member ones and address each member tile through λ⁻¹ — the inverse map the compact
+// layout needs (block_map.cpp:113-148) — instead of enumerating the λ orthotope.
+__global__ void __launch_bounds__(256, 3) ca_compact_bb_kernel(CompactCaArgs a, FastDiv div_hb,
+                                                              const int32_t* __restrict__ halo_tab) {
+    constexpr bool P2P = false;
+    const P2PArgs p{};
+    __shared__ __align__(16) uint8_t s_cell[8][32 * 32];
+    __shared__ uint32_t s_new[8][32];
+    __shared__ uint16_t s_pos[256];  // c_local_pos (per-lane constant-bank reads serialise)
+    __shared__ const long long* s_peer[kMaxP2P];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint8_t* cell = s_cell[wib];
+    pdl_trigger();
+    s_pos[threadIdx.x] = threadIdx.x < 243 ? c_local_pos[threadIdx.x] : 0;
+    if (P2P && p.wait_target != 0u) {
+        // the arrival wait subsumes pdl_wait: this rank's own arrival for the previous step is
+        // in it (its last CTA's stores released before it), so no grid-completion wait
+        if (threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
+        if (threadIdx.x == 0) p2p_wait(p);
+    } else {
+        // plain steps, and the first P2P step of a sequence (its predecessor on the stream is
+        // whatever produced the state, not a P2P step)
+        if (P2P && threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
+        pdl_wait();
+    }
+    __syncthreads();
+    uint32_t sl_off[8], sl_pos[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t li = 32u * k + lane;
+        const bool ok = li < 243u;
+        const uint32_t row = ok ? li / 27u : 0u, col = ok ? li % 27u : 0u;
+        sl_off[k] = (row * a.W + col) * 8u;  // byte offset inside the tile's sub-block
+        sl_pos[k] = s_pos[li];               // x | y << 5 = byte index in the 32 x 32 tile
+    }
+    const bool k7 = lane < 19;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) reinterpret_cast<uint32_t*>(cell)[32 * i + lane] = 0u;
+    const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t warp_stride = (gridDim.x * blockDim.x) >> 5;
+    const char* src0 = reinterpret_cast<const char*>(a.src);
+    char* dst0 = reinterpret_cast<char*>(a.dst);
+    __syncwarp();
+
+    // Software-pipelined over the warp's tiles: tile u+stride's loads (its 243 values and
+    // halo cells) are issued as soon as tile u's values are in the byte tile — into the same
+    // registers — so they fly while tile u's rule and stores run; the halo-table entries run
+    // one more tile ahead (the halo load depends on them).
+    auto tile_base = [&](uint32_t t) -> uint64_t {
+        const uint32_t wxb = fastdiv(t, div_hb), wyb = t - wxb * a.Hb;
+        return ((uint64_t)(9u * wxb) * a.W + 27u * wyb) * 8u;
+    };
+    long long v[8];
+    auto load_tile = [&](uint64_t b) {
+        const char* src = src0 + b;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) v[k] = __ldg(reinterpret_cast<const long long*>(src + sl_off[k]));
+        v[7] = k7 ? __ldg(reinterpret_cast<const long long*>(src + sl_off[7])) : 0ll;
+    };
+    auto load_halo = [&](int32_t off, uint32_t own) -> long long {
+        long long hv = 0;
+        if (off >= 0) {
+            if (!P2P || own == (uint32_t)p.rank)
+                hv = __ldg(a.src + off);
+            else  // a cell of another rank's tile: read its buffer over NVLink
+                asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(hv) : "l"(s_peer[own] + off));
+        }
+        return hv;
+    };
+    auto halo_entry = [&](uint32_t t, int32_t& off, uint32_t& own) {
+        const bool ok = t < a.tile_end && lane < 8;
+        off = ok ? __ldg(halo_tab + 8ull * t + lane) : -1;
+        own = (P2P && ok) ? p.halo_owner[8ull * t + lane] : 0u;
+    };
+
+    // the bounding box of (n/32)^2 tiles, walked with an odd warp stride (tile_kernel); a box
+    // tile holds members iff bx ⊆ (n/32 - 1 - by) — the others are culled, as the reference's
+    // threads of such a block all fail their test — and a member tile finds its storage in the
+    // compact state through λ⁻¹ of its block coordinates (u = ωx_b·H_b + ωy_b)
+    const uint32_t nb = (uint32_t)(a.n >> 5), lg = 31u - __clz(nb), boxes = nb * nb;
+    const uint32_t ustride = (warp_stride | 1u) - ((warp_stride & 1u) ? 0u : 2u);
+    auto next_member = [&](uint32_t bi) -> uint32_t {
+        while (bi < boxes && ((bi & (nb - 1u)) & (nb - 1u - (bi >> lg))) != 0u) bi += ustride;
+        return bi;
+    };
+    auto tile_of_box = [&](uint32_t bi) -> uint32_t {
+        const uint32_t bx = bi & (nb - 1u), by = bi >> lg;
+        const uint32_t wx = bits_base3(even_bits(bx)) + bits_base3(even_bits(by));
+        const uint32_t wy = bits_base3(even_bits(bx >> 1)) + bits_base3(even_bits(by >> 1));
+        return wx * a.Hb + wy;
+    };
+    uint32_t bcur = next_member(warp_global < ustride ? warp_global : boxes);
+    uint32_t bnext = bcur < boxes ? next_member(bcur + ustride) : boxes;
+    uint32_t u = bcur < boxes ? tile_of_box(bcur) : 0u;
+    uint32_t u_next = bnext < boxes ? tile_of_box(bnext) : 0u;
+    uint64_t base = 0;
+    long long hv = 0;
+    int32_t hoff_n = -1;
+    uint32_t hown_n = 0;
+    if (bcur < boxes) {
+        base = tile_base(u);
+        load_tile(base);
+        int32_t off;
+        uint32_t own;
+        halo_entry(u, off, own);
+        hv = load_halo(off, own);
+        halo_entry(bnext < boxes ? u_next : a.tile_end, hoff_n, hown_n);
+    }
+    while (bcur < boxes) {
+        const uint32_t un = u_next, bn = bnext;
+        const bool more = bn < boxes;
+        const uint32_t bnn = more ? next_member(bn + ustride) : boxes;  // the tile after next
+        u_next = bnn < boxes ? tile_of_box(bnn) : 0u;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) cell[sl_pos[k]] = v[k] != 0ll;
+        if (k7) cell[sl_pos[7]] = v[7] != 0ll;
+        const uint32_t h = __ballot_sync(0xFFFFFFFFu, hv != 0ll) & 0xFFu;
+        uint64_t base_n = 0;
+        if (more) {  // warp-uniform
+            base_n = tile_base(un);
+            load_tile(base_n);
+            hv = load_halo(hoff_n, hown_n);
+            halo_entry(bnn < boxes ? u_next : a.tile_end, hoff_n, hown_n);
+        }
+        __syncwarp();
+        uint32_t R = 0;
+        {
+            const uint4 q0 = reinterpret_cast<const uint4*>(cell + 32 * lane)[0];
+            const uint4 q1 = reinterpret_cast<const uint4*>(cell + 32 * lane)[1];
+            const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) R |= ((w[i] * 0x01020408u) >> 24 & 0xFu) << (4 * i);
+        }
+        uint64_t E = (uint64_t)R << 1;
+        if (lane == 31) E |= ((h >> 3) & 1u) | ((uint64_t)((h >> 5) & 1u) << 33);
+        if (lane == 30) E |= (uint64_t)((h >> 4) & 1u) << 33;
+        const uint64_t top = (h & 1u) | (((h >> 1) & 1u) << 1) | (((h >> 2) & 1u) << 2);
+        const uint64_t bottom = (((h >> 7) & 1u) << 1) | ((uint64_t)((h >> 6) & 1u) << 33);
+        const uint64_t Eu = __shfl_up_sync(0xFFFFFFFFu, E, 1);
+        const uint64_t Ed = __shfl_down_sync(0xFFFFFFFFu, E, 1);
+        const uint64_t U = lane == 0 ? top : Eu;
+        const uint64_t D = lane == 31 ? bottom : Ed;
+        s_new[wib][lane] = life_rule((uint32_t)U, (uint32_t)(U >> 1), (uint32_t)(U >> 2), (uint32_t)E,
+                                     (uint32_t)(E >> 2), (uint32_t)D, (uint32_t)(D >> 1), (uint32_t)(D >> 2),
+                                     (uint32_t)(E >> 1), a.birth, a.survive) &
+                           submask_bits((uint32_t)lane);
+        __syncwarp();
+        char* dst = dst0 + base;
+        base = base_n;
+        u = un;
+        bcur = bn;
+        bnext = bnn;
+#pragma unroll
+        for (int k = 0; k < 7; ++k)
+            *reinterpret_cast<long long*>(dst + sl_off[k]) =
+                (long long)((s_new[wib][sl_pos[k] >> 5] >> (sl_pos[k] & 31u)) & 1u);
+        if (k7)
+            *reinterpret_cast<long long*>(dst + sl_off[7]) =
+                (long long)((s_new[wib][sl_pos[7] >> 5] >> (sl_pos[7] & 31u)) & 1u);
+        __syncwarp();
+    }
+    (void)p;
+    (void)u;
+}
+
+
 // ---- embedded member sectors <-> compact state, tile by tile ------------------------------
 // Local compact index li = ωy_l·27 + ωx_l of member (x, y) of a ρ = 32 tile (x ⊆ y < 32).
 __device__ __forceinline__ uint32_t tile_local_index(uint32_t x, uint32_t y) {

@@ -669,13 +669,20 @@ unsigned grid_for(const DeviceCtx* c, uint64_t work) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, (uint64_t)c->sms * 16));
 }
 // compact CA / RD / SW validity: the gasket, λ launch, ρ = 32 tiles inside (r >= 5)
-int compact_workload_check(const nbb_config* cfg) {
+// allow_bb: the CA step also runs as the bounding-box launch over the compact state
+// (ca_compact_bb_kernel: box tiles culled, member tiles addressed through λ⁻¹), unsharded
+int compact_workload_check(const nbb_config* cfg, bool allow_bb = false) {
     NBB_TRY(nbbhost::validate(*cfg));
     NBB_TRY(nbbhost::require_gasket(cfg->spec));
     if (cfg->r < 5)
         return fail(NBB_ERR_INVALID_ARGUMENT, "compact-state workloads need r >= 5 (32 x 32 tiles)");
     if (cfg->r > 18)  // 32-bit tile / halo indices (3^18 < 2^31)
         return fail(NBB_ERR_RESOURCE, "compact-state workloads support r <= 18");
+    if (cfg->mode == NBB_MODE_BB && allow_bb) {
+        if (cfg->shard_count > 0)
+            return fail(NBB_ERR_INVALID_ARGUMENT, "the bounding-box launch over the compact state is unsharded");
+        return NBB_OK;
+    }
     if (cfg->mode != NBB_MODE_LAMBDA)
         return fail(NBB_ERR_INVALID_ARGUMENT, "the compact state is the lambda orthotope: lambda mode only");
     return NBB_OK;
@@ -771,9 +778,15 @@ int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, vo
     const int32_t* tab;
     NBB_CHECK(compact_halo_table(ctx, cfg, a, div_hb, &tab));
     int occ;
-    NBB_CHECK(occupancy<ca_compact_kernel<false>>(256, 0, &occ));
     const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
     if (want == 0) return NBB_OK;
+    if (cfg->mode == NBB_MODE_BB) {
+        NBB_CHECK(occupancy<ca_compact_bb_kernel>(256, 0, &occ));
+        const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
+        NBB_CUDA(launch_pdl(ca_compact_bb_kernel, blocks, 256, st, a, div_hb, tab));
+        return NBB_OK;
+    }
+    NBB_CHECK(occupancy<ca_compact_kernel<false>>(256, 0, &occ));
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
     NBB_CUDA(launch_pdl(ca_compact_kernel<false>, blocks, 256, st, a, div_hb, tab, P2PArgs{}));
     return NBB_OK;
@@ -1111,7 +1124,7 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
     if (cfg->flags & NBB_FLAG_COMPACT_STATE) {
         // compact state: member sectors -> the λ-ordered compact array (2 x 8·3^r bytes on the
         // device, no embedded grid), steps on the orthotope, compact -> member sectors.
-        NBB_CHECK(compact_workload_check(cfg));
+        NBB_CHECK(compact_workload_check(cfg, true));
         if (cw != 8) return fail(NBB_ERR_INVALID_ARGUMENT, "the compact state holds int64 values: cell_width 8");
         CompactShape cs;
         NBB_CHECK(compact_shape(cfg, &cs));
@@ -1393,7 +1406,7 @@ int nbb_gpu_compact_read(const char* path, const nbb_spec* spec, int32_t* level,
 int nbb_gpu_ca_compact_step_dev(const nbb_config* cfg, const void* d_src, void* d_dst, uint16_t birth,
                                 uint16_t survive, void* stream, nbb_report* report) {
     if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
-    NBB_CHECK(compact_workload_check(cfg));
+    NBB_CHECK(compact_workload_check(cfg, true));
     DeviceCtx* ctx;
     NBB_CHECK(ensure_device(cfg->device, &ctx));
     Timer t(cfg->timing != 0, (cudaStream_t)stream);
@@ -1406,7 +1419,7 @@ int nbb_gpu_ca_compact_run_dev(const nbb_config* cfg, void* d_a, void* d_b, int3
                                uint16_t survive, void* stream) {
     if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
     if (steps < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "run_ca: steps must be non-negative");
-    NBB_CHECK(compact_workload_check(cfg));
+    NBB_CHECK(compact_workload_check(cfg, true));
     DeviceCtx* ctx;
     NBB_CHECK(ensure_device(cfg->device, &ctx));
     for (int32_t i = 0; i < steps; ++i)

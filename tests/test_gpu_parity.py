@@ -407,8 +407,11 @@ def test_ca_compact_state(golden, r):
     for k, (pop, digest) in w["ca"].items():
         out = nbb.run_ca(cfg(r=r, rho=32, flags=abi.FLAG_COMPACT_STATE), g, int(k)).grid.values
         assert (int(out.sum()), fnv1a64(out)) == (pop, digest), k
-    with pytest.raises(nbb.InvalidArgument, match="lambda mode only"):
-        nbb.run_ca(cfg(r=r, rho=32, mode=MapMode.BoundingBox, flags=abi.FLAG_COMPACT_STATE), g, 1)
+    # the bounding-box launch over the same compact state (box tiles culled, λ⁻¹ addressing)
+    for steps in (1, 4):
+        out = nbb.run_ca(cfg(r=r, rho=32, mode=MapMode.BoundingBox, flags=abi.FLAG_COMPACT_STATE), g,
+                         steps).grid.values
+        assert (int(out.sum()), fnv1a64(out)) == tuple(w["ca"][str(steps)]), ("bb", steps)
 
 
 def test_compact_device_workloads():
