@@ -37,8 +37,9 @@ for be in (nbb.LambdaBackend.MmaV1, nbb.LambdaBackend.MmaV2):
     c = nbb.DispatchConfig(r=r, rho=8, backend=be, kernel=nbb.KernelFamily.PerCell)
     assert np.array_equal(nbb.run_ca(c, nbb.Grid(G, r, g), 3).grid.values, want)
     checks += 1
-c = nbb.DispatchConfig(r=r, rho=32, flags=_abi.FLAG_COMPACT_STATE)
-assert np.array_equal(nbb.run_ca(c, nbb.Grid(G, r, g), 3).grid.values, want)
+for mode in (nbb.MapMode.Lambda, nbb.MapMode.BoundingBox):  # λ and BB launches over the compact state
+    c = nbb.DispatchConfig(r=r, rho=32, mode=mode, flags=_abi.FLAG_COMPACT_STATE)
+    assert np.array_equal(nbb.run_ca(c, nbb.Grid(G, r, g), 3).grid.values, want), mode
 comp = nbb.compact_store(G, r, g)
 assert np.array_equal(nbb.compact_load(G, comp, 0), g)
 xy = nbb.lambda_coords(nbb.DispatchConfig(r=r, rho=1), r)
