@@ -112,7 +112,9 @@ typedef struct nbb_config {
 #define NBB_FLAG_OUT_ZEROED 1u
 /* NBB_FLAG_COMPACT_STATE: nbb_gpu_ca keeps the CA state on the device in the compact
  *   (λ-ordered CompactGrid) layout between the two conversions — int64 values, every
- *   byte a member (gasket, cell_width 8, r >= 5, lambda mode). */
+ *   byte a member (gasket, cell_width 8, r >= 5). Lambda mode walks the orthotope (the
+ *   compact array's own order); BB mode walks the bounding box, culls empty tiles and
+ *   addresses member tiles through λ⁻¹ (the comparison launch; unsharded). */
 #define NBB_FLAG_COMPACT_STATE 2u
 
 /* WorkReport (dispatch.hpp:44-61) */
