@@ -132,7 +132,9 @@ int main() {
         std::memset(p, 0, bytes);
         if (cudaHostRegister(p, bytes, cudaHostRegisterMapped) != cudaSuccess) return 2;
         h = (long long*)p;
-    } else if (cudaHostAlloc((void**)&h, bytes, cudaHostAllocMapped) != cudaSuccess) {
+    } else if (cudaHostAlloc((void**)&h, bytes,
+                             cudaHostAllocMapped | (getenv("PROBE_WC") ? cudaHostAllocWriteCombined : 0u)) !=
+               cudaSuccess) {
         return 1;
     }
     for (size_t i = 0; i < bytes / 8; i += 512) h[i] = (long long)i;
@@ -142,7 +144,7 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    printf("{\"host_alloc\": \"%s\", ", huge ? "mmap+MADV_HUGEPAGE+cudaHostRegister" : "cudaHostAlloc");
+    printf("{\"host_alloc\": \"%s\", ", huge ? "mmap+MADV_HUGEPAGE+cudaHostRegister" : getenv("PROBE_WC") ? "cudaHostAlloc(WriteCombined)" : "cudaHostAlloc");
     const char* names[3] = {"sector", "chunk", "line"};
     for (int g = 0; g < 3; ++g) {
         const int unit = 32 << g, per_row = 256 / unit;  // units per 256-byte tile row
