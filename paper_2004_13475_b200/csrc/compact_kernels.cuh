@@ -308,18 +308,20 @@ __global__ void compact_halo_table_kernel(CompactCaArgs a, FastDiv div_hb, int32
 // Per tile: 8 coalesced 8-byte loads per lane (compact rows of 27 values), the 8 halo cells
 // (compact offsets from the per-level halo table), alive bits scattered as bytes into a per-warp
 // 32 x 32 byte tile (non-member bytes stay 0, so no atomics and no clearing), rows packed back
-// to bit masks (lane = row) for the bit-sliced rule, and 8 stores per lane. The kernel is
-// issue-bound as much as DRAM-bound (ncu: ALU pipe 66%, long-scoreboard 61% of stalls),
-// hence the instruction diet. Tried and slower on B200 (profiles/r1_compact_ca_tuning.md):
-// a cp.async ring (8-byte copies), L2 bulk prefetch one tile ahead, 64/48-register budgets,
-// and cp.async.bulk row copies into an mbarrier ring.
+// to bit masks (lane = row) for the bit-sliced rule, and 8 stores per lane. Software-pipelined
+// (the next tile's loads fly during this tile's rule and stores) and launched with PDL; at
+// n = 2^16 a step runs at 0.964 of the measured HBM copy peak, long-scoreboard the dominant
+// stall (ncu: profiles/r1_ncu_ca_compact_v5.txt). Tried and slower on B200
+// (profiles/r1_compact_ca_tuning.md): a cp.async ring (8-byte copies), L2 bulk prefetch one
+// tile ahead, 64/48-register budgets, cp.async.bulk row copies into an mbarrier ring, all steps
+// in one launch with tile-level dataflow, and exported boundary-cell bytes for the halo.
 //
 // P2P = true is the multi-GPU form (one kernel per step, no separate exchange): each rank
 // owns a contiguous range of tiles in its own replica-sized buffers, the halo cells owned
 // by other ranks are read straight from their buffers over NVLink (CUDA IPC mappings,
 // ld.relaxed.sys), and a flag barrier in peer memory orders the steps: the kernel first
-// waits until every rank has finished the previous step (world x steps-done arrivals on this
-// rank's counter), and its last CTA to finish adds one arrival to every rank's flag.
+// waits until every rank has finished the previous step (world x i arrivals on this rank's
+// counter before step i), and its last CTA to finish adds one arrival to every rank's flag.
 template <bool P2P>
 __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, FastDiv div_hb,
                                                              const int32_t* __restrict__ halo_tab,
