@@ -21,7 +21,7 @@ from paper_2004_13475_b200 import _abi, nbb  # noqa: E402
 
 G = nbb.FractalSpec.sierpinski()
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 600.0
-rng = random.Random(20261017)
+rng = random.Random(int(os.environ.get("SWEEP_SEED", "20261017")))
 t_end = time.time() + budget
 counts, bad = {}, []
 
