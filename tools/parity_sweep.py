@@ -60,29 +60,44 @@ def families(r):
             fam.append((f"tile_{mode.name}_bit", cfg(r=r, rho=32, mode=mode, cell_width=0, kernel=nbb.KernelFamily.Tile)))
     if r >= 5:
         fam.append(("compact_state", cfg(r=r, rho=32, flags=_abi.FLAG_COMPACT_STATE)))
+        fam.append(("compact_state_bb", cfg(r=r, rho=32, mode=nbb.MapMode.BoundingBox,
+                                            flags=_abi.FLAG_COMPACT_STATE)))
     return fam
 
 
+def generic_families(spec, r):
+    """Vicsek / carpet (s = 3): the per-cell kernels with the table-driven λ, ρ = 1, 3, 9."""
+    fam = []
+    for mode in (nbb.MapMode.Lambda, nbb.MapMode.BoundingBox):
+        for rho in (1, 3, 9):
+            if rho <= spec.side_length(r):
+                fam.append((f"{spec.name}_percell_{mode.name}_rho{rho}",
+                            cfg(spec=spec, r=r, rho=rho, mode=mode, kernel=nbb.KernelFamily.PerCell)))
+    return fam
+
+
+it = 0
 while time.time() < t_end:
-    r = rng.randint(1, 12)
+    it += 1
+    spec = G if it % 4 else (nbb.FractalSpec.vicsek() if it % 8 else nbb.FractalSpec.carpet())
+    r = rng.randint(1, 12) if spec is G else rng.randint(1, 4)
     seed = rng.randrange(1 << 30)
     modulus = rng.choice([2, 3, 100, 1 << 20, 1 << 62])
-    g = orc_random_member_grid(r, seed, modulus)
+    g = orc_random_member_grid(r, seed, modulus, spec)
     rule = nbb.CaRule(birth=rng.randrange(1, 1 << 9), survive=rng.randrange(0, 1 << 9))
     steps = rng.randint(0, 6)
-    want_ca = orc_ca(r, g, steps, rule.birth, rule.survive)
-    want_rd = orc_reduction(r, g)
-    want_sw = orc_single_write(r)
-    grid = nbb.Grid(G, r, g)
-    for name, c in families(r):
-        info = {"r": r, "seed": seed, "modulus": modulus, "rule": [rule.birth, rule.survive], "steps": steps}
+    want_ca = orc_ca(r, g, steps, rule.birth, rule.survive, spec)
+    want_rd = orc_reduction(r, g, spec)
+    want_sw = orc_single_write(r, spec)
+    grid = nbb.Grid(spec, r, g)
+    for name, c in (families(r) if spec is G else generic_families(spec, r)):
+        info = {"spec": spec.name, "r": r, "seed": seed, "modulus": modulus, "rule": [rule.birth, rule.survive],
+                "steps": steps}
         try:
-            if c.cell_width == 8 or name == "compact_state":
-                out = nbb.run_ca(c, grid, steps, rule).grid.values
-            else:  # uint8 / 1-bit states: the reference's Grid in and out
-                out = nbb.run_ca(c, grid, steps, rule).grid.values
+            # every state layout keeps the reference's int64 Grid at the boundary
+            out = nbb.run_ca(c, grid, steps, rule).grid.values
             check(name + ":ca", np.array_equal(out, want_ca), info)
-            if c.cell_width == 8 and name != "compact_state":
+            if c.cell_width == 8 and not name.startswith("compact_state"):
                 check(name + ":rd", nbb.run_reduction(c, grid).value == want_rd, info)
                 check(name + ":sw", np.array_equal(nbb.run_single_write(c).grid.values, want_sw), info)
         except nbb.NbbError as e:  # configurations the reference rejects are rejected here too
