@@ -530,7 +530,7 @@ def test_full_size_r16_properties():
     assert int(k2.sum().item()) == ref_sum
 
 
-@pytest.mark.parametrize("r", [17])
+@pytest.mark.parametrize("r", [17, 18])
 def test_compact_ca_full_size_sampled(r):
     """C5 size (n = 2^17, 3^17 members): two steps through the library's step loop, then a third
     step checked against the oracle rule on 600k sampled cells — uniform, every tile-corner
