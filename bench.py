@@ -88,7 +88,7 @@ class ClockSampler:
                 self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
             except Exception:
                 pass
-            time.sleep(0.002)
+            time.sleep(0.001)
 
     def __enter__(self):
         if self._nv is not None:
@@ -300,12 +300,12 @@ def main():
     def timed_run(run, K, W, sampler=None, groups=None):
         """run(k) issues k steps on `stream`; W warm-up steps, then K timed with CUDA events.
         groups (a list) receives the per-step means of G equal sub-runs (events between them)."""
+        if sampler:  # NVML sampling from the warm-up on: the timed region alone is ~20 ms
+            sampler.__enter__()
         run(W)
         barrier()
         G = 10 if (groups is not None and K >= 10) else 1
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(G + 1)]
-        if sampler:
-            sampler.__enter__()
         ev[0].record(stream)
         for gi in range(G):
             k = K // G + (1 if gi < K % G else 0)
