@@ -226,12 +226,13 @@ def _p2p_full_worker(rank, world, port, r, steps, q):
     dist.destroy_process_group()
 
 
-def test_p2p_compact_ca_full_size_r17():
-    """C5 (n = 2^17) through the multi-rank P2P step loop (2 ranks time-sharing one B200, their
-    non-owned cells poisoned) equals the single-GPU compact step loop bit for bit."""
+@pytest.mark.parametrize("r,world", [(17, 2), (18, 2)])
+def test_p2p_compact_ca_full_size_r17(r, world):
+    """C5 (n = 2^17, and 2^18) through the multi-rank P2P step loop (2 ranks time-sharing one B200,
+    their non-owned cells poisoned) equals the single-GPU compact step loop bit for bit."""
     from paper_2004_13475_b200 import device as dev
     from paper_2004_13475_b200 import nbb
-    r, steps, world = 17, 3, 2
+    steps = 3
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
