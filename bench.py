@@ -356,6 +356,14 @@ def main():
                            f"tiles (segment_sum_kernel) + one int64 all-reduce, value read back on the host; state = the initial random_member_grid",
                "ms_per_call": rd_ms, "value": members * 1e3 / rd_ms, "unit": "cells/s",
                "GBps_per_gpu": 8 * members / world / (rd_ms * 1e-3) / 1e9, "sum": rd_val}
+    # the partial-sum kernel alone, back to back (no host read-back): its share of the call
+    rd_part = torch.empty(1, dtype=torch.int64, device="cuda")
+    rd_cfg = plan_c.local_config(cfg())
+    rd_kern_ms = timed(lambda: dev.reduction_compact_dev(rd_cfg, c1.data_ptr(), rd_part.data_ptr(), s),
+                       max(10, K // 4), W)
+    rd_line["kernel_only"] = {"ms": rd_kern_ms, "GBps": 8 * members / world / (rd_kern_ms * 1e-3) / 1e9,
+                              "frac": 8 * members / world / (rd_kern_ms * 1e-3) / 1e9 / measured_peaks()[0],
+                              "note": "memset + segment_sum_kernel per call, no host read-back"}
     # ---- headline: λ(ω) CA step on the compact state, ρ = 32 tiles ---------------------
     head_groups = []  # per-step means of 10 sub-runs (N = 1): median / paper-style mean
     # the step loop runs in the library (C++; one kernel per step, PDL between steps)

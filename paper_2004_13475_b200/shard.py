@@ -249,19 +249,38 @@ def sharded_reduction(plan: ShardPlan, config, d_state: int, dist, stream: int =
     import torch
     from . import device as dev
     c = plan.local_config(config)
-    part = torch.zeros(1, dtype=torch.int64, device=torch.device("cuda", device))
+    part, host = _scalar_buffers(device)  # the kernels overwrite the device scalar (no zero-fill)
     if plan.state == "compact":
         dev.reduction_compact_dev(c, d_state, part.data_ptr(), stream)
     else:
         dev.reduction_dev(c, d_state, part.data_ptr(), stream)
-    if plan.world > 1:
-        if dist.get_backend() == "nccl":
-            dist.all_reduce(part)
-        else:
-            h = part.cpu()
-            dist.all_reduce(h)
-            part = h
-    return int(part.item())
+    ts = (torch.cuda.ExternalStream(stream, device=part.device) if stream
+          else torch.cuda.default_stream(part.device))
+    with torch.cuda.stream(ts):
+        if plan.world > 1:
+            if dist.get_backend() == "nccl":
+                dist.all_reduce(part)
+            else:
+                h = part.cpu()
+                dist.all_reduce(h)
+                return int(h.item())
+        host.copy_(part, non_blocking=True)
+        ts.synchronize()
+    return int(host[0])
+
+
+_SCALARS: dict = {}
+
+
+def _scalar_buffers(device: int):
+    """One int64 device scalar and one pinned host scalar per device, reused across calls."""
+    import torch
+    b = _SCALARS.get(device)
+    if b is None:
+        b = (torch.empty(1, dtype=torch.int64, device=torch.device("cuda", device)),
+             torch.empty(1, dtype=torch.int64, pin_memory=True))
+        _SCALARS[device] = b
+    return b
 
 
 def sharded_single_write(plan: ShardPlan, config, d_state: int, stream: int = 0) -> None:
