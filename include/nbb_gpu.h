@@ -116,6 +116,11 @@ typedef struct nbb_config {
  *   compact array's own order); BB mode walks the bounding box, culls empty tiles and
  *   addresses member tiles through λ⁻¹ (the comparison launch; unsharded). */
 #define NBB_FLAG_COMPACT_STATE 2u
+/* NBB_FLAG_SINGLE_STEP: compact-state CA runs (nbb_gpu_ca with NBB_FLAG_COMPACT_STATE,
+ *   nbb_gpu_ca_compact_run_dev) launch one kernel per step. Without it, untimed lambda
+ *   runs advance two steps per pass over the state (ca_compact2_kernel: the tile and its
+ *   radius-2 halo are read once, the intermediate step stays on chip) — the same result. */
+#define NBB_FLAG_SINGLE_STEP 4u
 
 /* WorkReport (dispatch.hpp:44-61) */
 typedef struct nbb_report {

@@ -66,6 +66,7 @@ class NbbConfig(Structure):
 
 FLAG_OUT_ZEROED = 1
 FLAG_COMPACT_STATE = 2
+FLAG_SINGLE_STEP = 4
 
 
 class NbbReport(Structure):

@@ -460,6 +460,178 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
 }
 
 
+// ---- two CA steps per pass (temporal blocking of the compact step) ------------------------
+// The radius-2 halo of a ρ = 32 tile: the 8 cells of compact_halo_table_kernel (H1, the
+// member neighbours of the tile's members) followed by the 14 positions that can hold a member
+// neighbour of an H1 cell outside the tile (H2; found by brute force over every tile of r = 6..11,
+// the set is the same at every level by self-similarity). Tile-local (x, y).
+constexpr int kHalo2 = 22, kHalo2Stride = 24;
+__constant__ int8_t c_h2x[kHalo2] = {-1, 0, 1, -1, 32, 32, 32, 0, -2, -2, -2, -2, 0, 0, 1, 2, 2, 32, 32, 33, 33, 33};
+__constant__ int8_t c_h2y[kHalo2] = {-1, -1, -1, 31, 30, 31, 32, 32, -2, -1, 30, 31, -2, 33, 33, -2, -1, 29, 33, 29, 31, 33};
+
+// [tile u][k] compact offsets of the 22 halo positions (-1: not a member / outside), stride 24
+__global__ void compact_halo2_table_kernel(CompactCaArgs a, FastDiv div_hb, int32_t* tab) {
+    const uint32_t nm1 = (uint32_t)(a.n - 1);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (uint64_t)a.tiles * kHalo2Stride;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = (uint32_t)(i / kHalo2Stride), hk = (uint32_t)(i % kHalo2Stride);
+        int32_t off = -1;
+        if (hk < (uint32_t)kHalo2) {
+            const uint32_t wxb = fastdiv(u, div_hb), wyb = u - wxb * a.Hb;
+            uint32_t bx, by;
+            lambda_arith(wxb, wyb, bx, by);
+            const uint32_t gx = bx * 32u + (uint32_t)(int)c_h2x[hk], gy = by * 32u + (uint32_t)(int)c_h2y[hk];
+            if (gx <= nm1 && gy <= nm1 && (gx & (nm1 - gy)) == 0u) off = (int32_t)gasket_compact_offset(gx, gy, a.W);
+        }
+        tab[i] = off;
+    }
+}
+
+// One bit-sliced step of a tile held as row masks (lane = row y, bit x) with the 8 H1 halo
+// bits h (order of compact_halo_table_kernel); members only.
+__device__ __forceinline__ uint32_t compact_rows_step(uint32_t R, uint32_t h, int lane, uint32_t birth,
+                                                      uint32_t survive) {
+    uint64_t E = (uint64_t)R << 1;
+    if (lane == 31) E |= ((h >> 3) & 1u) | ((uint64_t)((h >> 5) & 1u) << 33);
+    if (lane == 30) E |= (uint64_t)((h >> 4) & 1u) << 33;
+    const uint64_t top = (h & 1u) | (((h >> 1) & 1u) << 1) | (((h >> 2) & 1u) << 2);
+    const uint64_t bottom = (((h >> 7) & 1u) << 1) | ((uint64_t)((h >> 6) & 1u) << 33);
+    const uint64_t Eu = __shfl_up_sync(0xFFFFFFFFu, E, 1);
+    const uint64_t Ed = __shfl_down_sync(0xFFFFFFFFu, E, 1);
+    const uint64_t U = lane == 0 ? top : Eu;
+    const uint64_t D = lane == 31 ? bottom : Ed;
+    return life_rule((uint32_t)U, (uint32_t)(U >> 1), (uint32_t)(U >> 2), (uint32_t)E, (uint32_t)(E >> 2),
+                     (uint32_t)D, (uint32_t)(D >> 1), (uint32_t)(D >> 2), (uint32_t)(E >> 1), birth, survive) &
+           submask_bits((uint32_t)lane);
+}
+
+// Two CA steps per pass over the compact state: each warp loads its tile (243 values) and the
+// 22 radius-2 halo cells once, computes step t+1 for the tile (bit-sliced) and for its 8 H1
+// halo cells (lanes 0..7, scalar, from the step-t bytes), then step t+2 for the tile from those,
+// and stores step t+2 — 8 B read + 8 B write per member per TWO steps. Same tile walk, software
+// pipeline and PDL as ca_compact_kernel; the step-t+1 state never reaches HBM.
+__global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, FastDiv div_hb,
+                                                             const int32_t* __restrict__ halo_tab) {
+    __shared__ __align__(16) uint8_t s_cell[8][32 * 32];
+    __shared__ uint32_t s_new[8][32];
+    __shared__ uint16_t s_pos[256];
+    __shared__ uint16_t s_code[64];  // H1 cell k, neighbour d: tile byte | 0x4000 + halo slot | 0x8000
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint8_t* cell = s_cell[wib];
+    pdl_trigger();
+    s_pos[threadIdx.x] = threadIdx.x < 243 ? c_local_pos[threadIdx.x] : 0;
+    if (threadIdx.x < 64) {
+        const int k = threadIdx.x >> 3, d = threadIdx.x & 7;
+        const int dd = d < 4 ? d : d + 1;  // the 8 neighbours of the 3 x 3 block, centre skipped
+        const int qx = c_h2x[k] + dd % 3 - 1, qy = c_h2y[k] + dd / 3 - 1;
+        uint16_t code = 0x8000u;
+        if (qx >= 0 && qx < 32 && qy >= 0 && qy < 32) {
+            code = (uint16_t)(qy * 32 + qx);
+        } else {
+            for (int j = 0; j < kHalo2; ++j)
+                if (c_h2x[j] == qx && c_h2y[j] == qy) code = (uint16_t)(0x4000u | j);
+        }
+        s_code[threadIdx.x] = code;
+    }
+    pdl_wait();
+    __syncthreads();
+    uint32_t sl_off[8], sl_pos[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t li = 32u * k + lane;
+        const bool ok = li < 243u;
+        const uint32_t row = ok ? li / 27u : 0u, col = ok ? li % 27u : 0u;
+        sl_off[k] = (row * a.W + col) * 8u;
+        sl_pos[k] = s_pos[li];
+    }
+    const uint16_t* my_code = s_code + (lane & 7) * 8;
+    const bool k7 = lane < 19;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) reinterpret_cast<uint32_t*>(cell)[32 * i + lane] = 0u;
+    const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t warp_stride = (gridDim.x * blockDim.x) >> 5;
+    const char* src0 = reinterpret_cast<const char*>(a.src);
+    char* dst0 = reinterpret_cast<char*>(a.dst);
+    __syncwarp();
+
+    auto tile_base = [&](uint32_t t) -> uint64_t {
+        const uint32_t wxb = fastdiv(t, div_hb), wyb = t - wxb * a.Hb;
+        return ((uint64_t)(9u * wxb) * a.W + 27u * wyb) * 8u;
+    };
+    long long v[8];
+    auto load_tile = [&](uint64_t b) {
+        const char* src = src0 + b;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) v[k] = __ldg(reinterpret_cast<const long long*>(src + sl_off[k]));
+        v[7] = k7 ? __ldg(reinterpret_cast<const long long*>(src + sl_off[7])) : 0ll;
+    };
+    auto halo_entry = [&](uint32_t t) -> int32_t {
+        return (t < a.tile_end && lane < kHalo2) ? __ldg(halo_tab + (uint64_t)kHalo2Stride * t + lane) : -1;
+    };
+
+    uint32_t u = a.tile_begin + warp_global;
+    uint64_t base = 0;
+    long long hv = 0;
+    uint32_t hmem = 0;  // H1 slots that are members (bit k)
+    int32_t hoff_n = -1;
+    if (u < a.tile_end) {
+        base = tile_base(u);
+        load_tile(base);
+        const int32_t off = halo_entry(u);
+        hv = off >= 0 ? __ldg(a.src + off) : 0ll;
+        hmem = __ballot_sync(0xFFFFFFFFu, off >= 0) & 0xFFu;
+        hoff_n = halo_entry(u + warp_stride);
+    }
+    for (; u < a.tile_end; u += warp_stride) {
+        const uint32_t un = u + warp_stride;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) cell[sl_pos[k]] = v[k] != 0ll;
+        if (k7) cell[sl_pos[7]] = v[7] != 0ll;
+        const uint32_t hm = __ballot_sync(0xFFFFFFFFu, hv != 0ll);  // step-t halo alive bits
+        const uint32_t hmem_cur = hmem;
+        uint64_t base_n = 0;
+        if (un < a.tile_end) {  // warp-uniform
+            base_n = tile_base(un);
+            load_tile(base_n);
+            hv = hoff_n >= 0 ? __ldg(a.src + hoff_n) : 0ll;
+            hmem = __ballot_sync(0xFFFFFFFFu, hoff_n >= 0) & 0xFFu;
+            hoff_n = halo_entry(un + warp_stride);
+        }
+        __syncwarp();
+        uint32_t R = 0;
+        {
+            const uint4 q0 = reinterpret_cast<const uint4*>(cell + 32 * lane)[0];
+            const uint4 q1 = reinterpret_cast<const uint4*>(cell + 32 * lane)[1];
+            const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) R |= ((w[i] * 0x01020408u) >> 24 & 0xFu) << (4 * i);
+        }
+        // step t+1: the tile (bit-sliced) and the H1 cells (lane k < 8, scalar)
+        const uint32_t R1 = compact_rows_step(R, hm & 0xFFu, lane, a.birth, a.survive);
+        uint32_t live = 0;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+            const uint32_t c = my_code[d];
+            live += (c & 0x8000u) ? 0u : (c & 0x4000u) ? (hm >> (c & 31u)) & 1u : (uint32_t)cell[c & 1023u];
+        }
+        const uint32_t rule = ((hm >> (lane & 7)) & 1u) ? a.survive : a.birth;
+        const uint32_t h1 = __ballot_sync(0xFFFFFFFFu, lane < 8 && ((rule >> live) & 1u)) & hmem_cur;
+        // step t+2: the tile only
+        s_new[wib][lane] = compact_rows_step(R1, h1, lane, a.birth, a.survive);
+        __syncwarp();
+        char* dst = dst0 + base;
+        base = base_n;
+#pragma unroll
+        for (int k = 0; k < 7; ++k)
+            *reinterpret_cast<long long*>(dst + sl_off[k]) =
+                (long long)((s_new[wib][sl_pos[k] >> 5] >> (sl_pos[k] & 31u)) & 1u);
+        if (k7)
+            *reinterpret_cast<long long*>(dst + sl_off[7]) =
+                (long long)((s_new[wib][sl_pos[7] >> 5] >> (sl_pos[7] & 31u)) & 1u);
+        __syncwarp();
+    }
+}
+
 // The BOUNDING-BOX launch of the compact-state CA step (the comparison for ca_compact_kernel on
 // the same storage): identical per-tile work, but the warps walk all (n/32)^2 box tiles, cull
 // the non-member ones and address each member tile through λ⁻¹ — the inverse map the compact

@@ -74,6 +74,7 @@ struct DeviceCtx {
     size_t buf_bytes[3] = {0, 0, 0};
     int16_t* lut[6] = {};                    // LocalCellTable per edge 2^i
     int32_t* halo_tab[32] = {};              // compact CA halo table per level r
+    int32_t* halo2_tab[32] = {};             // radius-2 halo table (two steps per pass) per level r
 };
 
 std::mutex g_mutex;
@@ -753,6 +754,23 @@ int compact_halo_table(DeviceCtx* ctx, const nbb_config* cfg, const CompactCaArg
     return NBB_OK;
 }
 
+// the radius-2 halo table of ca_compact2_kernel, built once (then cached) per device and level
+int compact_halo2_table(DeviceCtx* ctx, const nbb_config* cfg, const CompactCaArgs& a, const FastDiv& d,
+                        const int32_t** out) {
+    std::lock_guard<std::mutex> lock(g_mutex);
+    int32_t*& t = ctx->halo2_tab[cfg->r];
+    if (!t) {
+        NBB_CUDA(cudaMalloc(&t, (size_t)a.tiles * kHalo2Stride * sizeof(int32_t)));
+        const uint64_t n = (uint64_t)a.tiles * kHalo2Stride;
+        const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sms * 16));
+        compact_halo2_table_kernel<<<blocks, 256, 0, ctx->stream>>>(a, d, t);
+        NBB_CUDA(cudaGetLastError());
+        NBB_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    *out = t;
+    return NBB_OK;
+}
+
 // Launch with programmatic stream serialization (PDL): the kernel may start while the previous
 // kernel on the stream drains; kernels launched this way call griddepcontrol.wait before
 // touching memory the previous kernel writes (ca_compact_kernel: pdl_wait()).
@@ -789,6 +807,44 @@ int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, vo
     NBB_CHECK(occupancy<ca_compact_kernel<false>>(256, 0, &occ));
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
     NBB_CUDA(launch_pdl(ca_compact_kernel<false>, blocks, 256, st, a, div_hb, tab, P2PArgs{}));
+    return NBB_OK;
+}
+
+// two CA steps in one pass (ca_compact2_kernel); λ launch only
+int launch_ca_compact2(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* dst, uint16_t birth,
+                       uint16_t survive, cudaStream_t st) {
+    FastDiv div_hb;
+    const CompactCaArgs a = compact_args(cfg, src, dst, birth, survive, &div_hb);
+    const int32_t* tab;
+    NBB_CHECK(compact_halo2_table(ctx, cfg, a, div_hb, &tab));
+    const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
+    if (want == 0) return NBB_OK;
+    int occ;
+    NBB_CHECK(occupancy<ca_compact2_kernel>(256, 0, &occ));
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
+    NBB_CUDA(launch_pdl(ca_compact2_kernel, blocks, 256, st, a, div_hb, tab));
+    return NBB_OK;
+}
+
+// `steps` CA steps a <-> b on the compact state; the result lands in b for odd `steps`, in a
+// for even (as with one launch per step). λ launches without per-step timing run the steps in
+// pairs (ca_compact2_kernel); the number of pair launches is kept even (one pair split into two
+// single steps when needed) so the launch count's parity, and with it the result buffer, is
+// the same as stepping one by one.
+int run_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, void* d_a, void* d_b, int32_t steps, uint16_t birth,
+                   uint16_t survive, cudaStream_t st) {
+    int32_t pairs = 0;
+    if (cfg->mode != NBB_MODE_BB && !cfg->timing && !(cfg->flags & NBB_FLAG_SINGLE_STEP)) {
+        pairs = steps / 2;
+        if (pairs & 1) --pairs;
+    }
+    int64_t launches = 0;
+    auto src = [&] { return (launches & 1) ? d_b : d_a; };
+    auto dst = [&] { return (launches & 1) ? d_a : d_b; };
+    for (int32_t i = 0; i < pairs; ++i, ++launches)
+        NBB_CHECK(launch_ca_compact2(ctx, cfg, src(), dst(), birth, survive, st));
+    for (int32_t i = 2 * pairs; i < steps; ++i, ++launches)
+        NBB_CHECK(launch_ca_compact(ctx, cfg, src(), dst(), birth, survive, st));
     return NBB_OK;
 }
 }  // namespace
@@ -1141,12 +1197,19 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
         compact_from_rows_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)src, (long long*)ca,
                                                                         (int64_t)cs.n, (uint32_t)cs.W);
         NBB_CUDA(cudaGetLastError());
-        for (int s = 0; s < steps; ++s) {
-            Timer t(cfg->timing != 0, L.stream);
-            NBB_CHECK(launch_ca_compact(L.ctx, cfg, ca, cb, birth, survive, L.stream));
-            const uint64_t us = t.stop_micros();
-            if (per_step) fill_report(cfg, &per_step[s], us);
-            std::swap(ca, cb);
+        if (cfg->timing) {  // per-step launch times: one launch per step
+            for (int s = 0; s < steps; ++s) {
+                Timer t(true, L.stream);
+                NBB_CHECK(launch_ca_compact(L.ctx, cfg, ca, cb, birth, survive, L.stream));
+                const uint64_t us = t.stop_micros();
+                if (per_step) fill_report(cfg, &per_step[s], us);
+                std::swap(ca, cb);
+            }
+        } else {
+            NBB_CHECK(run_ca_compact(L.ctx, cfg, ca, cb, steps, birth, survive, L.stream));
+            if (per_step)
+                for (int s = 0; s < steps; ++s) fill_report(cfg, &per_step[s], 0);
+            if (steps & 1) std::swap(ca, cb);
         }
         if (h_out) {  // member sectors straight into the zeroed pinned output, row by row
             compact_to_rows_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)ca, h_out,
@@ -1422,10 +1485,7 @@ int nbb_gpu_ca_compact_run_dev(const nbb_config* cfg, void* d_a, void* d_b, int3
     NBB_CHECK(compact_workload_check(cfg, true));
     DeviceCtx* ctx;
     NBB_CHECK(ensure_device(cfg->device, &ctx));
-    for (int32_t i = 0; i < steps; ++i)
-        NBB_CHECK(launch_ca_compact(ctx, cfg, (i & 1) ? d_b : d_a, (i & 1) ? d_a : d_b, birth, survive,
-                                    (cudaStream_t)stream));
-    return NBB_OK;
+    return run_ca_compact(ctx, cfg, d_a, d_b, steps, birth, survive, (cudaStream_t)stream);
 }
 
 int nbb_gpu_ca_compact_p2p_dev(const nbb_config* cfg, int64_t first_step, int32_t steps, uint16_t birth,
@@ -1563,6 +1623,10 @@ int nbb_gpu_release(void) {
             c.buf_bytes[i] = 0;
         }
         for (auto& t : c.halo_tab) {
+            if (t) cudaFree(t);
+            t = nullptr;
+        }
+        for (auto& t : c.halo2_tab) {
             if (t) cudaFree(t);
             t = nullptr;
         }

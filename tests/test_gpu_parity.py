@@ -530,6 +530,53 @@ def test_full_size_r16_properties():
     assert int(k2.sum().item()) == ref_sum
 
 
+@pytest.mark.parametrize("r", [5, 6, 7, 8, 10, 13])
+def test_compact_ca_two_steps_per_pass(r):
+    """ca_compact2_kernel (two steps per pass, radius-2 halo) against the oracle and against
+    one launch per step (NBB_FLAG_SINGLE_STEP): random alive values (and values with other
+    non-zero bit patterns) for every rule in RULES — incl. births at 0 and 8 neighbours — and
+    step counts that use 0, 2 and 4 pair launches, odd and even."""
+    import torch
+    from paper_2004_13475_b200 import _abi as abi
+    from paper_2004_13475_b200 import device as dev
+    members = 3 ** r
+    s = torch.cuda.current_stream().cuda_stream
+    for rule in RULES:
+        init = orc_random_member_grid(r, 900 + r, 2)
+        for steps in (4, 5, 8, 9):
+            want = orc_ca(r, init, steps, rule.birth, rule.survive)
+            got = nbb.run_ca(cfg(r=r, rho=32, flags=abi.FLAG_COMPACT_STATE), grid(init, r), steps, rule)
+            assert np.array_equal(got.grid.values, want), (r, rule, steps)
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(r)
+        x0 = torch.randint(-3, 3, (members,), dtype=torch.int64, device="cuda", generator=gen)
+        outs = []
+        for flags in (0, abi.FLAG_SINGLE_STEP):
+            a, b = x0.clone(), torch.empty_like(x0)
+            dev.ca_compact_run_dev(cfg(r=r, rho=32, flags=flags), a.data_ptr(), b.data_ptr(), 12, rule, s)
+            outs.append(a)
+        assert torch.equal(outs[0], outs[1]), (r, rule)
+
+
+@pytest.mark.parametrize("r", [16, 17])
+def test_compact_ca_two_steps_per_pass_full_size(r):
+    """At full size: 8 steps as 4 pair launches equal 8 single-step launches, bit for bit."""
+    import torch
+    from paper_2004_13475_b200 import _abi as abi
+    from paper_2004_13475_b200 import device as dev
+    s = torch.cuda.current_stream().cuda_stream
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(4200 + r)
+    x0 = torch.randint(0, 2, (3 ** r,), dtype=torch.int64, device="cuda", generator=gen)
+    outs = []
+    for flags in (0, abi.FLAG_SINGLE_STEP):
+        a, b = x0.clone(), torch.empty_like(x0)
+        dev.ca_compact_run_dev(cfg(r=r, rho=32, flags=flags), a.data_ptr(), b.data_ptr(), 8, CaRule(), s)
+        outs.append(a)
+        del b
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("r", [17, 18])
 def test_compact_ca_full_size_sampled(r):
     """C5 size (n = 2^17, 3^17 members): two steps through the library's step loop, then a third
