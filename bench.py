@@ -165,10 +165,20 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def pair_launches(k):
+    """Launches of nbb_gpu_ca_compact_run_dev for k steps: pairs (two steps per pass, an even
+    number of them) + single steps (nbb_capi.cu run_ca_compact)."""
+    pairs = k // 2
+    pairs -= pairs & 1
+    return pairs, k - 2 * pairs
+
+
 def config_block(r, rho, world=1, transport="p2p"):
     return {"workload": f"C3: gasket n=2^{r} cellular-automaton step (B3/S23), lambda(omega) launch, "
                         f"rho={rho} tiles; device state = the lambda-ordered compact layout "
-                        f"(CompactGrid, 8 B per member), host I/O = the reference's int64 Grid",
+                        f"(CompactGrid, 8 B per member), host I/O = the reference's int64 Grid; "
+                        + ("two steps per pass over the state (ca_compact2_kernel)" if world == 1 else
+                           "one step per launch"),
             "r": r, "n": 1 << r, "rho": rho, "mode": "lambda", "cells_per_step": 3 ** r,
             "cell": "int64", "state": "compact",
             "parallelism": "1 GPU" if world == 1 else
@@ -176,7 +186,7 @@ def config_block(r, rho, world=1, transport="p2p"):
                                "halo cells read over peer memory (CUDA IPC) inside the step kernel"
                                if transport == "p2p" else
                                f"halo cells exchanged by gather + NCCL all_to_all + scatter ({transport})"),
-            "l2": "no flush: each step moves 689 MB compact / 1.7 GB embedded (> 126 MB L2)"}
+            "l2": "no flush: each pass moves 689 MB compact / 1.7 GB embedded (> 126 MB L2)"}
 
 
 # ---------------------------------------------------------------------------------
@@ -335,6 +345,7 @@ def main():
         run = compact_runner(cfg(), c1, c2)
         for _ in range(3):
             run()
+        dev.ca_compact_run_dev(cfg(), c1.data_ptr(), c2.data_ptr(), 4, nbb.CaRule(), s)  # 2 pairs
         for c in (cfg(), cfg(mode=nbb.MapMode.BoundingBox),
                   cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell)):
             run = ca_runner(c, a, b)
@@ -387,6 +398,17 @@ def main():
                                                              nbb.CaRule(), s), K, W, sampler, head_groups)
     value = members * 1e3 / head_ms  # all ranks together update the 3^r cells per step
     results["ca_lambda_compact_i64"] = head_ms
+    single = None
+    if world == 1:  # the same K steps with one launch per step (ca_compact_kernel)
+        single_ms = timed_run(lambda k: dev.ca_compact_run_dev(cfg(flags=nbb_abi.FLAG_SINGLE_STEP), c1.data_ptr(),
+                                                               c2.data_ptr(), k, nbb.CaRule(), s), K, W)
+        results["ca_lambda_compact_i64_single_step"] = single_ms
+        single = {"note": "the headline's K steps with one launch per step (ca_compact_kernel, "
+                          "NBB_FLAG_SINGLE_STEP): 8 B read + 8 B write per member and step",
+                  "ms_per_step": single_ms, "value": members * 1e3 / single_ms,
+                  "roofline": {"achieved": 16 * members / (single_ms * 1e-3) / 1e9,
+                               "frac": 16 * members / (single_ms * 1e-3) / 1e9 / measured_peaks()[0],
+                               "alg_bytes_per_launch": 16 * members}}
     # ---- C5: the same step on the gasket at n = 2^17 (BASELINE configs[4]), sharded by
     # contiguous compact tile ranges at N > 1 (halos over peer memory inside the kernel) ------
     c5 = None
@@ -410,7 +432,8 @@ def main():
                                                              nbb.CaRule(), s), K, W)
             del d2
         del d1
-        ach5 = 16 * m5 / (ms5 * 1e-3) / 1e9
+        p5, s5 = pair_launches(K) if world == 1 else (0, K)
+        ach5 = 16 * m5 * (p5 + s5) / K / (ms5 * 1e-3) / 1e9  # state bytes moved per step
         c5 = {"workload": f"C5: gasket n=2^{r5} CA step (B3/S23), compact state, rho=32 tiles, "
                           f"{world} rank(s), contiguous compact tile ranges",
               "data": "synthetic: iid alive values (torch.randint(0, 2), seed 18) over the 3^r member "
@@ -507,16 +530,18 @@ def main():
         del xy
     del c1, c2
 
-    # ---- roofline of the dominant kernel (ca_compact_kernel) ---------------------------
+    # ---- roofline of the dominant kernel (ca_compact2_kernel at N = 1) ------------------
     peak, peak_kind = measured_peaks()
-    alg_bytes = 2 * 8 * members            # read src + write dst, 8 B per member, per launch
-    achieved = alg_bytes / (head_ms * 1e-3) / 1e9
+    alg_bytes = 2 * 8 * members            # read src + write dst, 8 B per member, per launch (pass)
+    n_pairs, n_single = pair_launches(K) if world == 1 else (0, K)
+    launch_ms = head_ms * K / (n_pairs + n_single)  # average launch (pass) duration
+    achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     traffic = emb_traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
         with open(tf) as f:
             tj = json.load(f)
-        traffic = tj.get("ca_lambda_compact_i64")
+        traffic = tj.get("ca_lambda_compact2_i64" if n_pairs else "ca_lambda_compact_i64")
         emb_traffic = tj.get("ca_lambda_tile_rho32_i64")
     emb_alg = 2 * layout_bytes_per_pass(r, 8)  # 32-byte sectors holding a member, read + write
     emb_achieved = emb_alg / (emb_ms * 1e-3) / 1e9
@@ -602,11 +627,15 @@ def main():
         "data": f"synthetic: random_member_grid(gasket, {r}, seed=17, modulus=2) generated "
                 "bit-identically on device, B3/S23",
         "config": config_block(r, 32, world, args.transport),
-        "gpu_launches": K * launches_per_step,
+        "gpu_launches": (n_pairs + n_single) * launches_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
-                     "kernel": "ca_compact_kernel (8 B read + 8 B write per member cell)"},
+                     "launches": {"two_step": n_pairs, "one_step": n_single},
+                     "kernel": ("ca_compact2_kernel: two CA steps per pass, 8 B read + 8 B write per "
+                                "member cell per pass" if n_pairs else
+                                "ca_compact_kernel (8 B read + 8 B write per member cell)")},
+        "one_step_per_launch": single,
         "embedded_int64": {
             "note": "the same step on the reference's int64 embedded Grid (ca_pipe_kernel)",
             "ms_per_step": emb_ms, "value": members * 1e3 / emb_ms,

@@ -509,9 +509,15 @@ __device__ __forceinline__ uint32_t compact_rows_step(uint32_t R, uint32_t h, in
 // 22 radius-2 halo cells once, computes step t+1 for the tile (bit-sliced) and for its 8 H1
 // halo cells (lanes 0..7, scalar, from the step-t bytes), then step t+2 for the tile from those,
 // and stores step t+2 — 8 B read + 8 B write per member per TWO steps. Same tile walk, software
-// pipeline and PDL as ca_compact_kernel; the step-t+1 state never reaches HBM.
+// pipeline and PDL as ca_compact_kernel; the step-t+1 state never reaches HBM. The pass is
+// ALU-bound, so the reference's default rule (CaRule{}: B3/S23) has its own instantiation with
+// the rule masks known at compile time (the bit-sliced rule's leaves fold away); every other
+// rule runs the generic one.
+template <bool CONWAY>
 __global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, FastDiv div_hb,
                                                              const int32_t* __restrict__ halo_tab) {
+    const uint32_t birth = CONWAY ? (1u << 3) : a.birth;
+    const uint32_t survive = CONWAY ? (1u << 2) | (1u << 3) : a.survive;
     __shared__ __align__(16) uint8_t s_cell[8][32 * 32];
     __shared__ uint32_t s_new[8][32];
     __shared__ uint16_t s_pos[256];
@@ -607,17 +613,17 @@ __global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, Fa
             for (int i = 0; i < 8; ++i) R |= ((w[i] * 0x01020408u) >> 24 & 0xFu) << (4 * i);
         }
         // step t+1: the tile (bit-sliced) and the H1 cells (lane k < 8, scalar)
-        const uint32_t R1 = compact_rows_step(R, hm & 0xFFu, lane, a.birth, a.survive);
+        const uint32_t R1 = compact_rows_step(R, hm & 0xFFu, lane, birth, survive);
         uint32_t live = 0;
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
             const uint32_t c = my_code[d];
             live += (c & 0x8000u) ? 0u : (c & 0x4000u) ? (hm >> (c & 31u)) & 1u : (uint32_t)cell[c & 1023u];
         }
-        const uint32_t rule = ((hm >> (lane & 7)) & 1u) ? a.survive : a.birth;
+        const uint32_t rule = ((hm >> (lane & 7)) & 1u) ? survive : birth;
         const uint32_t h1 = __ballot_sync(0xFFFFFFFFu, lane < 8 && ((rule >> live) & 1u)) & hmem_cur;
         // step t+2: the tile only
-        s_new[wib][lane] = compact_rows_step(R1, h1, lane, a.birth, a.survive);
+        s_new[wib][lane] = compact_rows_step(R1, h1, lane, birth, survive);
         __syncwarp();
         char* dst = dst0 + base;
         base = base_n;

@@ -820,9 +820,18 @@ int launch_ca_compact2(DeviceCtx* ctx, const nbb_config* cfg, const void* src, v
     const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
     if (want == 0) return NBB_OK;
     int occ;
-    NBB_CHECK(occupancy<ca_compact2_kernel>(256, 0, &occ));
+    const bool conway = birth == (1u << 3) && survive == ((1u << 2) | (1u << 3));  // CaRule{} (B3/S23)
+    if (conway) {
+        NBB_CHECK(occupancy<ca_compact2_kernel<true>>(256, 0, &occ));
+    } else {
+        NBB_CHECK(occupancy<ca_compact2_kernel<false>>(256, 0, &occ));
+    }
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
-    NBB_CUDA(launch_pdl(ca_compact2_kernel, blocks, 256, st, a, div_hb, tab));
+    if (conway) {
+        NBB_CUDA(launch_pdl(ca_compact2_kernel<true>, blocks, 256, st, a, div_hb, tab));
+    } else {
+        NBB_CUDA(launch_pdl(ca_compact2_kernel<false>, blocks, 256, st, a, div_hb, tab));
+    }
     return NBB_OK;
 }
 

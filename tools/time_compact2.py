@@ -21,15 +21,17 @@ for r in (16, 17):
     members = 3 ** r
     a = torch.randint(0, 2, (members,), dtype=torch.int64, device="cuda")
     b = torch.empty_like(a)
-    for name, flags in (("pairs", 0), ("single", _abi.FLAG_SINGLE_STEP)):
+    highlife = nbb.CaRule(birth=(1 << 3) | (1 << 6), survive=(1 << 2) | (1 << 3))  # generic-rule kernel
+    for name, flags, rule in (("pairs", 0, nbb.CaRule()), ("pairs_generic_rule", 0, highlife),
+                              ("single", _abi.FLAG_SINGLE_STEP, nbb.CaRule())):
         c = nbb.DispatchConfig(r=r, rho=32, max_cells=(1 << r) ** 2, flags=flags)
-        dev.ca_compact_run_dev(c, a.data_ptr(), b.data_ptr(), 20, nbb.CaRule(), s)
+        dev.ca_compact_run_dev(c, a.data_ptr(), b.data_ptr(), 20, rule, s)
         torch.cuda.synchronize()
         best = 1e9
         for _ in range(5):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            dev.ca_compact_run_dev(c, a.data_ptr(), b.data_ptr(), K, nbb.CaRule(), s)
+            dev.ca_compact_run_dev(c, a.data_ptr(), b.data_ptr(), K, rule, s)
             e1.record()
             torch.cuda.synchronize()
             best = min(best, e0.elapsed_time(e1) / K)
