@@ -74,6 +74,12 @@ cfg = nbb.DispatchConfig(r=r, rho=32)
 dev.ca_compact_run_dev(cfg, ca.data_ptr(), cb.data_ptr(), 3, nbb.CaRule(), s)
 assert np.array_equal(cb.cpu().numpy(), want[cy, cx])
 checks += 1
+# two steps per pass (ca_compact2_kernel, B3/S23 and generic-rule instantiations): 4 steps = 2 pairs
+for rule in (nbb.CaRule(), nbb.CaRule(birth=(1 << 3) | (1 << 6), survive=(1 << 2) | (1 << 3))):
+    ca, cb = comp0.clone(), torch.empty_like(comp0)
+    dev.ca_compact_run_dev(cfg, ca.data_ptr(), cb.data_ptr(), 4, rule, s)
+    assert np.array_equal(ca.cpu().numpy(), orc_ca(r, g, 4, rule.birth, rule.survive)[cy, cx])
+    checks += 1
 plan = shard.ShardPlan(r=r, rho=32, world=2, rank=0, state="compact")
 ca, cb = comp0.clone(), torch.zeros_like(comp0)  # rank 0 writes only its tiles
 sync = torch.zeros(4, dtype=torch.int32, device="cuda")
