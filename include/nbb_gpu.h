@@ -284,6 +284,14 @@ typedef struct nbb_p2p {
 } nbb_p2p;
 int nbb_gpu_ca_compact_p2p_dev(const nbb_config* cfg, int64_t first_step, int32_t steps,
                                uint16_t birth, uint16_t survive, const nbb_p2p* p2p, void* stream);
+/* The same step sequence in PASSES of two steps (ca_compact2_kernel over peer memory: the
+ * radius-2 halo read once, the intermediate step kept on chip; a single-step pass last when
+ * `steps` is odd): steps / 2 + steps % 2 passes. Pass j (first_pass <= j) reads d_buf[j & 1],
+ * writes d_buf[(j + 1) & 1] and waits for world x j arrivals; first_pass must equal the number
+ * of passes (either entry point: a step of nbb_gpu_ca_compact_p2p_dev is one pass) this d_sync
+ * has already run. */
+int nbb_gpu_ca_compact_p2p_passes_dev(const nbb_config* cfg, int64_t first_pass, int32_t steps,
+                                      uint16_t birth, uint16_t survive, const nbb_p2p* p2p, void* stream);
 /* error flag of d_sync after a step sequence (synchronises the stream): 0 ok, 1 timed out */
 int nbb_gpu_p2p_check(const nbb_p2p* p2p, void* stream);
 /* device memory that can be exported (cudaMalloc: the IPC handle names the allocation) */

@@ -151,6 +151,8 @@ SIGNATURES = {
     "nbb_gpu_ca_compact_run_dev": (c_int, [CP, c_void_p, c_void_p, c_int32, c_uint16, c_uint16, c_void_p]),
     "nbb_gpu_ca_compact_p2p_dev": (c_int, [CP, ctypes.c_int64, c_int32, c_uint16, c_uint16,
                                            POINTER(NbbP2P), c_void_p]),
+    "nbb_gpu_ca_compact_p2p_passes_dev": (c_int, [CP, ctypes.c_int64, c_int32, c_uint16, c_uint16,
+                                                  POINTER(NbbP2P), c_void_p]),
     "nbb_gpu_p2p_check": (c_int, [POINTER(NbbP2P), c_void_p]),
     "nbb_gpu_malloc": (c_int, [c_int32, c_uint64, POINTER(c_void_p)]),
     "nbb_gpu_free": (c_int, [c_int32, c_void_p]),

@@ -227,6 +227,7 @@ struct P2PArgs {
     unsigned int wait_target;          // arrivals required before the step may start (world x step)
     unsigned int timeout_ms;
     int world, rank;
+    unsigned int chunk;                // tiles per rank (ca_compact2_kernel: owner = tile / chunk)
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -513,18 +514,26 @@ __device__ __forceinline__ uint32_t compact_rows_step(uint32_t R, uint32_t h, in
 // ALU-bound, so the reference's default rule (CaRule{}: B3/S23) has its own instantiation with
 // the rule masks known at compile time (the bit-sliced rule's leaves fold away); every other
 // rule runs the generic one.
-template <bool CONWAY>
+//
+// P2P = true is the multi-GPU pass (as ca_compact_kernel<true>): the halo cells of other ranks'
+// tiles are read from their buffers over NVLink, the owner computed from the compact offset
+// (tile = (row / 9) H_b + col / 27, owner = tile / chunk), and the same flag barrier orders
+// the passes (world x j arrivals before pass j).
+template <bool CONWAY, bool P2P>
 __global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, FastDiv div_hb,
-                                                             const int32_t* __restrict__ halo_tab) {
+                                                             const int32_t* __restrict__ halo_tab,
+                                                             P2PArgs p) {
     const uint32_t birth = CONWAY ? (1u << 3) : a.birth;
     const uint32_t survive = CONWAY ? (1u << 2) | (1u << 3) : a.survive;
     __shared__ __align__(16) uint8_t s_cell[8][32 * 32];
     __shared__ uint32_t s_new[8][32];
     __shared__ uint16_t s_pos[256];
     __shared__ uint16_t s_code[64];  // H1 cell k, neighbour d: tile byte | 0x4000 + halo slot | 0x8000
+    __shared__ const long long* s_peer[kMaxP2P];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint8_t* cell = s_cell[wib];
     pdl_trigger();
+    if (P2P && threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
     s_pos[threadIdx.x] = threadIdx.x < 243 ? c_local_pos[threadIdx.x] : 0;
     if (threadIdx.x < 64) {
         const int k = threadIdx.x >> 3, d = threadIdx.x & 7;
@@ -539,7 +548,11 @@ __global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, Fa
         }
         s_code[threadIdx.x] = code;
     }
-    pdl_wait();
+    if (P2P && p.wait_target != 0u) {  // the arrival wait subsumes pdl_wait (ca_compact_kernel)
+        if (threadIdx.x == 0) p2p_wait(p);
+    } else {
+        pdl_wait();
+    }
     __syncthreads();
     uint32_t sl_off[8], sl_pos[8];
 #pragma unroll
@@ -574,6 +587,21 @@ __global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, Fa
     auto halo_entry = [&](uint32_t t) -> int32_t {
         return (t < a.tile_end && lane < kHalo2) ? __ldg(halo_tab + (uint64_t)kHalo2Stride * t + lane) : -1;
     };
+    auto load_halo = [&](int32_t off) -> long long {
+        long long hv = 0;
+        if (off >= 0) {
+            uint32_t own = 0;
+            if (P2P) {
+                const uint32_t row = (uint32_t)off / a.W, col = (uint32_t)off - row * a.W;
+                own = ((row / 9u) * a.Hb + col / 27u) / p.chunk;
+            }
+            if (!P2P || own == (uint32_t)p.rank)
+                hv = __ldg(a.src + off);
+            else  // a cell of another rank's tile: read its buffer over NVLink
+                asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(hv) : "l"(s_peer[own] + off));
+        }
+        return hv;
+    };
 
     uint32_t u = a.tile_begin + warp_global;
     uint64_t base = 0;
@@ -584,7 +612,7 @@ __global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, Fa
         base = tile_base(u);
         load_tile(base);
         const int32_t off = halo_entry(u);
-        hv = off >= 0 ? __ldg(a.src + off) : 0ll;
+        hv = load_halo(off);
         hmem = __ballot_sync(0xFFFFFFFFu, off >= 0) & 0xFFu;
         hoff_n = halo_entry(u + warp_stride);
     }
@@ -599,7 +627,7 @@ __global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, Fa
         if (un < a.tile_end) {  // warp-uniform
             base_n = tile_base(un);
             load_tile(base_n);
-            hv = hoff_n >= 0 ? __ldg(a.src + hoff_n) : 0ll;
+            hv = load_halo(hoff_n);
             hmem = __ballot_sync(0xFFFFFFFFu, hoff_n >= 0) & 0xFFu;
             hoff_n = halo_entry(un + warp_stride);
         }
@@ -636,6 +664,7 @@ __global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, Fa
                 (long long)((s_new[wib][sl_pos[7] >> 5] >> (sl_pos[7] & 31u)) & 1u);
         __syncwarp();
     }
+    if (P2P) p2p_arrive(p);
 }
 
 // The BOUNDING-BOX launch of the compact-state CA step (the comparison for ca_compact_kernel on

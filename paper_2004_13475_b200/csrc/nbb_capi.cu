@@ -822,15 +822,15 @@ int launch_ca_compact2(DeviceCtx* ctx, const nbb_config* cfg, const void* src, v
     int occ;
     const bool conway = birth == (1u << 3) && survive == ((1u << 2) | (1u << 3));  // CaRule{} (B3/S23)
     if (conway) {
-        NBB_CHECK(occupancy<ca_compact2_kernel<true>>(256, 0, &occ));
+        NBB_CHECK(occupancy<ca_compact2_kernel<true, false>>(256, 0, &occ));
     } else {
-        NBB_CHECK(occupancy<ca_compact2_kernel<false>>(256, 0, &occ));
+        NBB_CHECK(occupancy<ca_compact2_kernel<false, false>>(256, 0, &occ));
     }
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
     if (conway) {
-        NBB_CUDA(launch_pdl(ca_compact2_kernel<true>, blocks, 256, st, a, div_hb, tab));
+        NBB_CUDA(launch_pdl(ca_compact2_kernel<true, false>, blocks, 256, st, a, div_hb, tab, P2PArgs{}));
     } else {
-        NBB_CUDA(launch_pdl(ca_compact2_kernel<false>, blocks, 256, st, a, div_hb, tab));
+        NBB_CUDA(launch_pdl(ca_compact2_kernel<false, false>, blocks, 256, st, a, div_hb, tab, P2PArgs{}));
     }
     return NBB_OK;
 }
@@ -854,6 +854,72 @@ int run_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, void* d_a, void* d_b, 
         NBB_CHECK(launch_ca_compact2(ctx, cfg, src(), dst(), birth, survive, st));
     for (int32_t i = 2 * pairs; i < steps; ++i, ++launches)
         NBB_CHECK(launch_ca_compact(ctx, cfg, src(), dst(), birth, survive, st));
+    return NBB_OK;
+}
+// The multi-GPU step loop: `steps` steps as passes j = first_pass, first_pass + 1, ... (two
+// steps per pass when `pairs`, the last pass single when `steps` is odd; one step per pass
+// otherwise). Pass j reads d_buf[j & 1], writes d_buf[(j + 1) & 1] and waits for world x j
+// arrivals.
+int p2p_passes(const nbb_config* cfg, int64_t first_pass, int32_t steps, bool pairs, uint16_t birth,
+               uint16_t survive, const nbb_p2p* p2p, cudaStream_t stream) {
+    if (!cfg || !p2p) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    if (steps < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "run_ca: steps must be non-negative");
+    if (first_pass < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: first_step must be non-negative");
+    NBB_CHECK(compact_workload_check(cfg));
+    if (p2p->world < 1 || p2p->world > kMaxP2P || p2p->rank < 0 || p2p->rank >= p2p->world)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: need 1 <= world <= 8 and 0 <= rank < world");
+    if (!p2p->d_buf[0] || !p2p->d_buf[1] || !p2p->d_peer_buf[0] || !p2p->d_peer_buf[1] ||
+        !p2p->d_halo_owner || !p2p->d_sync || !p2p->d_peer_flag)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: null device array");
+    DeviceCtx* ctx;
+    NBB_CHECK(ensure_device(cfg->device, &ctx));
+    FastDiv div_hb;
+    CompactCaArgs a = compact_args(cfg, p2p->d_buf[0], p2p->d_buf[1], birth, survive, &div_hb);
+    const int32_t *tab, *tab2 = nullptr;
+    NBB_CHECK(compact_halo_table(ctx, cfg, a, div_hb, &tab));
+    if (pairs && steps >= 2) NBB_CHECK(compact_halo2_table(ctx, cfg, a, div_hb, &tab2));
+    P2PArgs p;
+    p.halo_owner = (const uint8_t*)p2p->d_halo_owner;
+    p.sync = (unsigned int*)p2p->d_sync;
+    p.peer_flag = (unsigned int* const*)p2p->d_peer_flag;
+    p.timeout_ms = p2p->timeout_ms ? p2p->timeout_ms : 20000u;
+    p.world = p2p->world;
+    p.rank = p2p->rank;
+    p.chunk = (a.tiles + (uint32_t)p2p->world - 1) / (uint32_t)p2p->world;  // the shard split
+    const bool conway = birth == (1u << 3) && survive == ((1u << 2) | (1u << 3));
+    int occ1, occ2;
+    NBB_CHECK(occupancy<ca_compact_kernel<true>>(256, 0, &occ1));
+    if (conway) {
+        NBB_CHECK(occupancy<ca_compact2_kernel<true, true>>(256, 0, &occ2));
+    } else {
+        NBB_CHECK(occupancy<ca_compact2_kernel<false, true>>(256, 0, &occ2));
+    }
+    // every rank launches (and arrives) even with an empty shard: one CTA at least; at most one
+    // resident wave, so CTAs spinning in the wait never keep a CTA of the same pass off an SM
+    const uint64_t want = std::max<uint64_t>(1, (a.tile_end - a.tile_begin + 7) / 8);
+    const unsigned blocks1 = (unsigned)std::min<uint64_t>(want, (uint64_t)ctx->sms * occ1);
+    const unsigned blocks2 = (unsigned)std::min<uint64_t>(want, (uint64_t)ctx->sms * occ2);
+    // the pass loop lives here, not in the caller: back to back on the stream, no per-pass host
+    // arguments beyond the ping-pong parity
+    int64_t j = first_pass;
+    for (int32_t left = steps; left > 0; ++j) {
+        const int par = (int)(j & 1);
+        a.src = (const long long*)p2p->d_buf[par];
+        a.dst = (long long*)p2p->d_buf[par ^ 1];
+        p.peer_src = (const long long* const*)p2p->d_peer_buf[par];
+        p.wait_target = (unsigned int)((uint64_t)p2p->world * (uint64_t)j);
+        if (pairs && left >= 2) {
+            if (conway) {
+                NBB_CUDA(launch_pdl(ca_compact2_kernel<true, true>, blocks2, 256, stream, a, div_hb, tab2, p));
+            } else {
+                NBB_CUDA(launch_pdl(ca_compact2_kernel<false, true>, blocks2, 256, stream, a, div_hb, tab2, p));
+            }
+            left -= 2;
+        } else {
+            NBB_CUDA(launch_pdl(ca_compact_kernel<true>, blocks1, 256, stream, a, div_hb, tab, p));
+            left -= 1;
+        }
+    }
     return NBB_OK;
 }
 }  // namespace
@@ -1499,45 +1565,12 @@ int nbb_gpu_ca_compact_run_dev(const nbb_config* cfg, void* d_a, void* d_b, int3
 
 int nbb_gpu_ca_compact_p2p_dev(const nbb_config* cfg, int64_t first_step, int32_t steps, uint16_t birth,
                                uint16_t survive, const nbb_p2p* p2p, void* stream) {
-    if (!cfg || !p2p) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
-    if (steps < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "run_ca: steps must be non-negative");
-    if (first_step < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: first_step must be non-negative");
-    NBB_CHECK(compact_workload_check(cfg));
-    if (p2p->world < 1 || p2p->world > kMaxP2P || p2p->rank < 0 || p2p->rank >= p2p->world)
-        return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: need 1 <= world <= 8 and 0 <= rank < world");
-    if (!p2p->d_buf[0] || !p2p->d_buf[1] || !p2p->d_peer_buf[0] || !p2p->d_peer_buf[1] ||
-        !p2p->d_halo_owner || !p2p->d_sync || !p2p->d_peer_flag)
-        return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: null device array");
-    DeviceCtx* ctx;
-    NBB_CHECK(ensure_device(cfg->device, &ctx));
-    FastDiv div_hb;
-    CompactCaArgs a = compact_args(cfg, p2p->d_buf[0], p2p->d_buf[1], birth, survive, &div_hb);
-    const int32_t* tab;
-    NBB_CHECK(compact_halo_table(ctx, cfg, a, div_hb, &tab));
-    P2PArgs p;
-    p.halo_owner = (const uint8_t*)p2p->d_halo_owner;
-    p.sync = (unsigned int*)p2p->d_sync;
-    p.peer_flag = (unsigned int* const*)p2p->d_peer_flag;
-    p.timeout_ms = p2p->timeout_ms ? p2p->timeout_ms : 20000u;
-    p.world = p2p->world;
-    p.rank = p2p->rank;
-    int occ;
-    NBB_CHECK(occupancy<ca_compact_kernel<true>>(256, 0, &occ));
-    // every rank launches (and arrives) even with an empty shard: one CTA at least; at most one
-    // resident wave, so CTAs spinning in the wait never keep a CTA of the same step off an SM
-    const uint64_t want = std::max<uint64_t>(1, (a.tile_end - a.tile_begin + 7) / 8);
-    const unsigned blocks = (unsigned)std::min<uint64_t>(want, (uint64_t)ctx->sms * occ);
-    // the step loop lives here, not in the caller: one launch per step, back to back on the
-    // stream, no per-step host arguments beyond the ping-pong parity
-    for (int64_t i = first_step; i < first_step + steps; ++i) {
-        const int par = (int)(i & 1);
-        a.src = (const long long*)p2p->d_buf[par];
-        a.dst = (long long*)p2p->d_buf[par ^ 1];
-        p.peer_src = (const long long* const*)p2p->d_peer_buf[par];
-        p.wait_target = (unsigned int)((uint64_t)p2p->world * (uint64_t)i);
-        NBB_CUDA(launch_pdl(ca_compact_kernel<true>, blocks, 256, (cudaStream_t)stream, a, div_hb, tab, p));
-    }
-    return NBB_OK;
+    return p2p_passes(cfg, first_step, steps, false, birth, survive, p2p, (cudaStream_t)stream);
+}
+
+int nbb_gpu_ca_compact_p2p_passes_dev(const nbb_config* cfg, int64_t first_pass, int32_t steps, uint16_t birth,
+                                      uint16_t survive, const nbb_p2p* p2p, void* stream) {
+    return p2p_passes(cfg, first_pass, steps, true, birth, survive, p2p, (cudaStream_t)stream);
 }
 
 int nbb_gpu_p2p_check(const nbb_p2p* p2p, void* stream) {

@@ -352,7 +352,8 @@ class P2PCompactCA:
     no collective inside the step loop; the NCCL `exchange_halo` path is the baseline.
     """
 
-    def __init__(self, plan: ShardPlan, dist, device: int = 0, timeout_ms: int = 20000):
+    def __init__(self, plan: ShardPlan, dist, device: int = 0, timeout_ms: int = 20000,
+                 two_step: bool = True):
         import ctypes
         import torch
         from . import _abi
@@ -361,6 +362,7 @@ class P2PCompactCA:
         if plan.world > 8:
             raise ValueError("P2PCompactCA supports up to 8 ranks")
         self.plan, self.device, self.timeout_ms, self.dist = plan, device, timeout_ms, dist
+        self.two_step = two_step  # passes of two steps (ca_compact2_kernel) vs one launch per step
         self.lib = lib = _abi.load()
         self.count = 3 ** plan.r
         nbytes = self.count * 8
@@ -419,6 +421,7 @@ class P2PCompactCA:
                                  self._owner.data_ptr(), self._own[2], self._peer_flag.data_ptr(),
                                  timeout_ms)
         self.step_index = 0
+        self.pass_index = 0  # passes (launches) run so far: the state lives in buffer pass_index & 1
 
     def load(self, compact_state) -> None:
         """Set the state (a (3^r,) int64 tensor; this rank's tiles must be current). Collective:
@@ -433,16 +436,19 @@ class P2PCompactCA:
 
     def state(self):
         """The current state buffer (this rank's tiles are current)."""
-        return self.buffers[self.step_index & 1]
+        return self.buffers[self.pass_index & 1]
 
     def run(self, config, rule, steps: int, stream) -> None:
-        """`steps` steps, one kernel per step issued back to back by the library."""
+        """`steps` steps issued back to back by the library: passes of two steps (the last one
+        single for odd `steps`), or one kernel per step with two_step=False."""
         import ctypes
         c = self.plan.local_config(config).to_c()
-        _check(self.lib.nbb_gpu_ca_compact_p2p_dev(
-            ctypes.byref(c), self.step_index, steps, rule.birth, rule.survive,
-            ctypes.byref(self._args), ctypes.c_void_p(stream)))
+        fn = (self.lib.nbb_gpu_ca_compact_p2p_passes_dev if self.two_step
+              else self.lib.nbb_gpu_ca_compact_p2p_dev)
+        _check(fn(ctypes.byref(c), self.pass_index, steps, rule.birth, rule.survive,
+                  ctypes.byref(self._args), ctypes.c_void_p(stream)))
         self.step_index += steps
+        self.pass_index += (steps // 2 + steps % 2) if self.two_step else steps
 
     def step(self, config, rule, stream) -> None:
         self.run(config, rule, 1, stream)

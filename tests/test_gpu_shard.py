@@ -90,7 +90,7 @@ def test_sharded_ca_on_gpu(world, r, rho, cw):
     assert np.array_equal(got, want)
 
 
-def _p2p_worker(rank, world, port, r, steps, q):
+def _p2p_worker(rank, world, port, r, steps, q, mode="step", birth=8, survive=12):
     """The P2P compact CA: ranks on one B200 share buffers through CUDA IPC mappings."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -105,12 +105,17 @@ def _p2p_worker(rank, world, port, r, steps, q):
     own = torch.from_numpy(plan.owner(tile) == rank)
     init = torch.from_numpy(orc_random_member_grid(r, 4321, 2)[cy, cx].copy())
     init[~own] = 7  # only this rank's tiles are trusted: remote cells must come from peers
-    ca = P2PCompactCA(plan, dist, device=0, timeout_ms=60000)
+    ca = P2PCompactCA(plan, dist, device=0, timeout_ms=60000, two_step=(mode == "passes"))
     ca.load(init)
     c = nbb.DispatchConfig(r=r, rho=32, max_cells=n * n)
     s = torch.cuda.current_stream().cuda_stream
-    for _ in range(steps):
-        ca.step(c, nbb.CaRule(), s)
+    rule = nbb.CaRule(birth=birth, survive=survive)
+    if mode == "step":  # one call per step
+        for _ in range(steps):
+            ca.step(c, rule, s)
+    else:  # two calls: the pass parity and arrival targets carry across calls
+        ca.run(c, rule, steps // 2 + 1, s)
+        ca.run(c, rule, steps - steps // 2 - 1, s)
     ca.check(s)
     out = ca.state().cpu()
     mine_c = torch.where(own, out, torch.zeros_like(out))
@@ -123,20 +128,25 @@ def _p2p_worker(rank, world, port, r, steps, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,r", [(2, 10), (3, 11), (4, 12)])
-def test_p2p_compact_ca_on_gpu(world, r):
+@pytest.mark.parametrize("world,r,mode,steps,rule", [
+    (2, 10, "step", 6, (8, 12)), (3, 11, "step", 6, (8, 12)), (4, 12, "step", 6, (8, 12)),
+    # passes of two steps (ca_compact2_kernel over peer memory), odd and even step counts,
+    # the B3/S23 and the generic-rule instantiations
+    (2, 10, "passes", 7, (8, 12)), (3, 11, "passes", 6, (8, 12)), (4, 12, "passes", 9, (8, 12)),
+    (3, 10, "passes", 8, (72, 12)), (2, 12, "single", 5, (8, 12))])
+def test_p2p_compact_ca_on_gpu(world, r, mode, steps, rule):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    steps = 6
-    procs = [ctx.Process(target=_p2p_worker, args=(i, world, port, r, steps, q)) for i in range(world)]
+    procs = [ctx.Process(target=_p2p_worker, args=(i, world, port, r, steps, q, mode, *rule))
+             for i in range(world)]
     for p in procs:
         p.start()
     got = q.get(timeout=600)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    want = orc_ca(r, orc_random_member_grid(r, 4321, 2), steps)
+    want = orc_ca(r, orc_random_member_grid(r, 4321, 2), steps, *rule)
     assert np.array_equal(got, want)
 
 
