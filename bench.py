@@ -165,9 +165,12 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
-def pair_launches(k):
-    """Launches of nbb_gpu_ca_compact_run_dev for k steps: pairs (two steps per pass, an even
-    number of them) + single steps (nbb_capi.cu run_ca_compact)."""
+def pair_launches(k, world=1, transport="p2p"):
+    """(two-step, one-step) launches for k steps: nbb_gpu_ca_compact_run_dev at N = 1 (an even
+    number of pairs, nbb_capi.cu run_ca_compact), nbb_gpu_ca_compact_p2p_passes_dev at N > 1
+    (k // 2 pairs + k % 2), one launch per step with the NCCL exchange."""
+    if world > 1:
+        return (k // 2, k % 2) if transport == "p2p" else (0, k)
     pairs = k // 2
     pairs -= pairs & 1
     return pairs, k - 2 * pairs
@@ -177,8 +180,8 @@ def config_block(r, rho, world=1, transport="p2p"):
     return {"workload": f"C3: gasket n=2^{r} cellular-automaton step (B3/S23), lambda(omega) launch, "
                         f"rho={rho} tiles; device state = the lambda-ordered compact layout "
                         f"(CompactGrid, 8 B per member), host I/O = the reference's int64 Grid; "
-                        + ("two steps per pass over the state (ca_compact2_kernel)" if world == 1 else
-                           "one step per launch"),
+                        + ("two steps per pass over the state (ca_compact2_kernel)"
+                           if world == 1 or transport == "p2p" else "one step per launch"),
             "r": r, "n": 1 << r, "rho": rho, "mode": "lambda", "cells_per_step": 3 ** r,
             "cell": "int64", "state": "compact",
             "parallelism": "1 GPU" if world == 1 else
@@ -440,7 +443,7 @@ def main():
                                                              nbb.CaRule(), s), K, W)
             del d2
         del d1
-        p5, s5 = pair_launches(K) if world == 1 else (0, K)
+        p5, s5 = pair_launches(K, world, args.transport)
         ach5 = 16 * m5 * (p5 + s5) / K / (ms5 * 1e-3) / 1e9  # state bytes moved per step
         c5 = {"workload": f"C5: gasket n=2^{r5} CA step (B3/S23), compact state, rho=32 tiles, "
                           f"{world} rank(s), contiguous compact tile ranges",
@@ -541,7 +544,7 @@ def main():
     # ---- roofline of the dominant kernel (ca_compact2_kernel at N = 1) ------------------
     peak, peak_kind = measured_peaks()
     alg_bytes = 2 * 8 * members            # read src + write dst, 8 B per member, per launch (pass)
-    n_pairs, n_single = pair_launches(K) if world == 1 else (0, K)
+    n_pairs, n_single = pair_launches(K, world, args.transport)
     launch_ms = head_ms * K / (n_pairs + n_single)  # average launch (pass) duration
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     traffic = emb_traffic = None

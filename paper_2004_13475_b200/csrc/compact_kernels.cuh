@@ -228,6 +228,7 @@ struct P2PArgs {
     unsigned int timeout_ms;
     int world, rank;
     unsigned int chunk;                // tiles per rank (ca_compact2_kernel: owner = tile / chunk)
+    unsigned int own_lo, own_hi;       // compact offsets [lo, hi) inside this rank's whole tile rows
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -590,8 +591,8 @@ __global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, Fa
     auto load_halo = [&](int32_t off) -> long long {
         long long hv = 0;
         if (off >= 0) {
-            uint32_t own = 0;
-            if (P2P) {
+            uint32_t own = (uint32_t)p.rank;
+            if (P2P && ((uint32_t)off < p.own_lo || (uint32_t)off >= p.own_hi)) {  // not surely ours
                 const uint32_t row = (uint32_t)off / a.W, col = (uint32_t)off - row * a.W;
                 own = ((row / 9u) * a.Hb + col / 27u) / p.chunk;
             }

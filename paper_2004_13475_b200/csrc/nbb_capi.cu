@@ -886,6 +886,11 @@ int p2p_passes(const nbb_config* cfg, int64_t first_pass, int32_t steps, bool pa
     p.world = p2p->world;
     p.rank = p2p->rank;
     p.chunk = (a.tiles + (uint32_t)p2p->world - 1) / (uint32_t)p2p->world;  // the shard split
+    {   // the rank's whole tile rows (9 compact rows of W each): offsets there are its own
+        const uint32_t fr = (a.tile_begin + a.Hb - 1) / a.Hb, fe = a.tile_end / a.Hb;
+        p.own_lo = fe > fr ? fr * 9u * a.W : 0u;
+        p.own_hi = fe > fr ? fe * 9u * a.W : 0u;
+    }
     const bool conway = birth == (1u << 3) && survive == ((1u << 2) | (1u << 3));
     int occ1, occ2;
     NBB_CHECK(occupancy<ca_compact_kernel<true>>(256, 0, &occ1));

@@ -9,7 +9,9 @@ dispatch.cpp:419-427) is stepped K times back to back by the library's C++ step 
           buffers and flags = ours, N arrivals per step): the interior/boundary phases, the
           wait / arrive protocol and the remote-halo path all run; what a real N-GPU run adds
           is NVLink latency on the remote halo loads and the arrivals.
-Prints one JSON line; ms per step = CUDA-event time / K.
+Both for one launch per step (`*_ms`) and for passes of two steps (`*_two_step_ms`:
+ca_compact2_kernel / nbb_gpu_ca_compact_p2p_passes_dev). Prints one JSON line; ms per step =
+CUDA-event time / K.
 """
 import ctypes
 import json
@@ -50,7 +52,10 @@ for r in (16, 17):
     for N in (1, 2, 4, 8):
         plan = shard.ShardPlan(r=r, rho=32, world=N, rank=0, state="compact")
         lc = plan.local_config(base)
-        t_plain = timed(lambda k: dev.ca_compact_run_dev(lc, c1.data_ptr(), c2.data_ptr(), k, nbb.CaRule(), s))
+        lc1 = plan.local_config(nbb.DispatchConfig(r=r, rho=32, max_cells=(1 << r) ** 2,
+                                                   flags=_abi.FLAG_SINGLE_STEP))
+        t_plain = timed(lambda k: dev.ca_compact_run_dev(lc1, c1.data_ptr(), c2.data_ptr(), k, nbb.CaRule(), s))
+        t_plain2 = timed(lambda k: dev.ca_compact_run_dev(lc, c1.data_ptr(), c2.data_ptr(), k, nbb.CaRule(), s))
 
         sync = torch.zeros(4, dtype=torch.int32, device="cuda")
         # every "peer" is this process: N entries pointing at our own buffers and sync word, so
@@ -69,16 +74,26 @@ for r in (16, 17):
                                                 ctypes.c_void_p(s))
             assert rc == 0, lib.nbb_gpu_last_error()
             st["i"] += k
+
+        def p2p2(k):  # passes of two steps (k even here)
+            rc = lib.nbb_gpu_ca_compact_p2p_passes_dev(ctypes.byref(cc), st["i"], k, 8, 12,
+                                                       ctypes.byref(args), ctypes.c_void_p(s))
+            assert rc == 0, lib.nbb_gpu_last_error()
+            st["i"] += k // 2 + k % 2
         t_p2p = timed(p2p)
+        t_p2p2 = timed(p2p2)
         torch.cuda.synchronize()
         assert int(sync[2].item()) == 0, "a wait timed out"
         assert int(sync[0].item()) == N * st["i"], (int(sync[0].item()), st["i"])
-        out[f"r{r}_N{N}"] = {"tiles": plan.count, "plain_ms": t_plain, "p2p_world1_ms": t_p2p}
+        out[f"r{r}_N{N}"] = {"tiles": plan.count, "plain_ms": t_plain, "p2p_world1_ms": t_p2p,
+                             "plain_two_step_ms": t_plain2, "p2p_world1_two_step_ms": t_p2p2}
     one = out[f"r{r}_N1"]["plain_ms"]
+    one2 = out[f"r{r}_N1"]["plain_two_step_ms"]
     for N in (1, 2, 4, 8):
         d = out[f"r{r}_N{N}"]
         d["ideal_ms"] = one / N
         d["efficiency_plain"] = one / N / d["plain_ms"]
         d["efficiency_p2p_world1"] = one / N / d["p2p_world1_ms"]
+        d["efficiency_p2p_world1_two_step"] = one2 / N / d["p2p_world1_two_step_ms"]
     del c1, c2
 print(json.dumps(out))
