@@ -425,13 +425,13 @@ __global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, Fas
             halo_entry(un + warp_stride, hoff_n, hown_n);
         }
         __syncwarp();
-        uint32_t R = 0;
-        {
+        uint32_t R;
+        {   // 0/1 bytes -> bits (as in ca_compact2_kernel)
             const uint4 q0 = reinterpret_cast<const uint4*>(cell + 32 * lane)[0];
             const uint4 q1 = reinterpret_cast<const uint4*>(cell + 32 * lane)[1];
-            const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-#pragma unroll
-            for (int i = 0; i < 8; ++i) R |= ((w[i] * 0x01020408u) >> 24 & 0xFu) << (4 * i);
+            const uint32_t p0 = (q0.x + (q0.y << 4)) * 0x01020408u, p1 = (q0.z + (q0.w << 4)) * 0x01020408u;
+            const uint32_t p2 = (q1.x + (q1.y << 4)) * 0x01020408u, p3 = (q1.z + (q1.w << 4)) * 0x01020408u;
+            R = __byte_perm(__byte_perm(p0, p1, 0x0073u), __byte_perm(p2, p3, 0x0073u), 0x5410u);
         }
         uint64_t E = (uint64_t)R << 1;
         if (lane == 31) E |= ((h >> 3) & 1u) | ((uint64_t)((h >> 5) & 1u) << 33);
@@ -796,13 +796,13 @@ __global__ void __launch_bounds__(256, 3) ca_compact_bb_kernel(CompactCaArgs a, 
             halo_entry(bnn < boxes ? u_next : a.tile_end, hoff_n, hown_n);
         }
         __syncwarp();
-        uint32_t R = 0;
-        {
+        uint32_t R;
+        {   // 0/1 bytes -> bits (as in ca_compact2_kernel)
             const uint4 q0 = reinterpret_cast<const uint4*>(cell + 32 * lane)[0];
             const uint4 q1 = reinterpret_cast<const uint4*>(cell + 32 * lane)[1];
-            const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-#pragma unroll
-            for (int i = 0; i < 8; ++i) R |= ((w[i] * 0x01020408u) >> 24 & 0xFu) << (4 * i);
+            const uint32_t p0 = (q0.x + (q0.y << 4)) * 0x01020408u, p1 = (q0.z + (q0.w << 4)) * 0x01020408u;
+            const uint32_t p2 = (q1.x + (q1.y << 4)) * 0x01020408u, p3 = (q1.z + (q1.w << 4)) * 0x01020408u;
+            R = __byte_perm(__byte_perm(p0, p1, 0x0073u), __byte_perm(p2, p3, 0x0073u), 0x5410u);
         }
         uint64_t E = (uint64_t)R << 1;
         if (lane == 31) E |= ((h >> 3) & 1u) | ((uint64_t)((h >> 5) & 1u) << 33);
