@@ -529,25 +529,32 @@ __global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, Fa
     __shared__ __align__(16) uint8_t s_cell[8][32 * 32];
     __shared__ uint32_t s_new[8][32];
     __shared__ uint16_t s_pos[256];
-    __shared__ uint16_t s_code[64];  // H1 cell k, neighbour d: tile byte | 0x4000 + halo slot | 0x8000
+    // H1 cell k's neighbours: the halo slots among them (bit mask over the 22) and its <= 3
+    // in-tile positions (byte index; padded with byte 1 = cell (1, 0), never a member, always 0)
+    __shared__ uint32_t s_nb[8];
+    __shared__ __align__(8) uint16_t s_nt[8][4];
     __shared__ const long long* s_peer[kMaxP2P];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint8_t* cell = s_cell[wib];
     pdl_trigger();
     if (P2P && threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
     s_pos[threadIdx.x] = threadIdx.x < 243 ? c_local_pos[threadIdx.x] : 0;
-    if (threadIdx.x < 64) {
-        const int k = threadIdx.x >> 3, d = threadIdx.x & 7;
-        const int dd = d < 4 ? d : d + 1;  // the 8 neighbours of the 3 x 3 block, centre skipped
-        const int qx = c_h2x[k] + dd % 3 - 1, qy = c_h2y[k] + dd / 3 - 1;
-        uint16_t code = 0x8000u;
-        if (qx >= 0 && qx < 32 && qy >= 0 && qy < 32) {
-            code = (uint16_t)(qy * 32 + qx);
-        } else {
-            for (int j = 0; j < kHalo2; ++j)
-                if (c_h2x[j] == qx && c_h2y[j] == qy) code = (uint16_t)(0x4000u | j);
+    if (threadIdx.x < 8) {
+        const int k = threadIdx.x;
+        uint32_t nb = 0;
+        int nt = 0;
+        for (int i = 0; i < 4; ++i) s_nt[k][i] = 1;
+        for (int dd = 0; dd < 9; ++dd) {  // the 8 neighbours of the 3 x 3 block, centre skipped
+            if (dd == 4) continue;
+            const int qx = c_h2x[k] + dd % 3 - 1, qy = c_h2y[k] + dd / 3 - 1;
+            if (qx >= 0 && qx < 32 && qy >= 0 && qy < 32) {
+                if (nt < 4) s_nt[k][nt++] = (uint16_t)(qy * 32 + qx);
+            } else {
+                for (int j = 0; j < kHalo2; ++j)
+                    if (c_h2x[j] == qx && c_h2y[j] == qy) nb |= 1u << j;
+            }
         }
-        s_code[threadIdx.x] = code;
+        s_nb[k] = nb;
     }
     if (P2P && p.wait_target != 0u) {  // the arrival wait subsumes pdl_wait (ca_compact_kernel)
         if (threadIdx.x == 0) p2p_wait(p);
@@ -564,7 +571,6 @@ __global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, Fa
         sl_off[k] = (row * a.W + col) * 8u;
         sl_pos[k] = s_pos[li];
     }
-    const uint16_t* my_code = s_code + (lane & 7) * 8;
     const bool k7 = lane < 19;
 #pragma unroll
     for (int i = 0; i < 8; ++i) reinterpret_cast<uint32_t*>(cell)[32 * i + lane] = 0u;
@@ -644,11 +650,10 @@ __global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, Fa
         }
         // step t+1: the tile (bit-sliced) and the H1 cells (lane k < 8, scalar)
         const uint32_t R1 = compact_rows_step(R, hm & 0xFFu, lane, birth, survive);
-        uint32_t live = 0;
-#pragma unroll
-        for (int d = 0; d < 8; ++d) {
-            const uint32_t c = my_code[d];
-            live += (c & 0x8000u) ? 0u : (c & 0x4000u) ? (hm >> (c & 31u)) & 1u : (uint32_t)cell[c & 1023u];
+        uint32_t live;
+        {
+            const uint2 t = *reinterpret_cast<const uint2*>(s_nt[lane & 7]);
+            live = __popc(hm & s_nb[lane & 7]) + cell[t.x & 0xFFFFu] + cell[t.x >> 16] + cell[t.y & 0xFFFFu];
         }
         const uint32_t rule = ((hm >> (lane & 7)) & 1u) ? survive : birth;
         const uint32_t h1 = __ballot_sync(0xFFFFFFFFu, lane < 8 && ((rule >> live) & 1u)) & hmem_cur;
