@@ -626,13 +626,14 @@ def test_device_functor_launch(rho, mode):
     assert int(f[7]) == 3 ** r  # active threads = the members (closed-form counters)
 
 
-def test_host_buffer_compact_ca_pinned_zero_copy():
+@pytest.mark.parametrize("steps", [3, 4, 9])
+def test_host_buffer_compact_ca_pinned_zero_copy(steps):
     """nbb_gpu_ca on pinned host Grids with FLAG_OUT_ZEROED | FLAG_COMPACT_STATE: member sectors
     read and written zero-copy (the e2e path of the bench) — bit-exact with the oracle at
-    n = 2^13, twice (cached device buffers)."""
+    n = 2^13, twice (cached device buffers); 4 and 9 steps run two-step passes."""
     import ctypes
     import torch
-    r, steps = 13, 3
+    r = 13
     n = 1 << r
     g = orc_random_member_grid(r, 2024, 2)
     want = orc_ca(r, g, steps)
