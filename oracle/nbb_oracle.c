@@ -311,6 +311,145 @@ int64_t orc_ca_compact_check(const nbb_spec* spec, int r, const int64_t* src, co
     return bad;
 }
 
+/* λ and λ⁻¹ of the gasket (k = 3, s = 2, offsets (0,0) (0,1) (1,1)): the digit loops of
+ * block_map.cpp:77-111 / :113-148 with the spec's constants folded in (same arithmetic as
+ * orc_lambda_map / orc_lambda_inverse, which test_oracle.py pins to the reference). */
+static void gasket_lambda(int level, int64_t ox64, int64_t oy64, int64_t* x, int64_t* y) {
+    static const int tx[3] = {0, 0, 1}, ty[3] = {0, 1, 1};
+    uint32_t ox = (uint32_t)ox64, oy = (uint32_t)oy64;  /* < 3^10 for level <= 20 */
+    int64_t px = 0, py = 0;
+    for (int mu = 1; mu <= level; ++mu) {
+        int beta;
+        if (mu & 1) {
+            beta = (int)(ox % 3);
+            ox /= 3;
+        } else {
+            beta = (int)(oy % 3);
+            oy /= 3;
+        }
+        px += (int64_t)tx[beta] << (mu - 1);
+        py += (int64_t)ty[beta] << (mu - 1);
+    }
+    *x = px;
+    *y = py;
+}
+
+static void gasket_lambda_inverse(int level, int64_t x, int64_t y, int64_t* ox, int64_t* oy) {
+    int64_t wx = 0, wy = 0, dx = 1, dy = 1;
+    for (int mu = 1; mu <= level; ++mu) {  /* digit of level mu: replica (bit_x, bit_y) */
+        const int bx = (int)((x >> (mu - 1)) & 1), by = (int)((y >> (mu - 1)) & 1);
+        const int beta = bx + by;           /* (0,0) -> 0, (0,1) -> 1, (1,1) -> 2 */
+        if (mu & 1) {
+            wx += beta * dx;
+            dx *= 3;
+        } else {
+            wy += beta * dy;
+            dy *= 3;
+        }
+    }
+    *ox = wx;
+    *oy = wy;
+}
+
+/* ---- whole-trajectory checker on the compact state (full-size C3 / C5 parity) ---------------
+ * random_member_grid (dispatch.cpp:133-149) written straight into compact order: the reference
+ * walks the n x n grid row-major and draws rng() % modulus for each member cell; for the gasket
+ * the members of row y are the submasks x of y, visited in increasing order by x = (x - y) & y
+ * (SURVEY App. A.3). Each value lands at the cell's compact offset ωy·W + ωx, ω = λ⁻¹(x, y)
+ * (block_map.cpp:113-148), i.e. CompactGrid of the reference's Grid (block_map.cpp:245-263). */
+int orc_random_member_compact(const nbb_spec* spec, int r, uint64_t seed, uint64_t modulus,
+                              int64_t* out) {
+    if (!is_gasket(spec) || r < 0 || r > 20 || modulus == 0) return NBB_ERR_INVALID_ARGUMENT;
+    const int64_t n = (int64_t)1 << r;
+    int64_t W, H;
+    orc_orthotope_dims(spec, r, &W, &H);
+    orc_mt64 g;
+    orc_mt64_seed(&g, seed);
+    for (int64_t y = 0; y < n; ++y) {
+        int64_t x = 0;
+        do {
+            int64_t ox, oy;
+            gasket_lambda_inverse(r, x, y, &ox, &oy);
+            out[oy * W + ox] = (int64_t)(orc_mt64_next(&g) % modulus);
+            x = (x - y) & y;
+        } while (x != 0);
+    }
+    return NBB_OK;
+}
+
+/* run_ca (dispatch.cpp:517-557) on a CompactGrid: `steps` double-buffered steps of the
+ * reference rule (dispatch.cpp:530-550: live = #member Moore neighbours with value != 0,
+ * next = ((alive ? survive : birth) >> live) & 1, non-members stay 0), returned as the compact
+ * values of the final grid. The state between steps is the alive bit of every embedded cell
+ * (one bit per cell, n²/8 bytes: 512 MiB at r = 16, 2 GiB at r = 17) — exact because the rule
+ * reads only `value != 0` and writes 0/1; the compact <-> embedded mapping is the reference's
+ * λ (block_map.cpp:77-111), evaluated once per cell at entry and exit. steps == 0 copies. */
+static int bit_at(const uint64_t* b, int64_t n, int64_t x, int64_t y) {
+    const uint64_t i = (uint64_t)(y * n + x);
+    return (int)((b[i >> 6] >> (i & 63u)) & 1u);
+}
+
+int orc_ca_compact(const nbb_spec* spec, int r, const int64_t* src, int steps, uint16_t birth,
+                   uint16_t survive, int64_t* out) {
+    if (!is_gasket(spec) || r < 0 || r > 18 || steps < 0) return NBB_ERR_INVALID_ARGUMENT;
+    const int64_t n = (int64_t)1 << r;
+    int64_t W, H;
+    orc_orthotope_dims(spec, r, &W, &H);
+    const int64_t total = W * H;
+    if (steps == 0) {
+        memcpy(out, src, (size_t)total * sizeof(int64_t));
+        return NBB_OK;
+    }
+    const size_t words = (size_t)((n * n + 63) / 64);
+    uint64_t* a = (uint64_t*)calloc(words, sizeof(uint64_t));
+    uint64_t* b = (uint64_t*)calloc(words, sizeof(uint64_t));
+    if (!a || !b) {
+        free(a);
+        free(b);
+        return NBB_ERR_RESOURCE;
+    }
+    for (int64_t c = 0; c < total; ++c) {
+        int64_t x, y;
+        gasket_lambda(r, c % W, c / W, &x, &y);
+        if (src[c] != 0) {
+            const uint64_t i = (uint64_t)(y * n + x);
+            a[i >> 6] |= 1ull << (i & 63u);
+        }
+    }
+    for (int s = 0; s < steps; ++s) {
+        memset(b, 0, words * sizeof(uint64_t));
+        for (int64_t y = 0; y < n; ++y) {
+            int64_t x = 0;
+            do {  /* the member cells of row y */
+                int live = 0;
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        if (dx == 0 && dy == 0) continue;
+                        const int64_t nx = x + dx, ny = y + dy;
+                        if (orc_gasket_bit_test(r, nx, ny) && bit_at(a, n, nx, ny)) ++live;
+                    }
+                const uint16_t rule = bit_at(a, n, x, y) ? survive : birth;
+                if ((rule >> live) & 1u) {
+                    const uint64_t i = (uint64_t)(y * n + x);
+                    b[i >> 6] |= 1ull << (i & 63u);
+                }
+                x = (x - y) & y;
+            } while (x != 0);
+        }
+        uint64_t* t = a;
+        a = b;
+        b = t;
+    }
+    for (int64_t c = 0; c < total; ++c) {
+        int64_t x, y;
+        gasket_lambda(r, c % W, c / W, &x, &y);
+        out[c] = bit_at(a, n, x, y);
+    }
+    free(a);
+    free(b);
+    return NBB_OK;
+}
+
 void orc_ca(const nbb_spec* spec, int r, const int64_t* initial, int steps, uint16_t birth,
             uint16_t survive, int64_t* out) {
     const int64_t n = orc_side_length(spec, r);

@@ -63,6 +63,14 @@ void orc_ca_step(const nbb_spec* spec, int r, const int64_t* src, int64_t* dst, 
  * number of sampled offsets whose dst value differs (size-independent full-size check). */
 int64_t orc_ca_compact_check(const nbb_spec* spec, int r, const int64_t* src, const int64_t* dst,
                              const int64_t* offsets, int64_t count, uint16_t birth, uint16_t survive);
+/* Full-size trajectory checker on the compact state (gasket only): random_member_grid
+ * (dispatch.cpp:133-149) emitted in compact order (λ⁻¹ per member, block_map.cpp:113-148), and
+ * run_ca (dispatch.cpp:517-557) from a compact state to a compact state through a one-bit-per-cell
+ * embedded raster. Return nbb_status. */
+int orc_random_member_compact(const nbb_spec* spec, int r, uint64_t seed, uint64_t modulus,
+                              int64_t* out);
+int orc_ca_compact(const nbb_spec* spec, int r, const int64_t* src, int steps, uint16_t birth,
+                   uint16_t survive, int64_t* out);
 /* steps == 0 copies the input unchanged (B.4) */
 void orc_ca(const nbb_spec* spec, int r, const int64_t* initial, int steps, uint16_t birth,
             uint16_t survive, int64_t* out);

@@ -62,6 +62,8 @@ def orc_lib():
             "orc_reduction": (c_int64, [SP, c_int, c_void_p]),
             "orc_ca_step": (None, [SP, c_int, c_void_p, c_void_p, c_uint16, c_uint16]),
             "orc_ca": (None, [SP, c_int, c_void_p, c_int, c_uint16, c_uint16, c_void_p]),
+            "orc_random_member_compact": (c_int, [SP, c_int, c_uint64, c_uint64, c_void_p]),
+            "orc_ca_compact": (c_int, [SP, c_int, c_void_p, c_int, c_uint16, c_uint16, c_void_p]),
             "orc_ca_compact_check": (c_int64, [SP, c_int, c_void_p, c_void_p, c_void_p, c_int64,
                                                c_uint16, c_uint16]),
             "orc_validate": (c_int, [CP, c_char_p, c_size_t]),
@@ -170,6 +172,27 @@ def orc_ca_compact_check(r: int, src: np.ndarray, dst: np.ndarray, offsets: np.n
     offsets = np.ascontiguousarray(offsets, dtype=np.int64)
     return int(orc_lib().orc_ca_compact_check(ctypes.byref(spec.to_c()), r, _ptr(src), _ptr(dst),
                                               _ptr(offsets), offsets.size, birth, survive))
+
+
+def orc_random_member_compact(r: int, seed: int, modulus: int, spec: FractalSpec = GASKET) -> np.ndarray:
+    """random_member_grid(spec, r, seed, modulus) in compact (λ-ordered) layout, O(3^r)."""
+    w, h = 3 ** ((r + 1) // 2), 3 ** (r // 2)
+    out = np.zeros(w * h, dtype=np.int64)
+    rc = orc_lib().orc_random_member_compact(ctypes.byref(spec.to_c()), r, seed, modulus, _ptr(out))
+    if rc:
+        raise RuntimeError(f"orc_random_member_compact: status {rc}")
+    return out
+
+
+def orc_ca_compact(r: int, src: np.ndarray, steps: int, birth: int = 8, survive: int = 12,
+                   spec: FractalSpec = GASKET) -> np.ndarray:
+    """run_ca over a compact state: `steps` steps, compact values out (every cell, any r <= 18)."""
+    src = np.ascontiguousarray(src, dtype=np.int64).ravel()
+    out = np.empty_like(src)
+    rc = orc_lib().orc_ca_compact(ctypes.byref(spec.to_c()), r, _ptr(src), steps, birth, survive, _ptr(out))
+    if rc:
+        raise RuntimeError(f"orc_ca_compact: status {rc}")
+    return out
 
 
 def orc_lambda_coords(level: int, spec: FractalSpec = GASKET) -> np.ndarray:
