@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define NBB_GPU_ABI_VERSION 2
+#define NBB_GPU_ABI_VERSION 3
 #define NBB_MAX_REPLICAS 9
 
 /* Status codes; the C++ shim (nbb_gpu.hpp) rethrows the matching std:: type. */
@@ -100,7 +100,8 @@ typedef struct nbb_config {
     uint64_t shard_begin;
     uint64_t shard_count;
     uint32_t flags;     /* NBB_FLAG_* */
-    uint32_t reserved0;
+    uint32_t pass_steps; /* compact-state CA: at most this many steps per pass over the
+                          * state (1..4; 0 = 4). See nbb_gpu_ca_compact_passes_dev. */
 } nbb_config;
 
 /* nbb_config.flags
@@ -117,9 +118,10 @@ typedef struct nbb_config {
  *   addresses member tiles through λ⁻¹ (the comparison launch; unsharded). */
 #define NBB_FLAG_COMPACT_STATE 2u
 /* NBB_FLAG_SINGLE_STEP: compact-state CA runs (nbb_gpu_ca with NBB_FLAG_COMPACT_STATE,
- *   nbb_gpu_ca_compact_run_dev) launch one kernel per step. Without it, untimed lambda
- *   runs advance two steps per pass over the state (ca_compact2_kernel: the tile and its
- *   radius-2 halo are read once, the intermediate step stays on chip) — the same result. */
+ *   nbb_gpu_ca_compact_*_dev) launch one kernel per step (= pass_steps 1). Without it,
+ *   untimed runs advance up to pass_steps (default 4) steps per pass over the state
+ *   (ca_compact_pass_kernel: the tile and its radius-K halo are read once, the intermediate
+ *   steps stay on chip) — the same result. */
 #define NBB_FLAG_SINGLE_STEP 4u
 
 /* WorkReport (dispatch.hpp:44-61) */
@@ -241,11 +243,26 @@ int nbb_gpu_compact_read(const char* path, const nbb_spec* spec, int32_t* level,
  * rows), so each rank of the multi-GPU path updates one slab of the compact array. */
 int nbb_gpu_ca_compact_step_dev(const nbb_config* cfg, const void* d_src, void* d_dst,
                                 uint16_t birth, uint16_t survive, void* stream, nbb_report* report);
-/* `steps` compact CA steps ping-ponging between d_a and d_b (step i reads d_a when i is even),
- * issued back to back from C++ (the reference's run_ca step loop, dispatch.cpp:517-557);
- * the result is in d_a when steps is even, else in d_b. */
+/* `steps` compact CA steps ping-ponging between d_a and d_b, issued back to back from C++
+ * (the reference's run_ca step loop, dispatch.cpp:517-557) as passes of up to pass_steps
+ * steps each; the result is in d_a when steps is even, else in d_b (as stepping one by one:
+ * the pass count then has the parity of `steps`, which may cost one pass more). */
 int nbb_gpu_ca_compact_run_dev(const nbb_config* cfg, void* d_a, void* d_b, int32_t steps,
                                uint16_t birth, uint16_t survive, void* stream);
+/* What a pass sequence did: launches, launches per step count, where the result is. */
+typedef struct nbb_pass_stats {
+    int32_t passes;       /* kernel launches (passes over the state)                  */
+    int32_t by_steps[5];  /* by_steps[k]: passes that advanced k steps (k = 1..4)      */
+    int32_t result_in_b;  /* 1: the state after `steps` steps is in d_b; 0: in d_a     */
+} nbb_pass_stats;
+/* The same run with parity = 0: the fewest passes (ceil(steps / pass_steps)), the result in
+ * whichever buffer stats->result_in_b names; parity != 0 behaves as nbb_gpu_ca_compact_run_dev.
+ * stats may be NULL. */
+int nbb_gpu_ca_compact_passes_dev(const nbb_config* cfg, void* d_a, void* d_b, int32_t steps,
+                                  uint16_t birth, uint16_t survive, int32_t parity, void* stream,
+                                  nbb_pass_stats* stats);
+/* Host only: the passes the two calls above (parity as given) issue for `steps` steps. */
+int nbb_gpu_pass_plan(const nbb_config* cfg, int32_t steps, int32_t parity, nbb_pass_stats* stats);
 int nbb_gpu_reduction_compact_dev(const nbb_config* cfg, const void* d_compact, void* d_value,
                                   void* stream, nbb_report* report);
 int nbb_gpu_single_write_compact_dev(const nbb_config* cfg, void* d_compact, void* stream,
@@ -277,19 +294,23 @@ typedef struct nbb_p2p {
     int32_t world, rank;
     void* d_buf[2];              /* this rank's two compact buffers (3^r int64 each)            */
     const void* d_peer_buf[2];   /* [world] const int64_t*: every rank's buffer 0 / buffer 1   */
-    const void* d_halo_owner;    /* [tiles * 8] uint8: owner rank of each tile's halo cell     */
+    const void* reserved;        /* unused (ABI 2: a halo owner table; the owner of a halo cell
+                                  * is now its tile ordinal / ceil(tiles / world))            */
     void* d_sync;                /* this rank's uint32[4] {arrivals, done, error, 0}, zeroed    */
     const void* d_peer_flag;     /* [world] uint32*: every rank's d_sync (arrival counter)      */
     uint32_t timeout_ms;         /* bound on each wait; 0 = 20000                               */
 } nbb_p2p;
 int nbb_gpu_ca_compact_p2p_dev(const nbb_config* cfg, int64_t first_step, int32_t steps,
                                uint16_t birth, uint16_t survive, const nbb_p2p* p2p, void* stream);
-/* The same step sequence in PASSES of two steps (ca_compact2_kernel over peer memory: the
- * radius-2 halo read once, the intermediate step kept on chip; a single-step pass last when
- * `steps` is odd): steps / 2 + steps % 2 passes. Pass j (first_pass <= j) reads d_buf[j & 1],
- * writes d_buf[(j + 1) & 1] and waits for world x j arrivals; first_pass must equal the number
- * of passes (either entry point: a step of nbb_gpu_ca_compact_p2p_dev is one pass) this d_sync
- * has already run. */
+/* The same step sequence in PASSES of up to cfg->pass_steps steps (default 4; the
+ * ca_compact_pass_kernel over peer memory: the radius-K halo read once, the intermediate
+ * steps kept on chip): ceil(steps / K) passes, steps spread evenly. Pass j (first_pass <= j)
+ * reads d_buf[j & 1], writes d_buf[(j + 1) & 1] and waits for world x j arrivals; first_pass
+ * must equal the number of passes (either entry point: a step of nbb_gpu_ca_compact_p2p_dev
+ * is one pass) this d_sync has already run. The shard must be the rank's contiguous chunk:
+ * shard_begin = rank * ceil(tiles / world), shard_count = ceil(tiles / world) (clipped) —
+ * the owner of every halo cell is derived from it (NBB_ERR_INVALID_ARGUMENT otherwise).
+ * nbb_gpu_pass_plan(cfg, steps, 0, &stats) names the passes. */
 int nbb_gpu_ca_compact_p2p_passes_dev(const nbb_config* cfg, int64_t first_pass, int32_t steps,
                                       uint16_t birth, uint16_t survive, const nbb_p2p* p2p, void* stream);
 /* error flag of d_sync after a step sequence (synchronises the stream): 0 ok, 1 timed out */

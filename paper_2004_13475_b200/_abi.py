@@ -60,7 +60,7 @@ class NbbConfig(Structure):
         ("shard_begin", c_uint64),
         ("shard_count", c_uint64),
         ("flags", ctypes.c_uint32),
-        ("reserved0", ctypes.c_uint32),
+        ("pass_steps", ctypes.c_uint32),
     ]
 
 
@@ -87,6 +87,15 @@ class NbbReport(Structure):
     ]
 
 
+class NbbPassStats(Structure):
+    """nbb_pass_stats (nbb_gpu.h): the passes a compact CA run issued."""
+    _fields_ = [
+        ("passes", c_int32),
+        ("by_steps", c_int32 * 5),
+        ("result_in_b", c_int32),
+    ]
+
+
 class NbbP2P(Structure):
     """nbb_p2p (nbb_gpu.h): one rank's view of the multi-GPU compact CA."""
     _fields_ = [
@@ -94,7 +103,7 @@ class NbbP2P(Structure):
         ("rank", c_int32),
         ("d_buf", c_void_p * 2),
         ("d_peer_buf", c_void_p * 2),
-        ("d_halo_owner", c_void_p),
+        ("reserved", c_void_p),
         ("d_sync", c_void_p),
         ("d_peer_flag", c_void_p),
         ("timeout_ms", ctypes.c_uint32),
@@ -149,6 +158,9 @@ SIGNATURES = {
     "nbb_gpu_reduction_compact_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p, RP]),
     "nbb_gpu_single_write_compact_dev": (c_int, [CP, c_void_p, c_void_p, RP]),
     "nbb_gpu_ca_compact_run_dev": (c_int, [CP, c_void_p, c_void_p, c_int32, c_uint16, c_uint16, c_void_p]),
+    "nbb_gpu_ca_compact_passes_dev": (c_int, [CP, c_void_p, c_void_p, c_int32, c_uint16, c_uint16, c_int32,
+                                              c_void_p, POINTER(NbbPassStats)]),
+    "nbb_gpu_pass_plan": (c_int, [CP, c_int32, c_int32, POINTER(NbbPassStats)]),
     "nbb_gpu_ca_compact_p2p_dev": (c_int, [CP, ctypes.c_int64, c_int32, c_uint16, c_uint16,
                                            POINTER(NbbP2P), c_void_p]),
     "nbb_gpu_ca_compact_p2p_passes_dev": (c_int, [CP, ctypes.c_int64, c_int32, c_uint16, c_uint16,

@@ -1,4 +1,5 @@
-// compact_kernels.cuh — the compact (λ-ordered) codec and a CA step on compact state.
+// compact_kernels.cuh — the compact (λ-ordered) codec and the shared stages of the CA on
+// compact state (the pass kernel itself: compact_pass.cuh).
 //
 // CompactGrid (block_map.hpp:82-110): the k^r member values laid out row-major over
 // the packing orthotope, value(ω) = embedded(λ(ω)). compact_store / compact_load
@@ -220,15 +221,14 @@ __device__ __forceinline__ uint64_t gasket_compact_offset(uint32_t x, uint32_t y
 // ---- multi-GPU (P2P) step ordering -------------------------------------------------------
 constexpr int kMaxP2P = 8;
 struct P2PArgs {
-    const long long* const* peer_src;  // [world] each rank's source buffer of this step
-    const uint8_t* halo_owner;         // [tiles * 8] rank owning each halo cell
+    const long long* const* peer_src;  // [world] each rank's source buffer of this pass
     unsigned int* sync;                // this rank's {arrivals, done CTAs, error, unused}
     unsigned int* const* peer_flag;    // [world] every rank's sync word (arrival counter first)
-    unsigned int wait_target;          // arrivals required before the step may start (world x step)
+    unsigned int wait_target;          // arrivals required before the pass may start (world x pass)
     unsigned int timeout_ms;
     int world, rank;
-    unsigned int chunk;                // tiles per rank (ca_compact2_kernel: owner = tile / chunk)
-    unsigned int own_lo, own_hi;       // compact offsets [lo, hi) inside this rank's whole tile rows
+    FastDiv div_chunk;                 // tiles per rank: the owner of tile u is u / chunk
+    unsigned int first_pass;           // first pass of a call: also wait for the previous grid
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -283,212 +283,7 @@ __device__ __forceinline__ void p2p_arrive(const P2PArgs& p) {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-// The 8 halo cells of every ρ = 32 tile as compact offsets (-1: not a member / outside),
-// [tile u][k] for the tile-local positions (-1,-1) (0,-1) (1,-1) (-1,31) (32,30) (32,31)
-// (32,32) (0,32). Static per level; built once per device and level (5.7 MB at r = 16) so
-// the CA step spends one 32-byte load per tile instead of λ + λ⁻¹ arithmetic.
-__global__ void compact_halo_table_kernel(CompactCaArgs a, FastDiv div_hb, int32_t* tab) {
-    const uint32_t nm1 = (uint32_t)(a.n - 1);
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (uint64_t)a.tiles * 8u;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t u = (uint32_t)(i >> 3), hk = (uint32_t)i & 7u;
-        const int hx = (hk == 0 || hk == 3) ? -1 : (hk == 1 || hk == 7) ? 0 : (hk == 2) ? 1 : 32;
-        const int hy = (hk <= 2) ? -1 : (hk == 3 || hk == 5) ? 31 : (hk == 4) ? 30 : 32;
-        const uint32_t wxb = fastdiv(u, div_hb), wyb = u - wxb * a.Hb;
-        uint32_t bx, by;
-        lambda_arith(wxb, wyb, bx, by);
-        const uint32_t gx = bx * 32u + (uint32_t)hx, gy = by * 32u + (uint32_t)hy;  // wraps if < 0
-        const bool ok = gx <= nm1 && gy <= nm1 && (gx & (nm1 - gy)) == 0u;
-        tab[i] = ok ? (int32_t)gasket_compact_offset(gx, gy, a.W) : -1;
-    }
-}
-
-// One warp per tile; tile u -> (ωx_b = u / Hb, ωy_b = u % Hb) so consecutive warps walk along a
-// compact row block. 243 values per tile = slots k = 0..7 of lane l: li = 32k + l (k < 7 valid
-// for every lane, k = 7 for lanes < 19).
-//
-// Per tile: 8 coalesced 8-byte loads per lane (compact rows of 27 values), the 8 halo cells
-// (compact offsets from the per-level halo table), alive bits scattered as bytes into a per-warp
-// 32 x 32 byte tile (non-member bytes stay 0, so no atomics and no clearing), rows packed back
-// to bit masks (lane = row) for the bit-sliced rule, and 8 stores per lane. Software-pipelined
-// (the next tile's loads fly during this tile's rule and stores) and launched with PDL; at
-// n = 2^16 a step runs at 0.964 of the measured HBM copy peak, long-scoreboard the dominant
-// stall (ncu: profiles/r1_ncu_ca_compact_v5.txt). Tried and slower on B200
-// (profiles/r1_compact_ca_tuning.md): a cp.async ring (8-byte copies), L2 bulk prefetch one
-// tile ahead, 64/48-register budgets, cp.async.bulk row copies into an mbarrier ring, all steps
-// in one launch with tile-level dataflow, and exported boundary-cell bytes for the halo.
-//
-// P2P = true is the multi-GPU form (one kernel per step, no separate exchange): each rank
-// owns a contiguous range of tiles in its own replica-sized buffers, the halo cells owned
-// by other ranks are read straight from their buffers over NVLink (CUDA IPC mappings,
-// ld.relaxed.sys), and a flag barrier in peer memory orders the steps: the kernel first
-// waits until every rank has finished the previous step (world x i arrivals on this rank's
-// counter before step i), and its last CTA to finish adds one arrival to every rank's flag.
-template <bool P2P>
-__global__ void __launch_bounds__(256, 3) ca_compact_kernel(CompactCaArgs a, FastDiv div_hb,
-                                                             const int32_t* __restrict__ halo_tab,
-                                                             P2PArgs p) {
-    __shared__ __align__(16) uint8_t s_cell[8][32 * 32];
-    __shared__ uint32_t s_new[8][32];
-    __shared__ uint16_t s_pos[256];  // c_local_pos (per-lane constant-bank reads serialise)
-    __shared__ const long long* s_peer[kMaxP2P];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    uint8_t* cell = s_cell[wib];
-    pdl_trigger();
-    s_pos[threadIdx.x] = threadIdx.x < 243 ? c_local_pos[threadIdx.x] : 0;
-    if (P2P && p.wait_target != 0u) {
-        // the arrival wait subsumes pdl_wait: this rank's own arrival for the previous step is
-        // in it (its last CTA's stores released before it), so no grid-completion wait
-        if (threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
-        if (threadIdx.x == 0) p2p_wait(p);
-    } else {
-        // plain steps, and the first P2P step of a sequence (its predecessor on the stream is
-        // whatever produced the state, not a P2P step)
-        if (P2P && threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
-        pdl_wait();
-    }
-    __syncthreads();
-    uint32_t sl_off[8], sl_pos[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const uint32_t li = 32u * k + lane;
-        const bool ok = li < 243u;
-        const uint32_t row = ok ? li / 27u : 0u, col = ok ? li % 27u : 0u;
-        sl_off[k] = (row * a.W + col) * 8u;  // byte offset inside the tile's sub-block
-        sl_pos[k] = s_pos[li];               // x | y << 5 = byte index in the 32 x 32 tile
-    }
-    const bool k7 = lane < 19;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) reinterpret_cast<uint32_t*>(cell)[32 * i + lane] = 0u;
-    const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t warp_stride = (gridDim.x * blockDim.x) >> 5;
-    const char* src0 = reinterpret_cast<const char*>(a.src);
-    char* dst0 = reinterpret_cast<char*>(a.dst);
-    __syncwarp();
-
-    // Software-pipelined over the warp's tiles: tile u+stride's loads (its 243 values and
-    // halo cells) are issued as soon as tile u's values are in the byte tile — into the same
-    // registers — so they fly while tile u's rule and stores run; the halo-table entries run
-    // one more tile ahead (the halo load depends on them).
-    auto tile_base = [&](uint32_t t) -> uint64_t {
-        const uint32_t wxb = fastdiv(t, div_hb), wyb = t - wxb * a.Hb;
-        return ((uint64_t)(9u * wxb) * a.W + 27u * wyb) * 8u;
-    };
-    long long v[8];
-    auto load_tile = [&](uint64_t b) {
-        const char* src = src0 + b;
-#pragma unroll
-        for (int k = 0; k < 7; ++k) v[k] = __ldg(reinterpret_cast<const long long*>(src + sl_off[k]));
-        v[7] = k7 ? __ldg(reinterpret_cast<const long long*>(src + sl_off[7])) : 0ll;
-    };
-    auto load_halo = [&](int32_t off, uint32_t own) -> long long {
-        long long hv = 0;
-        if (off >= 0) {
-            if (!P2P || own == (uint32_t)p.rank)
-                hv = __ldg(a.src + off);
-            else  // a cell of another rank's tile: read its buffer over NVLink
-                asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(hv) : "l"(s_peer[own] + off));
-        }
-        return hv;
-    };
-    auto halo_entry = [&](uint32_t t, int32_t& off, uint32_t& own) {
-        const bool ok = t < a.tile_end && lane < 8;
-        off = ok ? __ldg(halo_tab + 8ull * t + lane) : -1;
-        own = (P2P && ok) ? p.halo_owner[8ull * t + lane] : 0u;
-    };
-
-    uint32_t u = a.tile_begin + warp_global;
-    uint64_t base = 0;
-    long long hv = 0;
-    int32_t hoff_n = -1;
-    uint32_t hown_n = 0;
-    if (u < a.tile_end) {
-        base = tile_base(u);
-        load_tile(base);
-        int32_t off;
-        uint32_t own;
-        halo_entry(u, off, own);
-        hv = load_halo(off, own);
-        halo_entry(u + warp_stride, hoff_n, hown_n);
-    }
-    for (; u < a.tile_end; u += warp_stride) {
-        const uint32_t un = u + warp_stride;
-#pragma unroll
-        for (int k = 0; k < 7; ++k) cell[sl_pos[k]] = v[k] != 0ll;
-        if (k7) cell[sl_pos[7]] = v[7] != 0ll;
-        const uint32_t h = __ballot_sync(0xFFFFFFFFu, hv != 0ll) & 0xFFu;
-        uint64_t base_n = 0;
-        if (un < a.tile_end) {  // warp-uniform
-            base_n = tile_base(un);
-            load_tile(base_n);
-            hv = load_halo(hoff_n, hown_n);
-            halo_entry(un + warp_stride, hoff_n, hown_n);
-        }
-        __syncwarp();
-        uint32_t R;
-        {   // 0/1 bytes -> bits (as in ca_compact2_kernel)
-            const uint4 q0 = reinterpret_cast<const uint4*>(cell + 32 * lane)[0];
-            const uint4 q1 = reinterpret_cast<const uint4*>(cell + 32 * lane)[1];
-            const uint32_t p0 = (q0.x + (q0.y << 4)) * 0x01020408u, p1 = (q0.z + (q0.w << 4)) * 0x01020408u;
-            const uint32_t p2 = (q1.x + (q1.y << 4)) * 0x01020408u, p3 = (q1.z + (q1.w << 4)) * 0x01020408u;
-            R = __byte_perm(__byte_perm(p0, p1, 0x0073u), __byte_perm(p2, p3, 0x0073u), 0x5410u);
-        }
-        uint64_t E = (uint64_t)R << 1;
-        if (lane == 31) E |= ((h >> 3) & 1u) | ((uint64_t)((h >> 5) & 1u) << 33);
-        if (lane == 30) E |= (uint64_t)((h >> 4) & 1u) << 33;
-        const uint64_t top = (h & 1u) | (((h >> 1) & 1u) << 1) | (((h >> 2) & 1u) << 2);
-        const uint64_t bottom = (((h >> 7) & 1u) << 1) | ((uint64_t)((h >> 6) & 1u) << 33);
-        const uint64_t Eu = __shfl_up_sync(0xFFFFFFFFu, E, 1);
-        const uint64_t Ed = __shfl_down_sync(0xFFFFFFFFu, E, 1);
-        const uint64_t U = lane == 0 ? top : Eu;
-        const uint64_t D = lane == 31 ? bottom : Ed;
-        s_new[wib][lane] = life_rule((uint32_t)U, (uint32_t)(U >> 1), (uint32_t)(U >> 2), (uint32_t)E,
-                                     (uint32_t)(E >> 2), (uint32_t)D, (uint32_t)(D >> 1), (uint32_t)(D >> 2),
-                                     (uint32_t)(E >> 1), a.birth, a.survive) &
-                           submask_bits((uint32_t)lane);
-        __syncwarp();
-        char* dst = dst0 + base;
-        base = base_n;
-#pragma unroll
-        for (int k = 0; k < 7; ++k)
-            *reinterpret_cast<long long*>(dst + sl_off[k]) =
-                (long long)((s_new[wib][sl_pos[k] >> 5] >> (sl_pos[k] & 31u)) & 1u);
-        if (k7)
-            *reinterpret_cast<long long*>(dst + sl_off[7]) =
-                (long long)((s_new[wib][sl_pos[7] >> 5] >> (sl_pos[7] & 31u)) & 1u);
-        __syncwarp();
-    }
-    if (P2P) p2p_arrive(p);
-}
-
-
-// ---- two CA steps per pass (temporal blocking of the compact step) ------------------------
-// The radius-2 halo of a ρ = 32 tile: the 8 cells of compact_halo_table_kernel (H1, the
-// member neighbours of the tile's members) followed by the 14 positions that can hold a member
-// neighbour of an H1 cell outside the tile (H2; found by brute force over every tile of r = 6..11,
-// the set is the same at every level by self-similarity). Tile-local (x, y).
-constexpr int kHalo2 = 22, kHalo2Stride = 24;
-__constant__ int8_t c_h2x[kHalo2] = {-1, 0, 1, -1, 32, 32, 32, 0, -2, -2, -2, -2, 0, 0, 1, 2, 2, 32, 32, 33, 33, 33};
-__constant__ int8_t c_h2y[kHalo2] = {-1, -1, -1, 31, 30, 31, 32, 32, -2, -1, 30, 31, -2, 33, 33, -2, -1, 29, 33, 29, 31, 33};
-
-// [tile u][k] compact offsets of the 22 halo positions (-1: not a member / outside), stride 24
-__global__ void compact_halo2_table_kernel(CompactCaArgs a, FastDiv div_hb, int32_t* tab) {
-    const uint32_t nm1 = (uint32_t)(a.n - 1);
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (uint64_t)a.tiles * kHalo2Stride;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t u = (uint32_t)(i / kHalo2Stride), hk = (uint32_t)(i % kHalo2Stride);
-        int32_t off = -1;
-        if (hk < (uint32_t)kHalo2) {
-            const uint32_t wxb = fastdiv(u, div_hb), wyb = u - wxb * a.Hb;
-            uint32_t bx, by;
-            lambda_arith(wxb, wyb, bx, by);
-            const uint32_t gx = bx * 32u + (uint32_t)(int)c_h2x[hk], gy = by * 32u + (uint32_t)(int)c_h2y[hk];
-            if (gx <= nm1 && gy <= nm1 && (gx & (nm1 - gy)) == 0u) off = (int32_t)gasket_compact_offset(gx, gy, a.W);
-        }
-        tab[i] = off;
-    }
-}
-
+// ---- shared stage of the compact CA pass (compact_pass.cuh) --------------------------------
 // One bit-sliced step of a tile held as row masks (lane = row y, bit x) with the 8 H1 halo
 // bits h (order of compact_halo_table_kernel); members only.
 __device__ __forceinline__ uint32_t compact_rows_step(uint32_t R, uint32_t h, int lane, uint32_t birth,
@@ -506,341 +301,6 @@ __device__ __forceinline__ uint32_t compact_rows_step(uint32_t R, uint32_t h, in
                      (uint32_t)D, (uint32_t)(D >> 1), (uint32_t)(D >> 2), (uint32_t)(E >> 1), birth, survive) &
            submask_bits((uint32_t)lane);
 }
-
-// Two CA steps per pass over the compact state: each warp loads its tile (243 values) and the
-// 22 radius-2 halo cells once, computes step t+1 for the tile (bit-sliced) and for its 8 H1
-// halo cells (lanes 0..7, scalar, from the step-t bytes), then step t+2 for the tile from those,
-// and stores step t+2 — 8 B read + 8 B write per member per TWO steps. Same tile walk, software
-// pipeline and PDL as ca_compact_kernel; the step-t+1 state never reaches HBM. The pass is
-// ALU-bound, so the reference's default rule (CaRule{}: B3/S23) has its own instantiation with
-// the rule masks known at compile time (the bit-sliced rule's leaves fold away); every other
-// rule runs the generic one.
-//
-// P2P = true is the multi-GPU pass (as ca_compact_kernel<true>): the halo cells of other ranks'
-// tiles are read from their buffers over NVLink, the owner computed from the compact offset
-// (tile = (row / 9) H_b + col / 27, owner = tile / chunk), and the same flag barrier orders
-// the passes (world x j arrivals before pass j).
-template <bool CONWAY, bool P2P>
-__global__ void __launch_bounds__(256, 3) ca_compact2_kernel(CompactCaArgs a, FastDiv div_hb,
-                                                             const int32_t* __restrict__ halo_tab,
-                                                             P2PArgs p) {
-    const uint32_t birth = CONWAY ? (1u << 3) : a.birth;
-    const uint32_t survive = CONWAY ? (1u << 2) | (1u << 3) : a.survive;
-    __shared__ __align__(16) uint8_t s_cell[8][32 * 32];
-    __shared__ uint32_t s_new[8][32];
-    __shared__ uint16_t s_pos[256];
-    // H1 cell k's neighbours: the halo slots among them (bit mask over the 22) and its <= 3
-    // in-tile positions (byte index; padded with byte 1 = cell (1, 0), never a member, always 0)
-    __shared__ uint32_t s_nb[8];
-    __shared__ __align__(8) uint16_t s_nt[8][4];
-    __shared__ const long long* s_peer[kMaxP2P];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    uint8_t* cell = s_cell[wib];
-    pdl_trigger();
-    if (P2P && threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
-    s_pos[threadIdx.x] = threadIdx.x < 243 ? c_local_pos[threadIdx.x] : 0;
-    if (threadIdx.x < 8) {
-        const int k = threadIdx.x;
-        uint32_t nb = 0;
-        int nt = 0;
-        for (int i = 0; i < 4; ++i) s_nt[k][i] = 1;
-        for (int dd = 0; dd < 9; ++dd) {  // the 8 neighbours of the 3 x 3 block, centre skipped
-            if (dd == 4) continue;
-            const int qx = c_h2x[k] + dd % 3 - 1, qy = c_h2y[k] + dd / 3 - 1;
-            if (qx >= 0 && qx < 32 && qy >= 0 && qy < 32) {
-                if (nt < 4) s_nt[k][nt++] = (uint16_t)(qy * 32 + qx);
-            } else {
-                for (int j = 0; j < kHalo2; ++j)
-                    if (c_h2x[j] == qx && c_h2y[j] == qy) nb |= 1u << j;
-            }
-        }
-        s_nb[k] = nb;
-    }
-    if (P2P && p.wait_target != 0u) {  // the arrival wait subsumes pdl_wait (ca_compact_kernel)
-        if (threadIdx.x == 0) p2p_wait(p);
-    } else {
-        pdl_wait();
-    }
-    __syncthreads();
-    uint32_t sl_off[8], sl_pos[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const uint32_t li = 32u * k + lane;
-        const bool ok = li < 243u;
-        const uint32_t row = ok ? li / 27u : 0u, col = ok ? li % 27u : 0u;
-        sl_off[k] = (row * a.W + col) * 8u;
-        sl_pos[k] = s_pos[li];
-    }
-    const bool k7 = lane < 19;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) reinterpret_cast<uint32_t*>(cell)[32 * i + lane] = 0u;
-    const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t warp_stride = (gridDim.x * blockDim.x) >> 5;
-    const char* src0 = reinterpret_cast<const char*>(a.src);
-    char* dst0 = reinterpret_cast<char*>(a.dst);
-    __syncwarp();
-
-    auto tile_base = [&](uint32_t t) -> uint64_t {
-        const uint32_t wxb = fastdiv(t, div_hb), wyb = t - wxb * a.Hb;
-        return ((uint64_t)(9u * wxb) * a.W + 27u * wyb) * 8u;
-    };
-    long long v[8];
-    auto load_tile = [&](uint64_t b) {
-        const char* src = src0 + b;
-#pragma unroll
-        for (int k = 0; k < 7; ++k) v[k] = __ldg(reinterpret_cast<const long long*>(src + sl_off[k]));
-        v[7] = k7 ? __ldg(reinterpret_cast<const long long*>(src + sl_off[7])) : 0ll;
-    };
-    auto halo_entry = [&](uint32_t t) -> int32_t {
-        return (t < a.tile_end && lane < kHalo2) ? __ldg(halo_tab + (uint64_t)kHalo2Stride * t + lane) : -1;
-    };
-    auto load_halo = [&](int32_t off) -> long long {
-        long long hv = 0;
-        if (off >= 0) {
-            uint32_t own = (uint32_t)p.rank;
-            if (P2P && ((uint32_t)off < p.own_lo || (uint32_t)off >= p.own_hi)) {  // not surely ours
-                const uint32_t row = (uint32_t)off / a.W, col = (uint32_t)off - row * a.W;
-                own = ((row / 9u) * a.Hb + col / 27u) / p.chunk;
-            }
-            if (!P2P || own == (uint32_t)p.rank)
-                hv = __ldg(a.src + off);
-            else  // a cell of another rank's tile: read its buffer over NVLink
-                asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(hv) : "l"(s_peer[own] + off));
-        }
-        return hv;
-    };
-
-    uint32_t u = a.tile_begin + warp_global;
-    uint64_t base = 0;
-    long long hv = 0;
-    uint32_t hmem = 0;  // H1 slots that are members (bit k)
-    int32_t hoff_n = -1;
-    if (u < a.tile_end) {
-        base = tile_base(u);
-        load_tile(base);
-        const int32_t off = halo_entry(u);
-        hv = load_halo(off);
-        hmem = __ballot_sync(0xFFFFFFFFu, off >= 0) & 0xFFu;
-        hoff_n = halo_entry(u + warp_stride);
-    }
-    for (; u < a.tile_end; u += warp_stride) {
-        const uint32_t un = u + warp_stride;
-#pragma unroll
-        for (int k = 0; k < 7; ++k) cell[sl_pos[k]] = v[k] != 0ll;
-        if (k7) cell[sl_pos[7]] = v[7] != 0ll;
-        const uint32_t hm = __ballot_sync(0xFFFFFFFFu, hv != 0ll);  // step-t halo alive bits
-        const uint32_t hmem_cur = hmem;
-        uint64_t base_n = 0;
-        if (un < a.tile_end) {  // warp-uniform
-            base_n = tile_base(un);
-            load_tile(base_n);
-            hv = load_halo(hoff_n);
-            hmem = __ballot_sync(0xFFFFFFFFu, hoff_n >= 0) & 0xFFu;
-            hoff_n = halo_entry(un + warp_stride);
-        }
-        __syncwarp();
-        uint32_t R;
-        {   // 0/1 bytes -> bits: per 8 cells (w0 + w1 << 4) * 0x01020408 gathers cell j into bit
-            // 24 + j without carries; the four top bytes are then merged with byte permutes
-            const uint4 q0 = reinterpret_cast<const uint4*>(cell + 32 * lane)[0];
-            const uint4 q1 = reinterpret_cast<const uint4*>(cell + 32 * lane)[1];
-            const uint32_t p0 = (q0.x + (q0.y << 4)) * 0x01020408u, p1 = (q0.z + (q0.w << 4)) * 0x01020408u;
-            const uint32_t p2 = (q1.x + (q1.y << 4)) * 0x01020408u, p3 = (q1.z + (q1.w << 4)) * 0x01020408u;
-            R = __byte_perm(__byte_perm(p0, p1, 0x0073u), __byte_perm(p2, p3, 0x0073u), 0x5410u);
-        }
-        // step t+1: the tile (bit-sliced) and the H1 cells (lane k < 8, scalar)
-        const uint32_t R1 = compact_rows_step(R, hm & 0xFFu, lane, birth, survive);
-        uint32_t live;
-        {
-            const uint2 t = *reinterpret_cast<const uint2*>(s_nt[lane & 7]);
-            live = __popc(hm & s_nb[lane & 7]) + cell[t.x & 0xFFFFu] + cell[t.x >> 16] + cell[t.y & 0xFFFFu];
-        }
-        const uint32_t rule = ((hm >> (lane & 7)) & 1u) ? survive : birth;
-        const uint32_t h1 = __ballot_sync(0xFFFFFFFFu, lane < 8 && ((rule >> live) & 1u)) & hmem_cur;
-        // step t+2: the tile only
-        s_new[wib][lane] = compact_rows_step(R1, h1, lane, birth, survive);
-        __syncwarp();
-        char* dst = dst0 + base;
-        base = base_n;
-#pragma unroll
-        for (int k = 0; k < 7; ++k)
-            *reinterpret_cast<long long*>(dst + sl_off[k]) =
-                (long long)((s_new[wib][sl_pos[k] >> 5] >> (sl_pos[k] & 31u)) & 1u);
-        if (k7)
-            *reinterpret_cast<long long*>(dst + sl_off[7]) =
-                (long long)((s_new[wib][sl_pos[7] >> 5] >> (sl_pos[7] & 31u)) & 1u);
-        __syncwarp();
-    }
-    if (P2P) p2p_arrive(p);
-}
-
-// The BOUNDING-BOX launch of the compact-state CA step (the comparison for ca_compact_kernel on
-// the same storage): identical per-tile work, but the warps walk all (n/32)^2 box tiles, cull
-// the non-member ones and address each member tile through λ⁻¹ — the inverse map the compact
-// layout needs (block_map.cpp:113-148) — instead of enumerating the λ orthotope.
-__global__ void __launch_bounds__(256, 3) ca_compact_bb_kernel(CompactCaArgs a, FastDiv div_hb,
-                                                              const int32_t* __restrict__ halo_tab) {
-    constexpr bool P2P = false;
-    const P2PArgs p{};
-    __shared__ __align__(16) uint8_t s_cell[8][32 * 32];
-    __shared__ uint32_t s_new[8][32];
-    __shared__ uint16_t s_pos[256];  // c_local_pos (per-lane constant-bank reads serialise)
-    __shared__ const long long* s_peer[kMaxP2P];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    uint8_t* cell = s_cell[wib];
-    pdl_trigger();
-    s_pos[threadIdx.x] = threadIdx.x < 243 ? c_local_pos[threadIdx.x] : 0;
-    if (P2P && p.wait_target != 0u) {
-        // the arrival wait subsumes pdl_wait: this rank's own arrival for the previous step is
-        // in it (its last CTA's stores released before it), so no grid-completion wait
-        if (threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
-        if (threadIdx.x == 0) p2p_wait(p);
-    } else {
-        // plain steps, and the first P2P step of a sequence (its predecessor on the stream is
-        // whatever produced the state, not a P2P step)
-        if (P2P && threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
-        pdl_wait();
-    }
-    __syncthreads();
-    uint32_t sl_off[8], sl_pos[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const uint32_t li = 32u * k + lane;
-        const bool ok = li < 243u;
-        const uint32_t row = ok ? li / 27u : 0u, col = ok ? li % 27u : 0u;
-        sl_off[k] = (row * a.W + col) * 8u;  // byte offset inside the tile's sub-block
-        sl_pos[k] = s_pos[li];               // x | y << 5 = byte index in the 32 x 32 tile
-    }
-    const bool k7 = lane < 19;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) reinterpret_cast<uint32_t*>(cell)[32 * i + lane] = 0u;
-    const uint32_t warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t warp_stride = (gridDim.x * blockDim.x) >> 5;
-    const char* src0 = reinterpret_cast<const char*>(a.src);
-    char* dst0 = reinterpret_cast<char*>(a.dst);
-    __syncwarp();
-
-    // Software-pipelined over the warp's tiles: tile u+stride's loads (its 243 values and
-    // halo cells) are issued as soon as tile u's values are in the byte tile — into the same
-    // registers — so they fly while tile u's rule and stores run; the halo-table entries run
-    // one more tile ahead (the halo load depends on them).
-    auto tile_base = [&](uint32_t t) -> uint64_t {
-        const uint32_t wxb = fastdiv(t, div_hb), wyb = t - wxb * a.Hb;
-        return ((uint64_t)(9u * wxb) * a.W + 27u * wyb) * 8u;
-    };
-    long long v[8];
-    auto load_tile = [&](uint64_t b) {
-        const char* src = src0 + b;
-#pragma unroll
-        for (int k = 0; k < 7; ++k) v[k] = __ldg(reinterpret_cast<const long long*>(src + sl_off[k]));
-        v[7] = k7 ? __ldg(reinterpret_cast<const long long*>(src + sl_off[7])) : 0ll;
-    };
-    auto load_halo = [&](int32_t off, uint32_t own) -> long long {
-        long long hv = 0;
-        if (off >= 0) {
-            if (!P2P || own == (uint32_t)p.rank)
-                hv = __ldg(a.src + off);
-            else  // a cell of another rank's tile: read its buffer over NVLink
-                asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(hv) : "l"(s_peer[own] + off));
-        }
-        return hv;
-    };
-    auto halo_entry = [&](uint32_t t, int32_t& off, uint32_t& own) {
-        const bool ok = t < a.tile_end && lane < 8;
-        off = ok ? __ldg(halo_tab + 8ull * t + lane) : -1;
-        own = (P2P && ok) ? p.halo_owner[8ull * t + lane] : 0u;
-    };
-
-    // the bounding box of (n/32)^2 tiles, walked with an odd warp stride (tile_kernel); a box
-    // tile holds members iff bx ⊆ (n/32 - 1 - by) — the others are culled, as the reference's
-    // threads of such a block all fail their test — and a member tile finds its storage in the
-    // compact state through λ⁻¹ of its block coordinates (u = ωx_b·H_b + ωy_b)
-    const uint32_t nb = (uint32_t)(a.n >> 5), lg = 31u - __clz(nb), boxes = nb * nb;
-    const uint32_t ustride = (warp_stride | 1u) - ((warp_stride & 1u) ? 0u : 2u);
-    auto next_member = [&](uint32_t bi) -> uint32_t {
-        while (bi < boxes && ((bi & (nb - 1u)) & (nb - 1u - (bi >> lg))) != 0u) bi += ustride;
-        return bi;
-    };
-    auto tile_of_box = [&](uint32_t bi) -> uint32_t {
-        const uint32_t bx = bi & (nb - 1u), by = bi >> lg;
-        const uint32_t wx = bits_base3(even_bits(bx)) + bits_base3(even_bits(by));
-        const uint32_t wy = bits_base3(even_bits(bx >> 1)) + bits_base3(even_bits(by >> 1));
-        return wx * a.Hb + wy;
-    };
-    uint32_t bcur = next_member(warp_global < ustride ? warp_global : boxes);
-    uint32_t bnext = bcur < boxes ? next_member(bcur + ustride) : boxes;
-    uint32_t u = bcur < boxes ? tile_of_box(bcur) : 0u;
-    uint32_t u_next = bnext < boxes ? tile_of_box(bnext) : 0u;
-    uint64_t base = 0;
-    long long hv = 0;
-    int32_t hoff_n = -1;
-    uint32_t hown_n = 0;
-    if (bcur < boxes) {
-        base = tile_base(u);
-        load_tile(base);
-        int32_t off;
-        uint32_t own;
-        halo_entry(u, off, own);
-        hv = load_halo(off, own);
-        halo_entry(bnext < boxes ? u_next : a.tile_end, hoff_n, hown_n);
-    }
-    while (bcur < boxes) {
-        const uint32_t un = u_next, bn = bnext;
-        const bool more = bn < boxes;
-        const uint32_t bnn = more ? next_member(bn + ustride) : boxes;  // the tile after next
-        u_next = bnn < boxes ? tile_of_box(bnn) : 0u;
-#pragma unroll
-        for (int k = 0; k < 7; ++k) cell[sl_pos[k]] = v[k] != 0ll;
-        if (k7) cell[sl_pos[7]] = v[7] != 0ll;
-        const uint32_t h = __ballot_sync(0xFFFFFFFFu, hv != 0ll) & 0xFFu;
-        uint64_t base_n = 0;
-        if (more) {  // warp-uniform
-            base_n = tile_base(un);
-            load_tile(base_n);
-            hv = load_halo(hoff_n, hown_n);
-            halo_entry(bnn < boxes ? u_next : a.tile_end, hoff_n, hown_n);
-        }
-        __syncwarp();
-        uint32_t R;
-        {   // 0/1 bytes -> bits (as in ca_compact2_kernel)
-            const uint4 q0 = reinterpret_cast<const uint4*>(cell + 32 * lane)[0];
-            const uint4 q1 = reinterpret_cast<const uint4*>(cell + 32 * lane)[1];
-            const uint32_t p0 = (q0.x + (q0.y << 4)) * 0x01020408u, p1 = (q0.z + (q0.w << 4)) * 0x01020408u;
-            const uint32_t p2 = (q1.x + (q1.y << 4)) * 0x01020408u, p3 = (q1.z + (q1.w << 4)) * 0x01020408u;
-            R = __byte_perm(__byte_perm(p0, p1, 0x0073u), __byte_perm(p2, p3, 0x0073u), 0x5410u);
-        }
-        uint64_t E = (uint64_t)R << 1;
-        if (lane == 31) E |= ((h >> 3) & 1u) | ((uint64_t)((h >> 5) & 1u) << 33);
-        if (lane == 30) E |= (uint64_t)((h >> 4) & 1u) << 33;
-        const uint64_t top = (h & 1u) | (((h >> 1) & 1u) << 1) | (((h >> 2) & 1u) << 2);
-        const uint64_t bottom = (((h >> 7) & 1u) << 1) | ((uint64_t)((h >> 6) & 1u) << 33);
-        const uint64_t Eu = __shfl_up_sync(0xFFFFFFFFu, E, 1);
-        const uint64_t Ed = __shfl_down_sync(0xFFFFFFFFu, E, 1);
-        const uint64_t U = lane == 0 ? top : Eu;
-        const uint64_t D = lane == 31 ? bottom : Ed;
-        s_new[wib][lane] = life_rule((uint32_t)U, (uint32_t)(U >> 1), (uint32_t)(U >> 2), (uint32_t)E,
-                                     (uint32_t)(E >> 2), (uint32_t)D, (uint32_t)(D >> 1), (uint32_t)(D >> 2),
-                                     (uint32_t)(E >> 1), a.birth, a.survive) &
-                           submask_bits((uint32_t)lane);
-        __syncwarp();
-        char* dst = dst0 + base;
-        base = base_n;
-        u = un;
-        bcur = bn;
-        bnext = bnn;
-#pragma unroll
-        for (int k = 0; k < 7; ++k)
-            *reinterpret_cast<long long*>(dst + sl_off[k]) =
-                (long long)((s_new[wib][sl_pos[k] >> 5] >> (sl_pos[k] & 31u)) & 1u);
-        if (k7)
-            *reinterpret_cast<long long*>(dst + sl_off[7]) =
-                (long long)((s_new[wib][sl_pos[7] >> 5] >> (sl_pos[7] & 31u)) & 1u);
-        __syncwarp();
-    }
-    (void)p;
-    (void)u;
-}
-
 
 // ---- embedded member sectors <-> compact state, tile by tile ------------------------------
 // Local compact index li = ωy_l·27 + ωx_l of member (x, y) of a ρ = 32 tile (x ⊆ y < 32).

@@ -28,6 +28,7 @@
 #include "ca_pipe_kernel.cuh"
 #include "bits_kernels.cuh"
 #include "compact_kernels.cuh"
+#include "compact_pass.cuh"
 #include "util_kernels.cuh"
 
 using namespace nbbgpu;
@@ -73,8 +74,7 @@ struct DeviceCtx {
     void* bufs[3] = {nullptr, nullptr, nullptr};
     size_t buf_bytes[3] = {0, 0, 0};
     int16_t* lut[6] = {};                    // LocalCellTable per edge 2^i
-    int32_t* halo_tab[32] = {};              // compact CA halo table per level r
-    int32_t* halo2_tab[32] = {};             // radius-2 halo table (two steps per pass) per level r
+    int32_t* nbr_tab[32] = {};               // compact CA neighbour-tile table per level r
 };
 
 std::mutex g_mutex;
@@ -116,6 +116,13 @@ int ensure_device(int device, DeviceCtx** out) {
         }
         NBB_CUDA(cudaMemcpyToSymbol(c_local_pos, pos, sizeof(pos)));
         NBB_CUDA(cudaMemcpyToSymbol(c_local_idx, idx, sizeof(idx)));
+        // halo slots of the K-step compact pass (compact_pass.cuh)
+        nbbhost::HaloSlots hs;
+        NBB_TRY(nbbhost::halo_slots(&hs));
+        for (int k = 1; k <= kPassMaxK; ++k)
+            if (hs.upto[k] != pass_slots(k))
+                return fail(NBB_ERR_RUNTIME, "halo slots: layer sizes differ from the compiled pass shapes");
+        NBB_CUDA(cudaMemcpyToSymbol(c_slots, &hs, sizeof(hs)));
         NBB_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         NBB_CUDA(cudaMalloc(&c.partials, 4097 * sizeof(unsigned long long)));
         c.ready = true;
@@ -737,33 +744,17 @@ int compact_to_sectors(DeviceCtx* ctx, const nbb_config* cfg, const void* comp, 
     return NBB_OK;
 }
 
-// the per-level halo table of ca_compact_kernel, built once (then cached) per device
-int compact_halo_table(DeviceCtx* ctx, const nbb_config* cfg, const CompactCaArgs& a, const FastDiv& d,
-                       const int32_t** out) {
+// the per-level neighbour-tile table of ca_compact_pass_kernel (8 tile ordinals per tile),
+// built once (then cached) per device and level
+int compact_nbr_table(DeviceCtx* ctx, const nbb_config* cfg, const CompactCaArgs& a, const FastDiv& d,
+                      const int32_t** out) {
     std::lock_guard<std::mutex> lock(g_mutex);
-    int32_t*& t = ctx->halo_tab[cfg->r];
+    int32_t*& t = ctx->nbr_tab[cfg->r];
     if (!t) {
         NBB_CUDA(cudaMalloc(&t, (size_t)a.tiles * 8 * sizeof(int32_t)));
         const uint64_t n = (uint64_t)a.tiles * 8;
         const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sms * 16));
-        compact_halo_table_kernel<<<blocks, 256, 0, ctx->stream>>>(a, d, t);
-        NBB_CUDA(cudaGetLastError());
-        NBB_CUDA(cudaStreamSynchronize(ctx->stream));
-    }
-    *out = t;
-    return NBB_OK;
-}
-
-// the radius-2 halo table of ca_compact2_kernel, built once (then cached) per device and level
-int compact_halo2_table(DeviceCtx* ctx, const nbb_config* cfg, const CompactCaArgs& a, const FastDiv& d,
-                        const int32_t** out) {
-    std::lock_guard<std::mutex> lock(g_mutex);
-    int32_t*& t = ctx->halo2_tab[cfg->r];
-    if (!t) {
-        NBB_CUDA(cudaMalloc(&t, (size_t)a.tiles * kHalo2Stride * sizeof(int32_t)));
-        const uint64_t n = (uint64_t)a.tiles * kHalo2Stride;
-        const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->sms * 16));
-        compact_halo2_table_kernel<<<blocks, 256, 0, ctx->stream>>>(a, d, t);
+        compact_nbr_table_kernel<<<blocks, 256, 0, ctx->stream>>>(a, d, t);
         NBB_CUDA(cudaGetLastError());
         NBB_CUDA(cudaStreamSynchronize(ctx->stream));
     }
@@ -773,7 +764,7 @@ int compact_halo2_table(DeviceCtx* ctx, const nbb_config* cfg, const CompactCaAr
 
 // Launch with programmatic stream serialization (PDL): the kernel may start while the previous
 // kernel on the stream drains; kernels launched this way call griddepcontrol.wait before
-// touching memory the previous kernel writes (ca_compact_kernel: pdl_wait()).
+// touching memory the previous kernel writes (ca_compact_pass_kernel: pdl_wait()).
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args&&... args) {
     cudaLaunchConfig_t c = {};
@@ -789,142 +780,165 @@ cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaS
     return cudaLaunchKernelEx(&c, k, std::forward<Args>(args)...);
 }
 
-int launch_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* dst, uint16_t birth,
-                      uint16_t survive, cudaStream_t st) {
-    FastDiv div_hb;
-    const CompactCaArgs a = compact_args(cfg, src, dst, birth, survive, &div_hb);
-    const int32_t* tab;
-    NBB_CHECK(compact_halo_table(ctx, cfg, a, div_hb, &tab));
-    int occ;
-    const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
-    if (want == 0) return NBB_OK;
-    if (cfg->mode == NBB_MODE_BB) {
-        NBB_CHECK(occupancy<ca_compact_bb_kernel>(256, 0, &occ));
-        const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
-        NBB_CUDA(launch_pdl(ca_compact_bb_kernel, blocks, 256, st, a, div_hb, tab));
-        return NBB_OK;
+bool is_conway(uint16_t birth, uint16_t survive) {  // CaRule{} (B3/S23): its own instantiation
+    return birth == (1u << 3) && survive == ((1u << 2) | (1u << 3));
+}
+
+// the kernel of one pass: K steps, rule instantiation, walk (λ / BB / multi-GPU)
+template <int K, bool P2P, bool BB>
+using PassKernel = void (*)(CompactCaArgs, FastDiv, const int32_t*, P2PArgs);
+template <int K, bool P2P, bool BB>
+PassKernel<K, P2P, BB> pass_kernel(bool conway) {
+    return conway ? ca_compact_pass_kernel<K, true, P2P, BB> : ca_compact_pass_kernel<K, false, P2P, BB>;
+}
+template <bool P2P, bool BB>
+void (*pass_kernel_k(int k, bool conway))(CompactCaArgs, FastDiv, const int32_t*, P2PArgs) {
+    switch (k) {
+        case 1: return pass_kernel<1, P2P, BB>(conway);
+        case 2: return pass_kernel<2, P2P, BB>(conway);
+        case 3: return pass_kernel<3, P2P, BB>(conway);
+        default: return pass_kernel<4, P2P, BB>(conway);
     }
-    NBB_CHECK(occupancy<ca_compact_kernel<false>>(256, 0, &occ));
-    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
-    NBB_CUDA(launch_pdl(ca_compact_kernel<false>, blocks, 256, st, a, div_hb, tab, P2PArgs{}));
+}
+// resident CTAs per SM of a pass kernel (cached per kernel pointer)
+int pass_occupancy(const void* k, int* occ) {
+    static std::mutex m;
+    static std::vector<std::pair<const void*, int>> cache;
+    std::lock_guard<std::mutex> lock(m);
+    for (auto& e : cache)
+        if (e.first == k) {
+            *occ = e.second;
+            return NBB_OK;
+        }
+    NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, 256, 0));
+    if (*occ < 1) *occ = 1;
+    cache.push_back({k, *occ});
     return NBB_OK;
 }
 
-// two CA steps in one pass (ca_compact2_kernel); λ launch only
-int launch_ca_compact2(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* dst, uint16_t birth,
-                       uint16_t survive, cudaStream_t st) {
-    FastDiv div_hb;
-    const CompactCaArgs a = compact_args(cfg, src, dst, birth, survive, &div_hb);
-    const int32_t* tab;
-    NBB_CHECK(compact_halo2_table(ctx, cfg, a, div_hb, &tab));
-    const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
-    if (want == 0) return NBB_OK;
-    int occ;
-    const bool conway = birth == (1u << 3) && survive == ((1u << 2) | (1u << 3));  // CaRule{} (B3/S23)
-    if (conway) {
-        NBB_CHECK(occupancy<ca_compact2_kernel<true, false>>(256, 0, &occ));
-    } else {
-        NBB_CHECK(occupancy<ca_compact2_kernel<false, false>>(256, 0, &occ));
-    }
-    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
-    if (conway) {
-        NBB_CUDA(launch_pdl(ca_compact2_kernel<true, false>, blocks, 256, st, a, div_hb, tab, P2PArgs{}));
-    } else {
-        NBB_CUDA(launch_pdl(ca_compact2_kernel<false, false>, blocks, 256, st, a, div_hb, tab, P2PArgs{}));
-    }
+// steps per pass: cfg->pass_steps (0 = kDefaultPassSteps), 1 with NBB_FLAG_SINGLE_STEP
+constexpr int kDefaultPassSteps = 4;
+int max_pass_steps(const nbb_config* cfg) {
+    if (cfg->flags & NBB_FLAG_SINGLE_STEP) return 1;
+    const int k = cfg->pass_steps ? (int)cfg->pass_steps : kDefaultPassSteps;
+    return std::max(1, std::min(k, kPassMaxK));
+}
+int check_pass_steps(const nbb_config* cfg) {
+    if (cfg->pass_steps > (uint32_t)kPassMaxK)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "pass_steps: at most 4 CA steps per pass over the compact state");
     return NBB_OK;
 }
 
-// `steps` CA steps a <-> b on the compact state; the result lands in b for odd `steps`, in a
-// for even (as with one launch per step). λ launches without per-step timing run the steps in
-// pairs (ca_compact2_kernel); the number of pair launches is kept even (one pair split into two
-// single steps when needed) so the launch count's parity, and with it the result buffer, is
-// the same as stepping one by one.
+// The passes of `steps` steps with at most kmax per pass: the fewest passes, steps spread evenly.
+// With `parity`, the pass count has the parity of `steps` (the result then lands in the buffer a
+// run of single steps leaves it in: the reference's double buffering), one pass more if needed.
+std::vector<int> plan_passes(int32_t steps, int kmax, bool parity) {
+    std::vector<int> out;
+    if (steps <= 0) return out;
+    int64_t p = (steps + kmax - 1) / kmax;
+    if (parity && ((p ^ steps) & 1)) ++p;
+    for (int64_t i = 0; i < p; ++i) out.push_back((int)(steps / p + (i < steps % p ? 1 : 0)));
+    return out;
+}
+
+// One pass of k steps src -> dst on the compact state (λ or BB walk), this cfg's shard.
+int launch_pass(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* dst, int k, uint16_t birth,
+                uint16_t survive, cudaStream_t st) {
+    FastDiv div_hb;
+    const CompactCaArgs a = compact_args(cfg, src, dst, birth, survive, &div_hb);
+    const int32_t* tab;
+    NBB_CHECK(compact_nbr_table(ctx, cfg, a, div_hb, &tab));
+    const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
+    if (want == 0) return NBB_OK;
+    const bool bb = cfg->mode == NBB_MODE_BB;
+    auto kern = bb ? pass_kernel_k<false, true>(k, is_conway(birth, survive))
+                   : pass_kernel_k<false, false>(k, is_conway(birth, survive));
+    int occ;
+    NBB_CHECK(pass_occupancy((const void*)kern, &occ));
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->sms * occ));
+    NBB_CUDA(launch_pdl(kern, blocks, 256, st, a, div_hb, tab, P2PArgs{}));
+    return NBB_OK;
+}
+
+// `steps` CA steps a <-> b on the compact state in passes (plan_passes); *result_in_b says where
+// the result is; stats (optional) counts the launches.
 int run_ca_compact(DeviceCtx* ctx, const nbb_config* cfg, void* d_a, void* d_b, int32_t steps, uint16_t birth,
-                   uint16_t survive, cudaStream_t st) {
-    int32_t pairs = 0;
-    if (cfg->mode != NBB_MODE_BB && !cfg->timing && !(cfg->flags & NBB_FLAG_SINGLE_STEP)) {
-        pairs = steps / 2;
-        if (pairs & 1) --pairs;
+                   uint16_t survive, cudaStream_t st, bool parity, nbb_pass_stats* stats) {
+    NBB_CHECK(check_pass_steps(cfg));
+    const std::vector<int> passes = plan_passes(steps, cfg->timing ? 1 : max_pass_steps(cfg), parity);
+    nbb_pass_stats ps{};
+    for (size_t i = 0; i < passes.size(); ++i) {
+        NBB_CHECK(launch_pass(ctx, cfg, (i & 1) ? d_b : d_a, (i & 1) ? d_a : d_b, passes[i], birth, survive, st));
+        ++ps.passes;
+        ++ps.by_steps[passes[i]];
     }
-    int64_t launches = 0;
-    auto src = [&] { return (launches & 1) ? d_b : d_a; };
-    auto dst = [&] { return (launches & 1) ? d_a : d_b; };
-    for (int32_t i = 0; i < pairs; ++i, ++launches)
-        NBB_CHECK(launch_ca_compact2(ctx, cfg, src(), dst(), birth, survive, st));
-    for (int32_t i = 2 * pairs; i < steps; ++i, ++launches)
-        NBB_CHECK(launch_ca_compact(ctx, cfg, src(), dst(), birth, survive, st));
+    ps.result_in_b = (int32_t)(passes.size() & 1);
+    if (stats) *stats = ps;
     return NBB_OK;
 }
-// The multi-GPU step loop: `steps` steps as passes j = first_pass, first_pass + 1, ... (two
-// steps per pass when `pairs`, the last pass single when `steps` is odd; one step per pass
-// otherwise). Pass j reads d_buf[j & 1], writes d_buf[(j + 1) & 1] and waits for world x j
-// arrivals.
-int p2p_passes(const nbb_config* cfg, int64_t first_pass, int32_t steps, bool pairs, uint16_t birth,
-               uint16_t survive, const nbb_p2p* p2p, cudaStream_t stream) {
+
+// The multi-GPU pass loop: `steps` steps in passes j = first_pass, first_pass + 1, ... of up to
+// kmax steps (plan_passes, no parity constraint: pass j reads d_buf[j & 1] and writes
+// d_buf[(j + 1) & 1] whatever its step count). Pass j waits for world x j arrivals.
+int p2p_passes(const nbb_config* cfg, int64_t first_pass, int32_t steps, int kmax, uint16_t birth,
+               uint16_t survive, const nbb_p2p* p2p, cudaStream_t stream, nbb_pass_stats* stats) {
     if (!cfg || !p2p) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
     if (steps < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "run_ca: steps must be non-negative");
     if (first_pass < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: first_step must be non-negative");
     NBB_CHECK(compact_workload_check(cfg));
+    NBB_CHECK(check_pass_steps(cfg));
     if (p2p->world < 1 || p2p->world > kMaxP2P || p2p->rank < 0 || p2p->rank >= p2p->world)
         return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: need 1 <= world <= 8 and 0 <= rank < world");
-    if (!p2p->d_buf[0] || !p2p->d_buf[1] || !p2p->d_peer_buf[0] || !p2p->d_peer_buf[1] ||
-        !p2p->d_halo_owner || !p2p->d_sync || !p2p->d_peer_flag)
+    if (!p2p->d_buf[0] || !p2p->d_buf[1] || !p2p->d_peer_buf[0] || !p2p->d_peer_buf[1] || !p2p->d_sync ||
+        !p2p->d_peer_flag)
         return fail(NBB_ERR_INVALID_ARGUMENT, "p2p: null device array");
     DeviceCtx* ctx;
     NBB_CHECK(ensure_device(cfg->device, &ctx));
     FastDiv div_hb;
     CompactCaArgs a = compact_args(cfg, p2p->d_buf[0], p2p->d_buf[1], birth, survive, &div_hb);
-    const int32_t *tab, *tab2 = nullptr;
-    NBB_CHECK(compact_halo_table(ctx, cfg, a, div_hb, &tab));
-    if (pairs && steps >= 2) NBB_CHECK(compact_halo2_table(ctx, cfg, a, div_hb, &tab2));
+    // the owner of a halo cell is its tile's ordinal / chunk: the shard must be the reference's
+    // contiguous worker chunk (dispatch.cpp:419-427) of this rank, as every peer assumes
+    const uint32_t chunk = (a.tiles + (uint32_t)p2p->world - 1) / (uint32_t)p2p->world;
+    const uint64_t want_b = std::min<uint64_t>((uint64_t)chunk * (uint64_t)p2p->rank, a.tiles);
+    const uint64_t want_e = std::min<uint64_t>(want_b + chunk, a.tiles);
+    if (cfg->shard_count == 0 || a.tile_begin != want_b || a.tile_end != want_e)
+        return fail(NBB_ERR_INVALID_ARGUMENT,
+                    "p2p: the shard must be the rank's contiguous chunk of ceil(tiles / world) tiles: [" +
+                        std::to_string(want_b) + ", " + std::to_string(want_e) + ")");
+    const int32_t* tab;
+    NBB_CHECK(compact_nbr_table(ctx, cfg, a, div_hb, &tab));
     P2PArgs p;
-    p.halo_owner = (const uint8_t*)p2p->d_halo_owner;
     p.sync = (unsigned int*)p2p->d_sync;
     p.peer_flag = (unsigned int* const*)p2p->d_peer_flag;
     p.timeout_ms = p2p->timeout_ms ? p2p->timeout_ms : 20000u;
     p.world = p2p->world;
     p.rank = p2p->rank;
-    p.chunk = (a.tiles + (uint32_t)p2p->world - 1) / (uint32_t)p2p->world;  // the shard split
-    {   // the rank's whole tile rows (9 compact rows of W each): offsets there are its own
-        const uint32_t fr = (a.tile_begin + a.Hb - 1) / a.Hb, fe = a.tile_end / a.Hb;
-        p.own_lo = fe > fr ? fr * 9u * a.W : 0u;
-        p.own_hi = fe > fr ? fe * 9u * a.W : 0u;
-    }
-    const bool conway = birth == (1u << 3) && survive == ((1u << 2) | (1u << 3));
-    int occ1, occ2;
-    NBB_CHECK(occupancy<ca_compact_kernel<true>>(256, 0, &occ1));
-    if (conway) {
-        NBB_CHECK(occupancy<ca_compact2_kernel<true, true>>(256, 0, &occ2));
-    } else {
-        NBB_CHECK(occupancy<ca_compact2_kernel<false, true>>(256, 0, &occ2));
-    }
+    p.div_chunk.d = chunk;
+    nbbhost::fastdiv_magic(chunk, &p.div_chunk.m, &p.div_chunk.s);
+    const bool conway = is_conway(birth, survive);
     // every rank launches (and arrives) even with an empty shard: one CTA at least; at most one
     // resident wave, so CTAs spinning in the wait never keep a CTA of the same pass off an SM
     const uint64_t want = std::max<uint64_t>(1, (a.tile_end - a.tile_begin + 7) / 8);
-    const unsigned blocks1 = (unsigned)std::min<uint64_t>(want, (uint64_t)ctx->sms * occ1);
-    const unsigned blocks2 = (unsigned)std::min<uint64_t>(want, (uint64_t)ctx->sms * occ2);
-    // the pass loop lives here, not in the caller: back to back on the stream, no per-pass host
-    // arguments beyond the ping-pong parity
+    const std::vector<int> passes = plan_passes(steps, kmax, false);
+    nbb_pass_stats ps{};
     int64_t j = first_pass;
-    for (int32_t left = steps; left > 0; ++j) {
+    for (size_t i = 0; i < passes.size(); ++i, ++j) {
         const int par = (int)(j & 1);
         a.src = (const long long*)p2p->d_buf[par];
         a.dst = (long long*)p2p->d_buf[par ^ 1];
         p.peer_src = (const long long* const*)p2p->d_peer_buf[par];
         p.wait_target = (unsigned int)((uint64_t)p2p->world * (uint64_t)j);
-        if (pairs && left >= 2) {
-            if (conway) {
-                NBB_CUDA(launch_pdl(ca_compact2_kernel<true, true>, blocks2, 256, stream, a, div_hb, tab2, p));
-            } else {
-                NBB_CUDA(launch_pdl(ca_compact2_kernel<false, true>, blocks2, 256, stream, a, div_hb, tab2, p));
-            }
-            left -= 2;
-        } else {
-            NBB_CUDA(launch_pdl(ca_compact_kernel<true>, blocks1, 256, stream, a, div_hb, tab, p));
-            left -= 1;
-        }
+        p.first_pass = i == 0 ? 1u : 0u;
+        auto kern = pass_kernel_k<true, false>(passes[i], conway);
+        int occ;
+        NBB_CHECK(pass_occupancy((const void*)kern, &occ));
+        const unsigned blocks = (unsigned)std::min<uint64_t>(want, (uint64_t)ctx->sms * occ);
+        NBB_CUDA(launch_pdl(kern, blocks, 256, stream, a, div_hb, tab, p));
+        ++ps.passes;
+        ++ps.by_steps[passes[i]];
     }
+    ps.result_in_b = (int32_t)(j & 1);
+    if (stats) *stats = ps;
     return NBB_OK;
 }
 }  // namespace
@@ -1278,18 +1292,20 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
                                                                         (int64_t)cs.n, (uint32_t)cs.W);
         NBB_CUDA(cudaGetLastError());
         if (cfg->timing) {  // per-step launch times: one launch per step
+            NBB_CHECK(check_pass_steps(cfg));
             for (int s = 0; s < steps; ++s) {
                 Timer t(true, L.stream);
-                NBB_CHECK(launch_ca_compact(L.ctx, cfg, ca, cb, birth, survive, L.stream));
+                NBB_CHECK(launch_pass(L.ctx, cfg, ca, cb, 1, birth, survive, L.stream));
                 const uint64_t us = t.stop_micros();
                 if (per_step) fill_report(cfg, &per_step[s], us);
                 std::swap(ca, cb);
             }
-        } else {
-            NBB_CHECK(run_ca_compact(L.ctx, cfg, ca, cb, steps, birth, survive, L.stream));
+        } else {  // passes of up to 4 steps; the result in whichever buffer the last pass wrote
+            nbb_pass_stats ps;
+            NBB_CHECK(run_ca_compact(L.ctx, cfg, ca, cb, steps, birth, survive, L.stream, false, &ps));
             if (per_step)
                 for (int s = 0; s < steps; ++s) fill_report(cfg, &per_step[s], 0);
-            if (steps & 1) std::swap(ca, cb);
+            if (ps.result_in_b) std::swap(ca, cb);
         }
         if (h_out) {  // member sectors straight into the zeroed pinned output, row by row
             compact_to_rows_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)ca, h_out,
@@ -1553,29 +1569,50 @@ int nbb_gpu_ca_compact_step_dev(const nbb_config* cfg, const void* d_src, void* 
     DeviceCtx* ctx;
     NBB_CHECK(ensure_device(cfg->device, &ctx));
     Timer t(cfg->timing != 0, (cudaStream_t)stream);
-    NBB_CHECK(launch_ca_compact(ctx, cfg, d_src, d_dst, birth, survive, (cudaStream_t)stream));
+    NBB_CHECK(launch_pass(ctx, cfg, d_src, d_dst, 1, birth, survive, (cudaStream_t)stream));
     fill_report(cfg, report, t.stop_micros());
     return NBB_OK;
 }
 
 int nbb_gpu_ca_compact_run_dev(const nbb_config* cfg, void* d_a, void* d_b, int32_t steps, uint16_t birth,
                                uint16_t survive, void* stream) {
+    return nbb_gpu_ca_compact_passes_dev(cfg, d_a, d_b, steps, birth, survive, 1, stream, nullptr);
+}
+
+int nbb_gpu_ca_compact_passes_dev(const nbb_config* cfg, void* d_a, void* d_b, int32_t steps, uint16_t birth,
+                                  uint16_t survive, int32_t parity, void* stream, nbb_pass_stats* stats) {
     if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
     if (steps < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "run_ca: steps must be non-negative");
     NBB_CHECK(compact_workload_check(cfg, true));
     DeviceCtx* ctx;
     NBB_CHECK(ensure_device(cfg->device, &ctx));
-    return run_ca_compact(ctx, cfg, d_a, d_b, steps, birth, survive, (cudaStream_t)stream);
+    return run_ca_compact(ctx, cfg, d_a, d_b, steps, birth, survive, (cudaStream_t)stream, parity != 0, stats);
+}
+
+int nbb_gpu_pass_plan(const nbb_config* cfg, int32_t steps, int32_t parity, nbb_pass_stats* stats) {
+    if (!cfg || !stats) return fail(NBB_ERR_INVALID_ARGUMENT, "null argument");
+    if (steps < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "run_ca: steps must be non-negative");
+    NBB_CHECK(check_pass_steps(cfg));
+    const std::vector<int> passes = plan_passes(steps, cfg->timing ? 1 : max_pass_steps(cfg), parity != 0);
+    *stats = nbb_pass_stats{};
+    for (int k : passes) {
+        ++stats->passes;
+        ++stats->by_steps[k];
+    }
+    stats->result_in_b = (int32_t)(passes.size() & 1);
+    return NBB_OK;
 }
 
 int nbb_gpu_ca_compact_p2p_dev(const nbb_config* cfg, int64_t first_step, int32_t steps, uint16_t birth,
                                uint16_t survive, const nbb_p2p* p2p, void* stream) {
-    return p2p_passes(cfg, first_step, steps, false, birth, survive, p2p, (cudaStream_t)stream);
+    return p2p_passes(cfg, first_step, steps, 1, birth, survive, p2p, (cudaStream_t)stream, nullptr);
 }
 
 int nbb_gpu_ca_compact_p2p_passes_dev(const nbb_config* cfg, int64_t first_pass, int32_t steps, uint16_t birth,
                                       uint16_t survive, const nbb_p2p* p2p, void* stream) {
-    return p2p_passes(cfg, first_pass, steps, true, birth, survive, p2p, (cudaStream_t)stream);
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    return p2p_passes(cfg, first_pass, steps, max_pass_steps(cfg), birth, survive, p2p, (cudaStream_t)stream,
+                      nullptr);
 }
 
 int nbb_gpu_p2p_check(const nbb_p2p* p2p, void* stream) {
@@ -1669,11 +1706,7 @@ int nbb_gpu_release(void) {
             c.bufs[i] = nullptr;
             c.buf_bytes[i] = 0;
         }
-        for (auto& t : c.halo_tab) {
-            if (t) cudaFree(t);
-            t = nullptr;
-        }
-        for (auto& t : c.halo2_tab) {
+        for (auto& t : c.nbr_tab) {
             if (t) cudaFree(t);
             t = nullptr;
         }

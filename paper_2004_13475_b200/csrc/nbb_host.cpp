@@ -1,7 +1,9 @@
 // nbb_host.cpp — host-side logic of the engine; see nbb_host.hpp.
 #include "nbb_host.hpp"
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <random>
@@ -493,4 +495,96 @@ void fastdiv_magic(uint32_t d, uint32_t* m, uint32_t* s) {
     *s = l;
 }
 
+}  // namespace nbbhost
+
+// ---- halo slots (see nbb_host.hpp) ---------------------------------------------------------
+namespace nbbhost {
+namespace {
+uint32_t tile_local_index_host(uint32_t x, uint32_t y) {  // λ⁻¹ inside a ρ = 32 gasket tile
+    auto b3 = [](uint32_t bits) {  // even bits of `bits` read as base-3 digits in {0, 1}
+        uint32_t v = 0, p = 1;
+        for (int j = 0; j < 16; j += 2, p *= 3) v += ((bits >> j) & 1u) * p;
+        return v;
+    };
+    const uint32_t wx = b3(x) + b3(y), wy = b3(x >> 1) + b3(y >> 1);
+    return wy * 27u + wx;
+}
+}  // namespace
+
+Error halo_slots(HaloSlots* out) {
+    constexpr int L = 13, T = 32, K = kPassMaxK;
+    const int64_t n = int64_t(1) << L, nb = n / T;
+    auto member = [&](int64_t x, int64_t y) { return x >= 0 && y >= 0 && x < n && y < n && (x & y) == x; };
+    // the first 8 slots keep the order of the one-step halo (compact_rows_step's h bits)
+    const int h1x[8] = {-1, 0, 1, -1, 32, 32, 32, 0}, h1y[8] = {-1, -1, -1, 31, 30, 31, 32, 32};
+    constexpr int E = T + 2 * K;  // the tile and a K-cell frame, (x, y) -> (x + K, y + K)
+    std::vector<int> best(E * E, 99);
+    std::vector<int> layer(E * E);
+    for (int64_t by = 0; by < nb; ++by)
+        for (int64_t bx = 0; bx < nb; ++bx) {
+            if ((bx & by) != bx) continue;
+            std::fill(layer.begin(), layer.end(), -1);
+            for (int y = 0; y < T; ++y)
+                for (int x = 0; x < T; ++x)
+                    if ((x & y) == x) layer[(y + K) * E + x + K] = 0;
+            for (int d = 1; d <= K; ++d)
+                for (int y = -K; y < T + K; ++y)
+                    for (int x = -K; x < T + K; ++x) {
+                        const int i = (y + K) * E + x + K;
+                        if (layer[i] >= 0 || !member(bx * T + x, by * T + y)) continue;
+                        bool adj = false;
+                        for (int dy = -1; dy <= 1 && !adj; ++dy)
+                            for (int dx = -1; dx <= 1 && !adj; ++dx) {
+                                const int qx = x + dx, qy = y + dy;
+                                if ((dx || dy) && qx >= -K && qy >= -K && qx < T + K && qy < T + K)
+                                    adj = layer[(qy + K) * E + qx + K] == d - 1;
+                            }
+                        if (adj) layer[i] = d;
+                    }
+            for (int i = 0; i < E * E; ++i)
+                if (layer[i] > 0) best[i] = std::min(best[i], layer[i]);
+        }
+    std::vector<std::pair<int, int>> pos;  // (layer, index)
+    for (int i = 0; i < E * E; ++i)
+        if (best[i] <= K) pos.push_back({best[i], i});
+    std::vector<int> order;
+    for (int k = 0; k < 8; ++k) order.push_back((h1y[k] + K) * E + h1x[k] + K);
+    std::stable_sort(pos.begin(), pos.end(), [](auto a, auto b) { return a.first < b.first; });
+    for (auto& pi : pos)
+        if (std::find(order.begin(), order.end(), pi.second) == order.end()) order.push_back(pi.second);
+    if ((int)order.size() > kPassSlots || (int)pos.size() != (int)order.size())
+        return err(NBB_ERR_RUNTIME, "halo slots: unexpected layer structure");
+    HaloSlots h{};
+    h.count = (int32_t)order.size();
+    for (int d = 0; d <= K; ++d)
+        for (auto& pi : pos) h.upto[d] += pi.first <= d;
+    for (int s = 0; s < h.count; ++s) {
+        const int x = order[s] % E - K, y = order[s] / E - K;
+        if (s < 8 ? best[order[s]] != 1 : best[order[s]] < 2)
+            return err(NBB_ERR_RUNTIME, "halo slots: H_1 is not the one-step halo");
+        h.x[s] = (int8_t)x;
+        h.y[s] = (int8_t)y;
+        const int dx = x < 0 ? -1 : x >= T ? 1 : 0, dy = y < 0 ? -1 : y >= T ? 1 : 0;
+        const int d9 = (dy + 1) * 3 + dx + 1;
+        h.dir[s] = (uint8_t)(d9 > 4 ? d9 - 1 : d9);
+        h.li[s] = (uint8_t)tile_local_index_host((uint32_t)(x - dx * T), (uint32_t)(y - dy * T));
+        for (int t = 0; t < h.count; ++t) {
+            const int tx = order[t] % E - K, ty = order[t] / E - K;
+            if (t != s && std::abs(tx - x) <= 1 && std::abs(ty - y) <= 1) {
+                if (t < 32) h.nb_lo[s] |= 1u << t; else h.nb_hi[s] |= 1u << (t - 32);
+            }
+        }
+        for (int qy = y - 1; qy <= y + 1; ++qy)
+            for (int qx = x - 1; qx <= x + 1; ++qx) {
+                if (qx < 0 || qy < 0 || qx >= T || qy >= T || (qx & qy) != qx) continue;
+                if (s >= 8) return err(NBB_ERR_RUNTIME, "halo slots: in-tile neighbour beyond H_1");
+                if (qy == 0) h.m0[s] |= 1u << qx;
+                else if (qy == 30) h.m30[s] |= 1u << qx;
+                else if (qy == 31) h.m31[s] |= 1u << qx;
+                else return err(NBB_ERR_RUNTIME, "halo slots: in-tile neighbour outside rows 0/30/31");
+            }
+    }
+    *out = h;
+    return {};
+}
 }  // namespace nbbhost

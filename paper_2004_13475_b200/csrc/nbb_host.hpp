@@ -69,6 +69,29 @@ void local_cell_table(const nbb_spec& s, int edge, int16_t* out);
 Error write_compact(const char* path, const nbb_spec& s, int level, const int64_t* values);
 Error read_compact(const char* path, const nbb_spec& s, int* level, int64_t* values, uint64_t capacity);
 
+// ---- halo slots of the multi-step compact CA pass (compact_pass.cuh) ----------------------
+// The member cells outside a ρ = 32 gasket tile that can reach one of its members within K <= 4
+// steps: the chain layers H_1 (member neighbours of the tile's members), H_2 (member neighbours
+// of H_1 outside the tile), ... found by brute force over every tile of level 13 (the 3 x 3
+// tile neighbourhoods repeat by self-similarity), each position labelled with its smallest
+// layer d over all tiles and sorted by d, so the slots of a K-step pass are a prefix
+// (8 / 22 / 36 / 58 for K = 1..4). Per slot: tile-local position, the neighbouring tile it lies
+// in (0..7, (dy+1)*3 + dx+1 with the centre skipped), its local compact index there, the
+// other slots adjacent to it (bit mask), and — for H_1 — its in-tile member neighbours as bit
+// masks over tile rows 0, 30 and 31 (the only rows they touch).
+constexpr int kPassMaxK = 4;
+constexpr int kPassSlots = 64;
+struct HaloSlots {
+    int32_t count;                 // slots with layer <= kPassMaxK
+    int32_t upto[kPassMaxK + 1];   // upto[d] = slots with layer <= d
+    int8_t x[kPassSlots], y[kPassSlots];
+    uint8_t dir[kPassSlots];       // neighbouring tile, 0..7
+    uint8_t li[kPassSlots];        // local compact index (ωy_l * 27 + ωx_l) in that tile
+    uint32_t nb_lo[kPassSlots], nb_hi[kPassSlots];  // adjacent slots
+    uint32_t m0[8], m30[8], m31[8];                 // H_1: in-tile neighbours in rows 0, 30, 31
+};
+Error halo_slots(HaloSlots* out);
+
 // precomputed fast division magic (see common.cuh FastDiv), exact for x < 2^31
 void fastdiv_magic(uint32_t d, uint32_t* m, uint32_t* s);
 

@@ -86,6 +86,24 @@ def ca_compact_run_dev(config: DispatchConfig, d_a: int, d_b: int, steps: int, r
                                              rule.birth, rule.survive, _vp(stream)))
 
 
+def ca_compact_passes_dev(config: DispatchConfig, d_a: int, d_b: int, steps: int, rule: CaRule = CaRule(),
+                          stream: int = 0, parity: bool = False) -> "_abi.NbbPassStats":
+    """`steps` steps in passes of up to config.pass_steps steps (default 4); without `parity`
+    the fewest passes, the result in d_b iff the returned stats.result_in_b."""
+    st = _abi.NbbPassStats()
+    _check(_lib().nbb_gpu_ca_compact_passes_dev(ctypes.byref(config.to_c()), _vp(d_a), _vp(d_b), steps,
+                                                rule.birth, rule.survive, 1 if parity else 0, _vp(stream),
+                                                ctypes.byref(st)))
+    return st
+
+
+def pass_plan(config: DispatchConfig, steps: int, parity: bool = False) -> "_abi.NbbPassStats":
+    """Host only: the passes a compact CA run of `steps` steps issues."""
+    st = _abi.NbbPassStats()
+    _check(_lib().nbb_gpu_pass_plan(ctypes.byref(config.to_c()), steps, 1 if parity else 0, ctypes.byref(st)))
+    return st
+
+
 def reduction_compact_dev(config: DispatchConfig, d_compact: int, d_value: int, stream: int = 0) -> WorkReport:
     rep = _abi.NbbReport()
     _check(_lib().nbb_gpu_reduction_compact_dev(ctypes.byref(config.to_c()), _vp(d_compact),

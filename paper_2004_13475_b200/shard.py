@@ -414,11 +414,10 @@ class P2PCompactCA:
                                        device=dev) for b in (0, 1)]
         self._peer_flag = torch.tensor([peers[r][2] for r in range(plan.world)], dtype=torch.int64,
                                        device=dev)
-        self._owner = torch.from_numpy(plan.halo_owner_table()).to(dev)
         self.buffers = [torch.as_tensor(_DevArray(p, self.count), device=dev) for p in self._own[:2]]
         self._args = _abi.NbbP2P(plan.world, plan.rank, (ctypes.c_void_p * 2)(*self._own[:2]),
                                  (ctypes.c_void_p * 2)(*(t.data_ptr() for t in self._peer_buf)),
-                                 self._owner.data_ptr(), self._own[2], self._peer_flag.data_ptr(),
+                                 None, self._own[2], self._peer_flag.data_ptr(),
                                  timeout_ms)
         self.step_index = 0
         self.pass_index = 0  # passes (launches) run so far: the state lives in buffer pass_index & 1
@@ -439,16 +438,23 @@ class P2PCompactCA:
         return self.buffers[self.pass_index & 1]
 
     def run(self, config, rule, steps: int, stream) -> None:
-        """`steps` steps issued back to back by the library: passes of two steps (the last one
-        single for odd `steps`), or one kernel per step with two_step=False."""
+        """`steps` steps issued back to back by the library: passes of up to config.pass_steps
+        steps (default 4; nbb_gpu_pass_plan names them), or one kernel per step with
+        two_step=False."""
         import ctypes
-        c = self.plan.local_config(config).to_c()
+        local = self.plan.local_config(config)
+        c = local.to_c()
         fn = (self.lib.nbb_gpu_ca_compact_p2p_passes_dev if self.two_step
               else self.lib.nbb_gpu_ca_compact_p2p_dev)
         _check(fn(ctypes.byref(c), self.pass_index, steps, rule.birth, rule.survive,
                   ctypes.byref(self._args), ctypes.c_void_p(stream)))
         self.step_index += steps
-        self.pass_index += (steps // 2 + steps % 2) if self.two_step else steps
+        if self.two_step:
+            st = _abi.NbbPassStats()
+            _check(self.lib.nbb_gpu_pass_plan(ctypes.byref(c), steps, 0, ctypes.byref(st)))
+            self.pass_index += st.passes
+        else:
+            self.pass_index += steps
 
     def step(self, config, rule, stream) -> None:
         self.run(config, rule, 1, stream)

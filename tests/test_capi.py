@@ -38,7 +38,34 @@ def test_library_exports_every_declared_symbol():
     for name in names:
         assert hasattr(lib, name), name
         assert name in _abi.SIGNATURES, f"{name} missing from _abi.SIGNATURES"
-    assert lib.nbb_gpu_abi_version() == 2
+    assert lib.nbb_gpu_abi_version() == 3
+
+
+@pytest.mark.parametrize("kmax", [1, 2, 3, 4])
+def test_pass_plan(kmax):
+    """nbb_gpu_pass_plan (host only): the passes a compact CA run issues — every step counted once,
+    at most pass_steps per pass, the fewest passes (ceil(steps / K)) without parity; with parity
+    the pass count has the parity of `steps` (result where single steps leave it), one more pass
+    at most."""
+    from paper_2004_13475_b200 import device as dev
+    c = _cfg(r=10, rho=32, pass_steps=kmax)
+    for steps in range(0, 41):
+        for parity in (False, True):
+            st = dev.pass_plan(c, steps, parity)
+            by = list(st.by_steps)
+            assert sum(k * by[k] for k in range(5)) == steps
+            assert all(by[k] == 0 for k in range(kmax + 1, 5))
+            assert st.passes == sum(by)
+            fewest = -(-steps // kmax)
+            if parity:
+                assert st.passes in (fewest, fewest + 1) and st.passes % 2 == steps % 2
+            else:
+                assert st.passes == fewest
+            assert st.result_in_b == st.passes % 2
+    single = dev.pass_plan(_cfg(r=10, rho=32, flags=_abi.FLAG_SINGLE_STEP), 7)
+    assert single.passes == 7 and single.by_steps[1] == 7
+    with pytest.raises(nbb.InvalidArgument):
+        dev.pass_plan(_cfg(r=10, rho=32, pass_steps=5), 4)
 
 
 def test_library_is_sm100a_and_native():
