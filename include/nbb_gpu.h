@@ -101,7 +101,7 @@ typedef struct nbb_config {
     uint64_t shard_count;
     uint32_t flags;     /* NBB_FLAG_* */
     uint32_t pass_steps; /* compact-state CA: at most this many steps per pass over the
-                          * state (1..4; 0 = 4). See nbb_gpu_ca_compact_passes_dev. */
+                          * state (1..8; 0 = 8). See nbb_gpu_ca_compact_passes_dev. */
 } nbb_config;
 
 /* nbb_config.flags
@@ -111,16 +111,22 @@ typedef struct nbb_config {
  *   buffers the kernels then move only member sectors over PCIe (zero-copy) instead of
  *   the whole n*n grid. Without the flag out_grid is always written in full. */
 #define NBB_FLAG_OUT_ZEROED 1u
-/* NBB_FLAG_COMPACT_STATE: nbb_gpu_ca keeps the CA state on the device in the compact
- *   (λ-ordered CompactGrid) layout between the two conversions — int64 values, every
- *   byte a member (gasket, cell_width 8, r >= 5). Lambda mode walks the orthotope (the
- *   compact array's own order); BB mode walks the bounding box, culls empty tiles and
- *   addresses member tiles through λ⁻¹ (the comparison launch; unsharded). */
+/* Device state of nbb_gpu_ca. By default (neither flag) the CA state lives on the device in the
+ *   compact (λ-ordered CompactGrid) layout between the two conversions — int64 values, every
+ *   byte a member — whenever that layout serves the call: the gasket, cell_width 8,
+ *   5 <= r <= 18, kernel AUTO, no shard. Lambda mode walks the orthotope (the compact array's
+ *   own order); BB mode walks the bounding box, culls empty tiles and addresses member tiles
+ *   through λ⁻¹ (the comparison launch). Other calls use the embedded grid of cell_width.
+ * NBB_FLAG_COMPACT_STATE: require the compact state (NBB_ERR_INVALID_ARGUMENT if the call
+ *   cannot use it).
+ * NBB_FLAG_EMBEDDED_STATE: opt out — step the reference's embedded n x n layout of cell_width
+ *   (int64, uint8 or 1-bit) with the tile / per-cell kernels (kernel, strategy, backend). */
 #define NBB_FLAG_COMPACT_STATE 2u
+#define NBB_FLAG_EMBEDDED_STATE 8u
 /* NBB_FLAG_SINGLE_STEP: compact-state CA runs (nbb_gpu_ca with NBB_FLAG_COMPACT_STATE,
  *   nbb_gpu_ca_compact_*_dev) launch one kernel per step (= pass_steps 1). Without it,
- *   untimed runs advance up to pass_steps (default 4) steps per pass over the state
- *   (ca_compact_pass_kernel: the tile and its radius-K halo are read once, the intermediate
+ *   untimed runs advance up to pass_steps (default 8) steps per pass over the state
+ *   (ca_compact_sliced_kernel: the tile and its radius-K halo are read once, the intermediate
  *   steps stay on chip) — the same result. */
 #define NBB_FLAG_SINGLE_STEP 4u
 
@@ -252,7 +258,7 @@ int nbb_gpu_ca_compact_run_dev(const nbb_config* cfg, void* d_a, void* d_b, int3
 /* What a pass sequence did: launches, launches per step count, where the result is. */
 typedef struct nbb_pass_stats {
     int32_t passes;       /* kernel launches (passes over the state)                  */
-    int32_t by_steps[5];  /* by_steps[k]: passes that advanced k steps (k = 1..4)      */
+    int32_t by_steps[9];  /* by_steps[k]: passes that advanced k steps (k = 1..8)      */
     int32_t result_in_b;  /* 1: the state after `steps` steps is in d_b; 0: in d_a     */
 } nbb_pass_stats;
 /* The same run with parity = 0: the fewest passes (ceil(steps / pass_steps)), the result in
@@ -302,8 +308,8 @@ typedef struct nbb_p2p {
 } nbb_p2p;
 int nbb_gpu_ca_compact_p2p_dev(const nbb_config* cfg, int64_t first_step, int32_t steps,
                                uint16_t birth, uint16_t survive, const nbb_p2p* p2p, void* stream);
-/* The same step sequence in PASSES of up to cfg->pass_steps steps (default 4; the
- * ca_compact_pass_kernel over peer memory: the radius-K halo read once, the intermediate
+/* The same step sequence in PASSES of up to cfg->pass_steps steps (default 8; the
+ * ca_compact_sliced_kernel over peer memory: the radius-K halo read once, the intermediate
  * steps kept on chip): ceil(steps / K) passes, steps spread evenly. Pass j (first_pass <= j)
  * reads d_buf[j & 1], writes d_buf[(j + 1) & 1] and waits for world x j arrivals; first_pass
  * must equal the number of passes (either entry point: a step of nbb_gpu_ca_compact_p2p_dev

@@ -100,6 +100,11 @@ struct DispatchConfig {  // dispatch.hpp:25-38
     int cell_width = 8;  // device-side extensions
     int kernel = NBB_KERNEL_AUTO;
     int device = 0;
+    // Device state of run_ca (nbb_gpu.h): Auto = the compact (λ-ordered) state whenever it
+    // serves the call, Compact = require it, Embedded = the reference's n x n layout.
+    enum class State { Auto, Compact, Embedded } state = State::Auto;
+    std::uint32_t flags = 0;       // further NBB_FLAG_* (e.g. NBB_FLAG_OUT_ZEROED)
+    std::uint32_t pass_steps = 0;  // compact state: steps per pass, 1..8 (0 = 8)
 
     nbb_config c() const {
         nbb_config out;
@@ -116,6 +121,9 @@ struct DispatchConfig {  // dispatch.hpp:25-38
         out.cell_width = cell_width;
         out.kernel = kernel;
         out.device = device;
+        out.flags = flags | (state == State::Compact ? NBB_FLAG_COMPACT_STATE : 0u) |
+                    (state == State::Embedded ? NBB_FLAG_EMBEDDED_STATE : 0u);
+        out.pass_steps = pass_steps;
         return out;
     }
     void validate() const {

@@ -67,6 +67,7 @@ class NbbConfig(Structure):
 FLAG_OUT_ZEROED = 1
 FLAG_COMPACT_STATE = 2
 FLAG_SINGLE_STEP = 4
+FLAG_EMBEDDED_STATE = 8
 
 
 class NbbReport(Structure):
@@ -91,7 +92,7 @@ class NbbPassStats(Structure):
     """nbb_pass_stats (nbb_gpu.h): the passes a compact CA run issued."""
     _fields_ = [
         ("passes", c_int32),
-        ("by_steps", c_int32 * 5),
+        ("by_steps", c_int32 * 9),
         ("result_in_b", c_int32),
     ]
 

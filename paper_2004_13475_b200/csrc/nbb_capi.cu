@@ -29,6 +29,7 @@
 #include "bits_kernels.cuh"
 #include "compact_kernels.cuh"
 #include "compact_pass.cuh"
+#include "compact_sliced.cuh"
 #include "util_kernels.cuh"
 
 using namespace nbbgpu;
@@ -123,6 +124,14 @@ int ensure_device(int device, DeviceCtx** out) {
             if (hs.upto[k] != pass_slots(k))
                 return fail(NBB_ERR_RUNTIME, "halo slots: layer sizes differ from the compiled pass shapes");
         NBB_CUDA(cudaMemcpyToSymbol(c_slots, &hs, sizeof(hs)));
+        nbbhost::SliceSlots ss;
+        NBB_TRY(nbbhost::slice_slots(&ss));
+        for (int d = 0; d < 8; ++d)
+            if (ss.dir_upto[d][kSliceMaxK] > ((d == 2 || d == 5) ? 0 : kSliceDirMax))
+                return fail(NBB_ERR_RUNTIME, "slice slots: a neighbouring tile holds more halo slots than compiled for");
+        if (ss.upto[kSliceMaxK - 1] > 32 * kSliceMaxM)
+            return fail(NBB_ERR_RUNTIME, "slice slots: more halo slots per step than compiled for");
+        NBB_CUDA(cudaMemcpyToSymbol(c_sslots, &ss, sizeof(ss)));
         NBB_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         NBB_CUDA(cudaMalloc(&c.partials, 4097 * sizeof(unsigned long long)));
         c.ready = true;
@@ -801,6 +810,20 @@ void (*pass_kernel_k(int k, bool conway))(CompactCaArgs, FastDiv, const int32_t*
     }
 }
 // resident CTAs per SM of a pass kernel (cached per kernel pointer)
+int pass_occupancy_threads(const void* k, int threads, int* occ) {
+    static std::mutex m;
+    static std::vector<std::pair<const void*, int>> cache;
+    std::lock_guard<std::mutex> lock(m);
+    for (auto& e : cache)
+        if (e.first == k) {
+            *occ = e.second;
+            return NBB_OK;
+        }
+    NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, threads, 0));
+    if (*occ < 1) *occ = 1;
+    cache.push_back({k, *occ});
+    return NBB_OK;
+}
 int pass_occupancy(const void* k, int* occ) {
     static std::mutex m;
     static std::vector<std::pair<const void*, int>> cache;
@@ -816,16 +839,70 @@ int pass_occupancy(const void* k, int* occ) {
     return NBB_OK;
 }
 
-// steps per pass: cfg->pass_steps (0 = kDefaultPassSteps), 1 with NBB_FLAG_SINGLE_STEP
-constexpr int kDefaultPassSteps = 4;
+// The pass kernel: the tile-sliced kernel (compact_sliced.cuh, up to 8 steps per pass) unless
+// NBB_PASS_IMPL=warp selects the warp-per-tile kernel (compact_pass.cuh, up to 4) for comparison.
+bool sliced_impl() {
+    static const bool v = [] {
+        const char* e = std::getenv("NBB_PASS_IMPL");
+        return !(e && std::strcmp(e, "warp") == 0);
+    }();
+    return v;
+}
+int impl_max_k() { return sliced_impl() ? kSliceMaxK : kPassMaxK; }
+// steps per pass: cfg->pass_steps (0 = the default), 1 with NBB_FLAG_SINGLE_STEP
+int default_pass_steps() {
+    static const int v = [] {
+        const char* e = std::getenv("NBB_PASS_STEPS");  // tuning
+        const int k = e ? std::atoi(e) : 0;
+        return k > 0 ? std::min(k, impl_max_k()) : (sliced_impl() ? 8 : 4);
+    }();
+    return v;
+}
 int max_pass_steps(const nbb_config* cfg) {
     if (cfg->flags & NBB_FLAG_SINGLE_STEP) return 1;
-    const int k = cfg->pass_steps ? (int)cfg->pass_steps : kDefaultPassSteps;
-    return std::max(1, std::min(k, kPassMaxK));
+    const int k = cfg->pass_steps ? (int)cfg->pass_steps : default_pass_steps();
+    return std::max(1, std::min(k, impl_max_k()));
 }
 int check_pass_steps(const nbb_config* cfg) {
-    if (cfg->pass_steps > (uint32_t)kPassMaxK)
-        return fail(NBB_ERR_INVALID_ARGUMENT, "pass_steps: at most 4 CA steps per pass over the compact state");
+    if (cfg->pass_steps > (uint32_t)kSliceMaxK)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "pass_steps: at most 8 CA steps per pass over the compact state");
+    return NBB_OK;
+}
+
+// the batches of the tile-sliced λ walk over this launch's shard [tile_begin, tile_end)
+SliceBatches slice_batches(const CompactCaArgs& a, int k) {
+    SliceBatches b{};
+    b.K = k;
+    const uint32_t Hb = a.Hb;
+    b.nb_row = (Hb + 31u) / 32u;
+    b.div_nb_row.d = b.nb_row;
+    nbbhost::fastdiv_magic(b.nb_row, &b.div_nb_row.m, &b.div_nb_row.s);
+    if (a.tile_end <= a.tile_begin) return b;
+    b.row0 = a.tile_begin / Hb;
+    b.col0 = a.tile_begin % Hb;
+    const uint32_t row_end = (b.row0 + 1u) * Hb;
+    if (a.tile_end <= row_end) {
+        b.cols0 = a.tile_end - a.tile_begin;
+    } else {
+        b.cols0 = Hb - b.col0;
+        const uint32_t rem = a.tile_end - row_end;
+        b.mid_rows = rem / Hb;
+        b.last_cols = rem % Hb;
+    }
+    b.nb0 = (b.cols0 + 31u) / 32u;
+    b.total = b.nb0 + b.mid_rows * b.nb_row + (b.last_cols + 31u) / 32u;
+    return b;
+}
+template <bool P2P, bool BB>
+void (*sliced_kernel(bool conway))(CompactCaArgs, SliceBatches, FastDiv, const int32_t*, P2PArgs) {
+    return conway ? ca_compact_sliced_kernel<true, P2P, BB> : ca_compact_sliced_kernel<false, P2P, BB>;
+}
+// grid of a tile-sliced launch: one wave (resident CTAs), fewer when the batches are fewer
+int sliced_grid(DeviceCtx* ctx, const void* kern, uint64_t batches, bool bb, unsigned* grid) {
+    int occ;
+    NBB_CHECK(pass_occupancy_threads(kern, 32 * kSliceWarps, &occ));
+    const uint64_t wave = (uint64_t)ctx->sms * occ;
+    *grid = (unsigned)std::max<uint64_t>(1, bb ? wave : std::min<uint64_t>(wave, (batches + kSliceWarps - 1) / kSliceWarps));
     return NBB_OK;
 }
 
@@ -851,6 +928,15 @@ int launch_pass(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* ds
     const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
     if (want == 0) return NBB_OK;
     const bool bb = cfg->mode == NBB_MODE_BB;
+    if (sliced_impl()) {
+        const SliceBatches sb = slice_batches(a, k);
+        auto kern = bb ? sliced_kernel<false, true>(is_conway(birth, survive))
+                       : sliced_kernel<false, false>(is_conway(birth, survive));
+        unsigned grid;
+        NBB_CHECK(sliced_grid(ctx, (const void*)kern, sb.total, bb, &grid));
+        NBB_CUDA(launch_pdl(kern, grid, 32 * kSliceWarps, st, a, sb, div_hb, tab, P2PArgs{}));
+        return NBB_OK;
+    }
     auto kern = bb ? pass_kernel_k<false, true>(k, is_conway(birth, survive))
                    : pass_kernel_k<false, false>(k, is_conway(birth, survive));
     int occ;
@@ -929,6 +1015,16 @@ int p2p_passes(const nbb_config* cfg, int64_t first_pass, int32_t steps, int kma
         p.peer_src = (const long long* const*)p2p->d_peer_buf[par];
         p.wait_target = (unsigned int)((uint64_t)p2p->world * (uint64_t)j);
         p.first_pass = i == 0 ? 1u : 0u;
+        if (sliced_impl()) {
+            const SliceBatches sb = slice_batches(a, passes[i]);
+            auto kern = sliced_kernel<true, false>(conway);
+            unsigned grid;
+            NBB_CHECK(sliced_grid(ctx, (const void*)kern, std::max<uint64_t>(1, sb.total), false, &grid));
+            NBB_CUDA(launch_pdl(kern, grid, 32 * kSliceWarps, stream, a, sb, div_hb, tab, p));
+            ++ps.passes;
+            ++ps.by_steps[passes[i]];
+            continue;
+        }
         auto kern = pass_kernel_k<true, false>(passes[i], conway);
         int occ;
         NBB_CHECK(pass_occupancy((const void*)kern, &occ));
@@ -1271,9 +1367,14 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
     const long long* h_in = gasket ? (const long long*)mapped_host_ptr(initial) : nullptr;
     long long* h_out = (gasket && (cfg->flags & NBB_FLAG_OUT_ZEROED))
                            ? (long long*)mapped_host_ptr(out_grid) : nullptr;
-    if (cfg->flags & NBB_FLAG_COMPACT_STATE) {
+    if ((cfg->flags & NBB_FLAG_COMPACT_STATE) && (cfg->flags & NBB_FLAG_EMBEDDED_STATE))
+        return fail(NBB_ERR_INVALID_ARGUMENT, "ca: NBB_FLAG_COMPACT_STATE and NBB_FLAG_EMBEDDED_STATE exclude each other");
+    // the compact state serves the call by default (nbb_gpu.h); the flags force either state
+    const bool compact_ok = gasket && cw == 8 && cfg->r >= 5 && cfg->r <= 18 && cfg->kernel == NBB_KERNEL_AUTO &&
+                            cfg->shard_count == 0;
+    if ((cfg->flags & NBB_FLAG_COMPACT_STATE) || (compact_ok && !(cfg->flags & NBB_FLAG_EMBEDDED_STATE))) {
         // compact state: member sectors -> the λ-ordered compact array (2 x 8·3^r bytes on the
-        // device, no embedded grid), steps on the orthotope, compact -> member sectors.
+        // device, no embedded grid), passes over the orthotope, compact -> member sectors.
         NBB_CHECK(compact_workload_check(cfg, true));
         if (cw != 8) return fail(NBB_ERR_INVALID_ARGUMENT, "the compact state holds int64 values: cell_width 8");
         CompactShape cs;

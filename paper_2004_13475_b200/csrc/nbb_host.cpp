@@ -588,3 +588,71 @@ Error halo_slots(HaloSlots* out) {
     return {};
 }
 }  // namespace nbbhost
+
+// ---- halo slots of the tile-sliced pass (see nbb_host.hpp) ----------------------------------
+namespace nbbhost {
+Error slice_slots(SliceSlots* out) {
+    constexpr int L = 12, T = 32, K = kSliceMaxK, E = T + 2 * K;
+    const int64_t n = int64_t(1) << L, nb = n / T;
+    auto member = [&](int64_t x, int64_t y) { return x >= 0 && y >= 0 && x < n && y < n && (x & y) == x; };
+    std::vector<int> best(E * E, 99), layer(E * E);
+    std::vector<int> front, next;
+    for (int64_t by = 0; by < nb; ++by)
+        for (int64_t bx = 0; bx < nb; ++bx) {
+            if ((bx & by) != bx) continue;
+            std::fill(layer.begin(), layer.end(), -1);
+            front.clear();
+            for (int y = 0; y < T; ++y)
+                for (int x = 0; x < T; ++x)
+                    if ((x & y) == x) {
+                        layer[(y + K) * E + x + K] = 0;
+                        front.push_back((y + K) * E + x + K);
+                    }
+            for (int d = 1; d <= K; ++d) {
+                next.clear();
+                for (int i : front) {
+                    const int x = i % E - K, y = i / E - K;
+                    for (int dy = -1; dy <= 1; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            const int qx = x + dx, qy = y + dy;
+                            if ((!dx && !dy) || qx < -K || qy < -K || qx >= T + K || qy >= T + K) continue;
+                            const int q = (qy + K) * E + qx + K;
+                            if (layer[q] >= 0 || !member(bx * T + qx, by * T + qy)) continue;
+                            layer[q] = d;
+                            next.push_back(q);
+                        }
+                }
+                front.swap(next);
+                for (int q : front) best[q] = std::min(best[q], d);
+            }
+        }
+    std::vector<std::pair<int, int>> pos;  // (layer, index), index in row-major frame order
+    for (int i = 0; i < E * E; ++i)
+        if (best[i] <= K) pos.push_back({best[i], i});
+    std::stable_sort(pos.begin(), pos.end(), [](auto a, auto b) { return a.first < b.first; });
+    if ((int)pos.size() > kSliceSlots) return err(NBB_ERR_RUNTIME, "slice slots: too many halo positions");
+    SliceSlots h{};
+    h.count = (int32_t)pos.size();
+    for (int s = 0; s < h.count; ++s) {
+        const int x = pos[s].second % E - K, y = pos[s].second / E - K, d = pos[s].first;
+        h.x[s] = (int8_t)x;
+        h.y[s] = (int8_t)y;
+        h.layer[s] = (uint8_t)d;
+        const int dx = x < 0 ? -1 : x >= T ? 1 : 0, dy = y < 0 ? -1 : y >= T ? 1 : 0;
+        const int d9 = (dy + 1) * 3 + dx + 1;
+        const int dir = d9 > 4 ? d9 - 1 : d9;
+        h.dir_of[s] = (uint8_t)dir;
+        h.li[s] = (uint8_t)tile_local_index_host((uint32_t)(x - dx * T), (uint32_t)(y - dy * T));
+        h.by_dir[dir][h.dir_upto[dir][K]++] = (uint8_t)s;
+        for (int k = d; k <= K; ++k) ++h.upto[k];
+    }
+    for (int dir = 0; dir < 8; ++dir)  // the per-tile lists are in slot (= layer) order
+        for (int k = 0; k <= K; ++k) {
+            int c = 0;
+            for (int i = 0; i < h.dir_upto[dir][K]; ++i) c += h.layer[h.by_dir[dir][i]] <= k;
+            h.dir_upto[dir][k] = c;
+        }
+    *out = h;
+    return {};
+}
+}  // namespace nbbhost

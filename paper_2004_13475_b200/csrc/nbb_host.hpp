@@ -92,6 +92,23 @@ struct HaloSlots {
 };
 Error halo_slots(HaloSlots* out);
 
+// The same layers up to K = 8 for the tile-sliced pass (compact_sliced.cuh): positions sorted by
+// layer, and per neighbouring tile the slots lying in it, sorted by layer (the halo loads walk
+// one neighbour at a time). 8 / 22 / 36 / 58 / 76 / 104 / 128 / 166 slots for K = 1..8.
+constexpr int kSliceMaxK = 8;
+constexpr int kSliceSlots = 192;
+struct SliceSlots {
+    int32_t count;                      // slots with layer <= kSliceMaxK
+    int32_t upto[kSliceMaxK + 1];       // upto[d] = slots with layer <= d
+    int8_t x[kSliceSlots], y[kSliceSlots];
+    uint8_t layer[kSliceSlots];
+    uint8_t li[kSliceSlots];            // local compact index in the neighbouring tile
+    uint8_t dir_of[kSliceSlots];        // neighbouring tile, 0..7 ((dy+1)*3 + dx+1, centre skipped)
+    uint8_t by_dir[8][kSliceSlots];     // per neighbouring tile: its slots, by layer
+    int32_t dir_upto[8][kSliceMaxK + 1];  // per neighbouring tile: slots with layer <= d
+};
+Error slice_slots(SliceSlots* out);
+
 // precomputed fast division magic (see common.cuh FastDiv), exact for x < 2^31
 void fastdiv_magic(uint32_t d, uint32_t* m, uint32_t* s);
 

@@ -450,6 +450,7 @@ class P2PCompactCA:
                   ctypes.byref(self._args), ctypes.c_void_p(stream)))
         self.step_index += steps
         if self.two_step:
+            from . import _abi
             st = _abi.NbbPassStats()
             _check(self.lib.nbb_gpu_pass_plan(ctypes.byref(c), steps, 0, ctypes.byref(st)))
             self.pass_index += st.passes

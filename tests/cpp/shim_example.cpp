@@ -3,7 +3,9 @@
 // tests/test_gpu_parity.py::test_cpp_shim_on_gpu.
 #include <cstdio>
 #include <cstring>
+#include <cstdint>
 #include <numeric>
+#include <vector>
 
 #include "nbb_gpu.hpp"
 
@@ -36,5 +38,27 @@ int main(int argc, char** argv) {
     const long long pop = std::accumulate(ca.grid.values().begin(), ca.grid.values().end(), 0LL);
     std::printf("ca pop %lld gen %llu reports %zu\n", pop, (unsigned long long)ca.grid.generation(),
                 ca.reports.size());
+    // n = 2^13: the default device state (compact, passes of up to 8 steps), the explicit compact
+    // state with 3 steps per pass, and the embedded int64 grid; FNV-1a of each result, which the
+    // test compares with the C oracle's trajectory
+    g::DispatchConfig c13 = cfg;
+    c13.r = 13;
+    c13.max_cells = 1ull << 26;
+    const auto init13 = g::random_member_grid(c13.spec, 13, 14, 2, c13.max_cells);
+    auto fnv = [](const std::vector<std::int64_t>& v) {
+        std::uint64_t h = 0xcbf29ce484222325ull;
+        for (std::int64_t x : v)
+            for (int b = 0; b < 8; ++b) {
+                h ^= (std::uint64_t)((unsigned long long)x >> (8 * b)) & 0xFFu;
+                h *= 0x100000001b3ull;
+            }
+        return h;
+    };
+    std::printf("ca13 default %016llx\n", (unsigned long long)fnv(g::run_ca(c13, init13, 20).grid.values()));
+    c13.state = g::DispatchConfig::State::Compact;
+    c13.pass_steps = 3;
+    std::printf("ca13 compact3 %016llx\n", (unsigned long long)fnv(g::run_ca(c13, init13, 20).grid.values()));
+    c13.state = g::DispatchConfig::State::Embedded;
+    std::printf("ca13 embedded %016llx\n", (unsigned long long)fnv(g::run_ca(c13, init13, 20).grid.values()));
     return (sum == 59049 && pop == 10398) ? 0 : 2;
 }

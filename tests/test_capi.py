@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
     assert lib.nbb_gpu_abi_version() == 3
 
 
-@pytest.mark.parametrize("kmax", [1, 2, 3, 4])
+@pytest.mark.parametrize("kmax", [1, 2, 3, 4, 5, 8])
 def test_pass_plan(kmax):
     """nbb_gpu_pass_plan (host only): the passes a compact CA run issues — every step counted once,
     at most pass_steps per pass, the fewest passes (ceil(steps / K)) without parity; with parity
@@ -53,8 +53,8 @@ def test_pass_plan(kmax):
         for parity in (False, True):
             st = dev.pass_plan(c, steps, parity)
             by = list(st.by_steps)
-            assert sum(k * by[k] for k in range(5)) == steps
-            assert all(by[k] == 0 for k in range(kmax + 1, 5))
+            assert sum(k * by[k] for k in range(9)) == steps
+            assert all(by[k] == 0 for k in range(kmax + 1, 9))
             assert st.passes == sum(by)
             fewest = -(-steps // kmax)
             if parity:
@@ -65,7 +65,7 @@ def test_pass_plan(kmax):
     single = dev.pass_plan(_cfg(r=10, rho=32, flags=_abi.FLAG_SINGLE_STEP), 7)
     assert single.passes == 7 and single.by_steps[1] == 7
     with pytest.raises(nbb.InvalidArgument):
-        dev.pass_plan(_cfg(r=10, rho=32, pass_steps=5), 4)
+        dev.pass_plan(_cfg(r=10, rho=32, pass_steps=9), 4)
 
 
 def test_library_is_sm100a_and_native():

@@ -51,7 +51,9 @@ KERNEL_COMBOS = [  # (mode, rho, kernel, cell_width)
     for cw in (8, 1)
 ] + [(MapMode.BoundingBox, rho, k, cw)
      for rho in (1, 2, 4, 8, 16, 32) for k in (KernelFamily.Auto, KernelFamily.PerCell)
-     for cw in (8, 1)]
+     for cw in (8, 1)
+] + [(mode, rho, KernelFamily.Tile, 8)  # the embedded int64 tile kernels (Auto takes the compact state)
+     for mode in (MapMode.Lambda, MapMode.BoundingBox) for rho in (8, 16, 32)]
 
 
 def test_device_present():
@@ -130,7 +132,8 @@ def test_ca_bit_packed_state(golden, r):
         nbb.run_ca(cfg(r=r, rho=16, cell_width=0), grid(init, r), 1)
 
 
-@pytest.mark.parametrize("cw,state", [(8, 0), (1, 0), (0, 0), (8, _abi.FLAG_COMPACT_STATE)])
+@pytest.mark.parametrize("cw,state", [(8, 0), (8, _abi.FLAG_EMBEDDED_STATE), (1, 0), (0, 0),
+                                      (8, _abi.FLAG_COMPACT_STATE)])
 def test_ca_host_buffers_pinned_zero_copy(cw, state):
     """nbb_gpu_ca on pinned host buffers: member sectors move in place over PCIe; with
     FLAG_OUT_ZEROED only member cells of out are written; without it out is written whole."""
@@ -203,6 +206,8 @@ def test_mode_equivalence_matrix(golden):
             tag = (r, rho, st.name, be.name)
             assert fnv1a64(nbb.run_single_write(c).grid.values) == w["sw_fnv"], tag
             assert nbb.run_reduction(c, grid(rd, r)).value == w["acceptance_rd_value"], tag
+            assert fnv1a64(nbb.run_ca(c, grid(ca, r), 2).grid.values) == w["acceptance_ca2_fnv"], tag
+            c.flags = _abi.FLAG_EMBEDDED_STATE  # the embedded grid with this (strategy, backend)
             assert fnv1a64(nbb.run_ca(c, grid(ca, r), 2).grid.values) == w["acceptance_ca2_fnv"], tag
             combos += 1
         assert combos > 0
@@ -460,6 +465,11 @@ def test_cpp_shim_on_gpu():
     r = subprocess.run([out], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ca pop 10398" in r.stdout
+    # nbb::gpu::run_ca (the reference signature) at n = 2^13, 20 steps: default (compact) state,
+    # compact with 3 steps per pass, embedded int64 grid — all equal the C oracle
+    want = f"{fnv1a64(orc_ca(13, orc_random_member_grid(13, 14, 2), 20)):016x}"
+    for tag in ("default", "compact3", "embedded"):
+        assert f"ca13 {tag} {want}" in r.stdout, (tag, want, r.stdout)
 
 
 @pytest.mark.slow

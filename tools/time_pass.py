@@ -1,9 +1,10 @@
-"""K steps per pass over the compact state (ca_compact_pass_kernel, K = 1..4): CUDA-event time
-of S steps through nbb_gpu_ca_compact_passes_dev (fewest passes) at n = 2^16 and 2^17, for the
-B3/S23 instantiation, a generic rule (B36/S23) and the bounding-box walk; results of every K
-checked equal to K = 1 after 12 steps.
+"""K steps per pass over the compact state: CUDA-event time of S steps through
+nbb_gpu_ca_compact_passes_dev (fewest passes) at n = 2^16 and 2^17, for the B3/S23
+instantiation, a generic rule (B36/S23) and the bounding-box walk; results of every K checked
+equal to K = 1 after 24 steps.
 
-    python tools/time_pass.py [S=240]      (NBB_GPU_LIB=... selects a tuning build)
+    python tools/time_pass.py [S=240] [K,K,...=1,2,3,4,6,8]
+    NBB_PASS_IMPL=warp selects the warp-per-tile kernel (K <= 4); NBB_GPU_LIB a tuning build
 """
 import json
 import os
@@ -18,6 +19,7 @@ from paper_2004_13475_b200 import nbb  # noqa: E402
 from paper_2004_13475_b200 import device as dev  # noqa: E402
 
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 240
+KS = [int(k) for k in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1, 2, 3, 4, 6, 8]
 s = torch.cuda.current_stream().cuda_stream
 hl = nbb.CaRule(birth=(1 << 3) | (1 << 6), survive=(1 << 2) | (1 << 3))
 for r in (16, 17):
@@ -27,12 +29,12 @@ for r in (16, 17):
     a0 = torch.randint(0, 2, (members,), dtype=torch.int64, device="cuda", generator=g)
     a, b = torch.empty_like(a0), torch.empty_like(a0)
     ref = {}
-    for K in (1, 2, 3, 4):
+    for K in KS:
         for name, rule, mode in (("conway", nbb.CaRule(), nbb.MapMode.Lambda), ("generic", hl, nbb.MapMode.Lambda),
                                  ("bb_conway", nbb.CaRule(), nbb.MapMode.BoundingBox)):
             c = nbb.DispatchConfig(r=r, rho=32, max_cells=(1 << r) ** 2, pass_steps=K, mode=mode)
             a.copy_(a0)
-            st = dev.ca_compact_passes_dev(c, a.data_ptr(), b.data_ptr(), 12, rule, s)
+            st = dev.ca_compact_passes_dev(c, a.data_ptr(), b.data_ptr(), 24, rule, s)
             out = (b if st.result_in_b else a).clone()
             key = (name.replace("bb_", ""))
             same = None
