@@ -190,15 +190,15 @@ def config_block(r, rho, world=1, transport="p2p"):
     return {"workload": f"C3: gasket n=2^{r} cellular-automaton step (B3/S23), lambda(omega) launch, "
                         f"rho={rho} tiles; device state = the lambda-ordered compact layout "
                         f"(CompactGrid, 8 B per member), host I/O = the reference's int64 Grid; "
-                        + ("up to 8 steps per pass over the state (ca_compact_sliced_kernel)"
-                           if world == 1 or transport == "p2p" else "one step per launch"),
+                        + "up to 8 steps per pass over the state (ca_compact_sliced_kernel)",
             "r": r, "n": 1 << r, "rho": rho, "mode": "lambda", "cells_per_step": 3 ** r,
             "cell": "int64", "state": "compact",
             "parallelism": "1 GPU" if world == 1 else
                            f"{world} ranks: contiguous tile-range shards; " + (
-                               "halo cells read over peer memory (CUDA IPC) inside the step kernel"
+                               "halo cells read over peer memory (CUDA IPC) inside the pass kernel"
                                if transport == "p2p" else
-                               f"halo cells exchanged by gather + NCCL all_to_all + scatter ({transport})"),
+                               f"halo cells exchanged by the library's NCCL communicator (gather + "
+                               f"ncclSend/ncclRecv + scatter) before every pass ({transport})"),
             "l2": "no flush: each pass moves 689 MB compact / 1.7 GB embedded (> 126 MB L2)"}
 
 
@@ -216,8 +216,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="headline, roofline and e2e only")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
-                    help="N > 1 halo exchange: inside the step kernel over peer memory (p2p, "
-                         "default) or gather + NCCL all_to_all + scatter per step (nccl)")
+                    help="N > 1 halo exchange: inside the pass kernel over peer memory (p2p, "
+                         "default) or the library's NCCL communicator before every pass (nccl)")
     ap.add_argument("--profile", action="store_true",
                     help="only run a few λ/BB CA passes (for ncu); prints nothing")
     args = ap.parse_args()
@@ -382,19 +382,13 @@ def main():
         p2p.close()
         ps = dev.pass_plan(plan_c.local_config(cfg()), K)
         head_stats = {"passes": ps.passes, "by_steps": list(ps.by_steps)}
-    elif world > 1:  # NCCL halo exchange between one-step launches
-        lc = plan_c.local_config(cfg())
-        bufs = [c1, c2]
-        stt = {"i": 0}
-
-        def nccl_run(k):
-            for _ in range(k):
-                i = stt["i"]
-                plan_c.exchange_halo(bufs[i & 1], dist)
-                dev.ca_compact_step_dev(lc, bufs[i & 1].data_ptr(), bufs[(i + 1) & 1].data_ptr(), CONWAY, s)
-                stt["i"] = i + 1
-        head_ms, head_all = timed_run(nccl_run, K, W, sampler, reps=3)
-        head_stats = {"passes": K, "by_steps": [0, K] + [0] * 7}
+    elif world > 1:  # the library's NCCL communicator: halo exchange (ncclSend/Recv) before each pass
+        ca_n = shard.NcclCompactCA(r, dist, local)
+        ca_n.load(c1)
+        head_ms, head_all = timed_run(lambda k: ca_n.run(cfg(), CONWAY, k, s), K, W, sampler, reps=3)
+        ca_n.close()
+        ps = dev.pass_plan(plan_c.local_config(cfg()), K)
+        head_stats = {"passes": ps.passes, "by_steps": list(ps.by_steps)}
         launches_per_step = 3
     else:
         run, st = compact_runner(cfg())

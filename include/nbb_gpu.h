@@ -189,6 +189,20 @@ int nbb_gpu_reduction(const nbb_config* cfg, const int64_t* grid, int32_t grid_l
 int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_level,
                int32_t steps, uint16_t birth, uint16_t survive, int64_t* out_grid,
                nbb_report* per_step);
+/* run_ca / run_reduction with the reference's `workers` mapped to DEVICES of this process
+ * (dispatch.cpp:416-432: contiguous ordinal chunks of ceil(total / workers), result independent
+ * of the count — byte-identical for any ndev). The compact tiles are split into ndev contiguous
+ * chunks; worker w advances chunk w on devices[w] in passes of up to pass_steps steps and reads
+ * the halo cells other workers own from their buffers over NVLink (peer access) inside the pass
+ * kernel; a flag barrier in device memory orders the passes. devices may repeat (several
+ * chunks on one GPU). Gasket, lambda mode, cell_width 8, 5 <= r <= 18; ndev <= 8; the host
+ * buffers as for nbb_gpu_ca / nbb_gpu_reduction (devices[0] converts them). */
+int nbb_gpu_ca_multi(const nbb_config* cfg, const int32_t* devices, int32_t ndev,
+                     const int64_t* initial, int32_t initial_level, int32_t steps, uint16_t birth,
+                     uint16_t survive, int64_t* out_grid, nbb_report* per_step);
+int nbb_gpu_reduction_multi(const nbb_config* cfg, const int32_t* devices, int32_t ndev,
+                            const int64_t* grid, int32_t grid_level, int64_t* value,
+                            nbb_report* report);
 /* λ(ω) for every ω of the level-`level` orthotope, ordinal-major
  * (xy[2*o], xy[2*o+1], o = ωy*W + ωx). Uses cfg->backend (direct or mma1/mma2). */
 int nbb_gpu_lambda_coords(const nbb_config* cfg, int32_t level, int64_t* xy);
@@ -328,6 +342,35 @@ int nbb_gpu_free(int32_t device, void* d_ptr);
 int nbb_gpu_ipc_handle(int32_t device, const void* d_ptr, uint8_t handle[64]);
 int nbb_gpu_ipc_open(int32_t device, const uint8_t handle[64], void** d_ptr);
 int nbb_gpu_ipc_close(int32_t device, void* d_ptr);
+
+/* ---- multi-GPU compact CA over NCCL (one process per GPU) ---------------------------------
+ * The north_star's transport: NCCL over NVLink only for the CA boundary halos and the final
+ * reduction. A communicator spans `world` processes (ncclCommInitRank; the 128-byte id comes from
+ * nbb_gpu_comm_unique_id on one rank and reaches the others through the caller's launcher).
+ * Rank i owns the contiguous compact tile chunk [i * chunk, min((i + 1) * chunk, tiles)),
+ * chunk = ceil(tiles / world) (dispatch.cpp:419-427; cfg->shard_* are set from it). Before every
+ * pass of up to pass_steps (<= 8) steps the halo cells the rank's tiles read from other ranks
+ * within 8 steps are gathered, exchanged with ncclSend / ncclRecv in one group on `stream` and
+ * scattered into the pass's source buffer; d_a / d_b are replica-sized (3^r int64) buffers in
+ * which this rank's tiles are current; the result buffer is named by stats->result_in_b. NCCL
+ * is bound at run time (libnccl.so.2); without it these calls return NBB_ERR_NCCL. */
+typedef struct nbb_comm nbb_comm;
+int nbb_gpu_comm_unique_id(uint8_t id[128]);
+int nbb_gpu_comm_init(const uint8_t id[128], int32_t world, int32_t rank, int32_t device,
+                      nbb_comm** comm);
+int nbb_gpu_comm_destroy(nbb_comm* comm);
+int nbb_gpu_ca_compact_comm_dev(const nbb_config* cfg, nbb_comm* comm, void* d_a, void* d_b,
+                                int32_t steps, uint16_t birth, uint16_t survive, void* stream,
+                                nbb_pass_stats* stats);
+/* Σ of the rank's tiles + one ncclAllReduce (int64 sum): *d_value on every rank. */
+int nbb_gpu_reduction_compact_comm_dev(const nbb_config* cfg, nbb_comm* comm, const void* d_compact,
+                                       void* d_value, void* stream);
+/* Host only: the halo exchange of rank `rank` for passes of up to kmax steps — cells sent to /
+ * received from every peer (counts[world]) and the sorted compact offsets for one peer. */
+int nbb_gpu_halo_exchange_counts(const nbb_config* cfg, int32_t world, int32_t rank, int32_t kmax,
+                                 uint64_t* send_counts, uint64_t* recv_counts);
+int nbb_gpu_halo_exchange_lists(const nbb_config* cfg, int32_t world, int32_t rank, int32_t kmax,
+                                int32_t peer, uint32_t* send, uint32_t* recv);
 
 #ifdef __cplusplus
 }

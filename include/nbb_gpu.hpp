@@ -221,6 +221,30 @@ inline CaResult run_ca(const DispatchConfig& config, const Grid& initial, int st
     return res;
 }
 
+// The reference's `workers` as devices of this process (nbb_gpu_ca_multi): contiguous chunks of
+// the compact tile range, halos over peer memory; byte-identical for any device list.
+inline CaResult run_ca(const DispatchConfig& config, const Grid& initial, int steps, CaRule rule,
+                       const std::vector<int>& devices) {
+    CaResult res{initial, {}};
+    const nbb_config c = config.c();
+    std::vector<std::int32_t> devs(devices.begin(), devices.end());
+    std::vector<nbb_report> reps((std::size_t)(steps > 0 ? steps : 0));
+    check(nbb_gpu_ca_multi(&c, devs.data(), (std::int32_t)devs.size(), initial.values().data(), initial.level(),
+                           steps, rule.birth, rule.survive, res.grid.values().data(),
+                           reps.empty() ? nullptr : reps.data()));
+    for (const auto& r : reps) res.reports.push_back(WorkReport{r});
+    res.grid.set_generation(initial.generation() + (std::uint64_t)(steps > 0 ? steps : 0));
+    return res;
+}
+inline ReductionResult run_reduction(const DispatchConfig& config, const Grid& grid, const std::vector<int>& devices) {
+    ReductionResult res;
+    const nbb_config c = config.c();
+    std::vector<std::int32_t> devs(devices.begin(), devices.end());
+    check(nbb_gpu_reduction_multi(&c, devs.data(), (std::int32_t)devs.size(), grid.values().data(), grid.level(),
+                                  &res.value, &res.report.c));
+    return res;
+}
+
 inline double work_quotient(const WorkReport& bounding_box, const WorkReport& lambda,
                             bool weighted = false) {
     double q = 0;

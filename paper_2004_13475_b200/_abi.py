@@ -137,6 +137,9 @@ SIGNATURES = {
     "nbb_gpu_reduction": (c_int, [CP, c_void_p, c_int32, I64P, RP]),
     "nbb_gpu_ca": (c_int, [CP, c_void_p, c_int32, c_int32, c_uint16, c_uint16, c_void_p, RP]),
     "nbb_gpu_lambda_coords": (c_int, [CP, c_int32, c_void_p]),
+    "nbb_gpu_ca_multi": (c_int, [CP, POINTER(c_int32), c_int32, c_void_p, c_int32, c_int32, c_uint16, c_uint16,
+                                 c_void_p, RP]),
+    "nbb_gpu_reduction_multi": (c_int, [CP, POINTER(c_int32), c_int32, c_void_p, c_int32, I64P, RP]),
     "nbb_gpu_single_write_dev": (c_int, [CP, c_void_p, c_void_p, RP]),
     "nbb_gpu_reduction_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p, RP]),
     "nbb_gpu_ca_step_dev": (c_int, [CP, c_void_p, c_void_p, c_uint16, c_uint16, c_void_p, RP]),
@@ -166,6 +169,14 @@ SIGNATURES = {
                                            POINTER(NbbP2P), c_void_p]),
     "nbb_gpu_ca_compact_p2p_passes_dev": (c_int, [CP, ctypes.c_int64, c_int32, c_uint16, c_uint16,
                                                   POINTER(NbbP2P), c_void_p]),
+    "nbb_gpu_comm_unique_id": (c_int, [POINTER(ctypes.c_uint8)]),
+    "nbb_gpu_comm_init": (c_int, [POINTER(ctypes.c_uint8), c_int32, c_int32, c_int32, POINTER(c_void_p)]),
+    "nbb_gpu_comm_destroy": (c_int, [c_void_p]),
+    "nbb_gpu_ca_compact_comm_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p, c_int32, c_uint16, c_uint16,
+                                            c_void_p, POINTER(NbbPassStats)]),
+    "nbb_gpu_reduction_compact_comm_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "nbb_gpu_halo_exchange_counts": (c_int, [CP, c_int32, c_int32, c_int32, POINTER(c_uint64), POINTER(c_uint64)]),
+    "nbb_gpu_halo_exchange_lists": (c_int, [CP, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
     "nbb_gpu_p2p_check": (c_int, [POINTER(NbbP2P), c_void_p]),
     "nbb_gpu_malloc": (c_int, [c_int32, c_uint64, POINTER(c_void_p)]),
     "nbb_gpu_free": (c_int, [c_int32, c_void_p]),

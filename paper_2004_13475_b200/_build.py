@@ -21,7 +21,7 @@ SOURCES = ["nbb_capi.cu", "nbb_host.cpp"]
 HEADERS = ["common.cuh", "tile_kernels.cuh", "ca_pipe_kernel.cuh", "bits_kernels.cuh",
            "compact_kernels.cuh", "compact_pass.cuh", "compact_sliced.cuh",
            "percell_kernels.cuh",
-           "util_kernels.cuh", "nbb_host.hpp"]
+           "util_kernels.cuh", "nbb_host.hpp", "nbb_multi.inc", "nbb_comm.inc"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:
@@ -40,7 +40,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
            "-Xptxas", "-v" if verbose else "-O3",
            f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}",
            "-shared", "-o", LIB + ".tmp",
-           *[os.path.join(CSRC, f) for f in SOURCES]]
+           *[os.path.join(CSRC, f) for f in SOURCES], "-ldl"]
     subprocess.run(cmd, check=True, cwd=ROOT)
     os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -123,6 +123,11 @@ __global__ void __launch_bounds__(256, NBB_PASS_MINB) ca_compact_pass_kernel(Com
         pdl_wait();
     }
     __syncthreads();
+    // every thread (not only the poller) orders its peer reads after the arrivals it waited for:
+    // the poller's ld.acquire.sys synchronises with the peers' fence.acq_rel.sys + red.relaxed.sys,
+    // bar.sync carries that to the CTA, and this fence makes each thread's own later ld.relaxed.sys
+    // of peer memory observe it at system scope
+    if (P2P && p.wait_target != 0u) asm volatile("fence.acq_rel.sys;" ::: "memory");
     // slot k of lane l = local index 32k + l: byte offset in the tile's sub-block | byte index
     // x | y << 5 in the 32 x 32 tile << 21 (offsets < 2^21 for W <= 3^9, i.e. r <= 18)
     uint32_t sl[8];

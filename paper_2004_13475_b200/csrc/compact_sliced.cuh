@@ -43,14 +43,15 @@ using nbbhost::kSliceSlots;
 using nbbhost::SliceSlots;
 __constant__ SliceSlots c_sslots;
 
-constexpr int kSliceWarps = 4;                    // warps per CTA (one batch each)
+constexpr int kSliceWarps = 2;                    // warps per CTA: a loader and a stepper
 constexpr int kBoxH = 32 + 2 * kSliceMaxK;        // box rows: the tile and a K-cell frame
 constexpr int kBoxW = kBoxH + 1;                  // odd row pitch: rows fall on different banks
 constexpr int kBoxWords = kBoxW * kBoxH;
 constexpr int kSliceChunk = 16;                   // halo loads in flight per lane
-constexpr int kSliceLag = 2;                      // tiles of loads in flight ahead of their use
+constexpr int kSliceLag = 1;                      // tiles of loads in flight ahead of their use
 constexpr int kSliceMaxM = 4;                     // halo slots a lane advances per step (<= 128 / 32)
-constexpr int kSliceDirMax = 32;                  // slots per neighbouring tile (host-checked)
+constexpr int kSliceDirMax = 30;                  // slots per neighbouring tile (host-checked)
+constexpr int kSliceLanesSlots = kSliceDirMax / 5; // halo slots per gathering lane (5 lanes per tile)
 
 // The λ walk's batches: up to 32 consecutive tile ordinals inside one tile row of the shard
 // [tile_begin, tile_end): the first (possibly partial) row, whole rows, a last partial row.
@@ -70,26 +71,46 @@ __device__ __forceinline__ uint32_t sliced_cell_step(const uint32_t* c, uint32_t
                      c[0], CONWAY ? (1u << 3) : birth, CONWAY ? (1u << 2) | (1u << 3) : survive);
 }
 
+// Named barriers of the loader / stepper hand-off (64 threads: both warps). Box b (b = batch
+// index & 1) is FULL once the loader stored the batch's tile words, EMPTY once the stepper
+// stored its results.
+// Compile-time ids: ptxas then reserves 5 barriers per CTA (a runtime id reserves all 16, and
+// the SM's barrier pool would cap the resident CTAs at 4).
+template <int ID>
+__device__ __forceinline__ void nb_sync() { asm volatile("bar.sync %0, 64;" ::"n"(ID) : "memory"); }
+template <int ID>
+__device__ __forceinline__ void nb_arrive() { asm volatile("bar.arrive %0, 64;" ::"n"(ID) : "memory"); }
+__device__ __forceinline__ void nb_sync_full(int b) { if (b) nb_sync<2>(); else nb_sync<1>(); }
+__device__ __forceinline__ void nb_arrive_full(int b) { if (b) nb_arrive<2>(); else nb_arrive<1>(); }
+__device__ __forceinline__ void nb_sync_empty(int b) { if (b) nb_sync<4>(); else nb_sync<3>(); }
+__device__ __forceinline__ void nb_arrive_empty(int b) { if (b) nb_arrive<4>(); else nb_arrive<3>(); }
+
 #ifndef NBB_SLICE_MINB  // resident CTAs per SM the register budget is cut for (tuning builds)
-#define NBB_SLICE_MINB 4
+#define NBB_SLICE_MINB 8
 #endif
+// CTA = one pipeline of two warps over two boxes: the LOADER streams each batch's tile values
+// from HBM (8 loads per lane per tile, kSliceLag tiles in flight) and folds them into the words
+// of box (i & 1); the STEPPER gathers the batch's halo words into the same box (disjoint
+// positions), waits for the tile words, advances K steps in place and stores the results, while
+// the loader already fills the other box. The CTAs walk the batches with a grid stride.
 template <bool CONWAY, bool P2P, bool BB>
-__global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB) ca_compact_sliced_kernel(CompactCaArgs a, SliceBatches sb,
-                                                                              FastDiv div_hb,
-                                                                              const int32_t* __restrict__ nbr_tab,
-                                                                              P2PArgs p) {
+__global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB)
+    ca_compact_sliced_kernel(CompactCaArgs a, SliceBatches sb, FastDiv div_hb, const int32_t* __restrict__ nbr_tab,
+                             P2PArgs p) {
     static_assert(!(P2P && BB), "the multi-GPU pass walks the λ orthotope");
     const uint32_t birth = a.birth, survive = a.survive;
-    __shared__ uint32_t s_box[kSliceWarps][kBoxWords];
-    __shared__ uint32_t s_hmask[kSliceWarps][kSliceSlots];  // slot s exists in tile t: bit t
+    __shared__ uint32_t s_box[2][kBoxWords];
+    __shared__ uint32_t s_hmask[2][kSliceSlots];             // slot s exists in tile t: bit t
     __shared__ uint2 s_dir[8][kSliceDirMax];                 // per neighbouring tile: (offset in it, slot)
     __shared__ uint16_t s_bidx[kSliceSlots];                 // box index of every slot
-    __shared__ uint16_t s_pos[256];
     __shared__ uint16_t s_tb[256];                           // box index of tile cell li
-    __shared__ uint32_t s_list[kSliceWarps][32];             // BB: the batch's tile ordinals
+    __shared__ uint16_t s_cb[256];                           // box index of the c-th member, row-major
+    __shared__ uint32_t s_list[2][2][32];                    // BB: [warp][box] the batch's tile ordinals
+    __shared__ unsigned long long s_hp[6][33];               // stepper: halo tile pointers [direction][tile]
+    __shared__ uint32_t s_hdm[6];                            // stepper: halo tiles present [direction]
     __shared__ const long long* s_peer[kMaxP2P];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    uint32_t* box = s_box[wib];
+    const bool loader = wib == 0;
     const int K = sb.K;
     pdl_trigger();
     if (P2P && threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
@@ -106,10 +127,9 @@ __global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB) ca_compact_s
     }
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         const uint32_t pos = i < 243 ? c_local_pos[i] : 0u;
-        s_pos[i] = (uint16_t)pos;
         s_tb[i] = (uint16_t)(((pos >> 5) + kSliceMaxK) * kBoxW + (pos & 31u) + kSliceMaxK);
     }
-    for (int i = lane; i < kBoxWords; i += 32) box[i] = 0u;
+    for (int i = threadIdx.x; i < 2 * kBoxWords; i += blockDim.x) (&s_box[0][0])[i] = 0u;
     if (P2P && p.wait_target != 0u) {
         // the arrival wait (this rank's own previous pass is among the arrivals); the first pass
         // of every call also waits for its predecessor grid (whatever last wrote the state)
@@ -119,137 +139,174 @@ __global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB) ca_compact_s
         pdl_wait();
     }
     __syncthreads();
-    // the lane's tile cells li = 32k + lane (loads, stores): byte offset in a tile's sub-block;
-    // the cells it advances in the steps: the (32k + lane)-th member in row-major order, so the
-    // 32 lanes' box words of one access fall on (nearly) distinct banks
-    uint32_t off[8], cb[8];
+    // every thread (not only the poller) orders its peer reads after the arrivals it waited for:
+    // the poller's ld.acquire.sys synchronises with the peers' fence.acq_rel.sys + red.relaxed.sys,
+    // bar.sync carries that to the CTA, and this fence makes each thread's own later ld.relaxed.sys
+    // of peer memory observe it at system scope
+    if (P2P && p.wait_target != 0u) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    // the lane's tile cells li = 32k + lane (loads, stores): byte offset in a tile's sub-block
+    // (recomputed per batch: short register lifetimes); the cells it advances in the steps: the
+    // (32k + lane)-th member in row-major order, so the 32 lanes' box words of one access fall on
+    // (nearly) distinct banks (box index table s_cb, built once)
     {
-        uint32_t y = 0, seen = 0;  // walk the rows to the lane's first member
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const uint32_t li = 32u * k + lane;
-            const bool ok = li < 243u;
-            const uint32_t row = ok ? li / 27u : 0u, col = ok ? li % 27u : 0u;
-            off[k] = 8u * (row * a.W + col);
-            const uint32_t c = ok ? li : 0u;  // the c-th member, row-major
+        uint32_t y = 0, seen = 0;
+        for (uint32_t c = threadIdx.x; c < 243u; c += blockDim.x) {
             while (seen + (1u << __popc(y)) <= c) seen += 1u << __popc(y++);
-            const uint32_t x = pdep32(c - seen, y);
-            cb[k] = (y + kSliceMaxK) * kBoxW + x + kSliceMaxK;
+            s_cb[c] = (uint16_t)((y + kSliceMaxK) * kBoxW + pdep32(c - seen, y) + kSliceMaxK);
         }
     }
+    __syncthreads();
+    auto tile_offsets = [&](uint32_t* off) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t li = min(32u * k + lane, 242u);
+            off[k] = 8u * ((li / 27u) * a.W + li % 27u);
+        }
+    };
     const bool k7 = lane < 19;  // slot k = 7 holds li < 243 for lanes 0..18
-    const uint32_t nwarps = gridDim.x * kSliceWarps, warp_global = blockIdx.x * kSliceWarps + wib;
     auto tile_base = [&](uint32_t t) -> uint32_t {  // element offset of tile t's sub-block
         const uint32_t wxb = fastdiv(t, div_hb), wyb = t - wxb * a.Hb;
         return 9u * wxb * a.W + 27u * wyb;
     };
 
-    // One batch: lane t < cnt holds tile ordinal u; base0 = element offset of tile 0 (λ walk:
-    // tile t at base0 + 27 t).
-    auto batch = [&](uint32_t u, uint32_t cnt, uint32_t base0) {
-        // ---- tile words: w[k] bit t = cell li = 32k + lane of tile t is alive ----------------
-        // Software-pipelined over the batch's tiles: tile t's 8 loads are issued kSliceLag tiles
-        // before they are folded into the words (bits of tiles >= cnt are never stored).
+    // ---- loader: tile words of a batch into box b ---------------------------------------------
+    // lane t < cnt holds tile ordinal u; base0 = element offset of tile 0 (λ: tile t at +27 t).
+    auto load_batch = [&](uint32_t u, uint32_t cnt, uint32_t base0, uint32_t* box) {
+        uint32_t off[8];
+        tile_offsets(off);
         uint32_t w[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) w[k] = 0u;
-        const uint64_t tbase = (BB && lane < cnt) ? 8ull * tile_base(u) : 0ull;  // BB: per tile
-        {
-            const char* P0 = reinterpret_cast<const char*>(a.src) + 8ull * base0;
-            long long ring[kSliceLag + 1][8];
+        const uint64_t tbase = (BB && lane < (int)cnt) ? 8ull * tile_base(u) : 0ull;
+        const char* P0 = reinterpret_cast<const char*>(a.src) + 8ull * base0;
+        long long ring[kSliceLag + 1][8];
 #pragma unroll
-            for (int t = 0; t < 32 + kSliceLag; ++t) {
-                if (t >= (int)cnt + kSliceLag) break;
-                if (t < 32 && t < (int)cnt) {
-                    const char* P = P0 + 216u * t;  // λ: tile t of the batch follows tile t - 1
-                    if constexpr (BB) P = reinterpret_cast<const char*>(a.src) + __shfl_sync(0xFFFFFFFFu, tbase, t);
+        for (int t = 0; t < 32 + kSliceLag; ++t) {
+            if (t >= (int)cnt + kSliceLag) break;
+            if (t < 32 && t < (int)cnt) {
+                const char* P = P0 + 216u * t;  // λ: tile t of the batch follows tile t - 1
+                if constexpr (BB) P = reinterpret_cast<const char*>(a.src) + __shfl_sync(0xFFFFFFFFu, tbase, t);
 #pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        ring[t % (kSliceLag + 1)][k] =
-                            (k < 7 || k7) ? __ldg(reinterpret_cast<const long long*>(P + off[k])) : 0ll;
-                }
-                if (t >= kSliceLag) {
-                    const int tc = t - kSliceLag;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const long long v = ring[tc % (kSliceLag + 1)][k];
-                        const uint32_t nz = (uint32_t)v | (uint32_t)((unsigned long long)v >> 32);
-                        w[k] |= min(nz, 1u) << tc;
-                    }
-                }
+                for (int k = 0; k < 8; ++k)
+                    ring[t % (kSliceLag + 1)][k] =
+                        (k < 7 || k7) ? __ldg(reinterpret_cast<const long long*>(P + off[k])) : 0ll;
             }
-        }
-        // ---- halo words: lane t gathers tile t's halo cell of each slot, a ballot makes the word
-        int32_t nbr[8];
-        {
-            int4 n0 = make_int4(-1, -1, -1, -1), n1 = n0;
-            if (lane < cnt) {
-                n0 = __ldg(reinterpret_cast<const int4*>(nbr_tab + 8ull * u));
-                n1 = __ldg(reinterpret_cast<const int4*>(nbr_tab + 8ull * u) + 1);
-            }
-            nbr[0] = n0.x; nbr[1] = n0.y; nbr[2] = n0.z; nbr[3] = n0.w;
-            nbr[4] = n1.x; nbr[5] = n1.y; nbr[6] = n1.z; nbr[7] = n1.w;
-        }
+            if (t >= kSliceLag) {
+                const int tc = t - kSliceLag;
 #pragma unroll
-        for (int d = 0; d < 8; ++d) {
-            if (d == 2 || d == 5) continue;  // the (+1,-1) and (-1,+1) tiles hold no halo cell
-            const bool ex = nbr[d] >= 0;
-            const long long* src = a.src;
-            uint32_t nb = 0;
-            if (ex) {
-                nb = tile_base((uint32_t)nbr[d]);
-                if (P2P) src = s_peer[fastdiv((uint32_t)nbr[d], p.div_chunk)];
-            }
-            const char* P = reinterpret_cast<const char*>(src) + 8ull * nb;
-            const uint32_t dm = __ballot_sync(0xFFFFFFFFu, ex);
-            const int ns = c_sslots.dir_upto[d][K];
-            for (int j0 = 0; j0 < ns; j0 += kSliceChunk) {  // kSliceChunk loads in flight, then ballots
-                long long v[kSliceChunk];
-#pragma unroll
-                for (int c = 0; c < kSliceChunk; ++c) {
-                    v[c] = 0;
-                    if (ex && j0 + c < ns) {
-                        const long long* q = reinterpret_cast<const long long*>(P + s_dir[d][j0 + c].x);
-                        if (P2P)
-                            asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v[c]) : "l"(q));
-                        else
-                            v[c] = __ldg(q);
-                    }
-                }
-#pragma unroll
-                for (int c = 0; c < kSliceChunk; ++c) {
-                    if (j0 + c < ns) {
-                        const uint32_t hw = __ballot_sync(0xFFFFFFFFu, v[c] != 0ll) & dm;
-                        if (lane == 0) {
-                            const uint32_t sl = s_dir[d][j0 + c].y;
-                            box[s_bidx[sl]] = hw;
-                            s_hmask[wib][sl] = dm;
-                        }
-                    }
+                for (int k = 0; k < 8; ++k) {
+                    const long long v = ring[tc % (kSliceLag + 1)][k];
+                    const uint32_t nz = (uint32_t)v | (uint32_t)((unsigned long long)v >> 32);
+                    w[k] |= min(nz, 1u) << tc;
                 }
             }
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             if (k < 7 || k7) box[s_tb[32 * k + lane]] = w[k];
+    };
+
+    // ---- stepper: halo words, K steps, stores ---------------------------------------------------
+    // Halo words: the 6 neighbouring tiles that hold halo cells (directions 0,1,3,4,6,7) each get 5
+    // lanes (lanes 0..29); lane 5q + r gathers slots r, r + 5, ... (<= 6) of direction q's list for
+    // every tile t of the batch — one load per slot and tile, software-pipelined over the tiles
+    // like the loader's stream — and folds them into the slots' words (bit t).
+    const int hq = lane / 5, hr = lane % 5;
+    const int hd = hq < 2 ? hq : hq < 4 ? hq + 1 : hq + 2;  // direction of the lane's group
+    const int hn = hq < 6 ? c_sslots.dir_upto[hd][K] : 0;    // the group's slots at this K
+    auto halo_batch = [&](uint32_t u, uint32_t cnt, uint32_t* box, uint32_t* hmask) {
+        uint32_t hloc[kSliceLanesSlots], hslot[kSliceLanesSlots];
+#pragma unroll
+        for (int i = 0; i < kSliceLanesSlots; ++i) {
+            const int j = hr + 5 * i;
+            const bool ok = hq < 6 && j < hn;
+            const uint2 e = ok ? s_dir[hd][j] : make_uint2(0u, 0xFFFFu);
+            hloc[i] = e.x;
+            hslot[i] = e.y;  // 0xFFFF: no slot
+        }
+        // lane t: the neighbouring tiles of tile t -> base pointers (0: no member tile there)
+        {
+            int4 n0 = make_int4(-1, -1, -1, -1), n1 = n0;
+            if (lane < (int)cnt) {
+                n0 = __ldg(reinterpret_cast<const int4*>(nbr_tab + 8ull * u));
+                n1 = __ldg(reinterpret_cast<const int4*>(nbr_tab + 8ull * u) + 1);
+            }
+            const int32_t nbr6[6] = {n0.x, n0.y, n0.w, n1.x, n1.z, n1.w};  // directions 0,1,3,4,6,7
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                const bool ex = nbr6[q] >= 0;
+                unsigned long long ptr = 0ull;
+                if (ex) {
+                    const long long* src = P2P ? s_peer[fastdiv((uint32_t)nbr6[q], p.div_chunk)] : a.src;
+                    ptr = reinterpret_cast<unsigned long long>(src) + 8ull * tile_base((uint32_t)nbr6[q]);
+                }
+                s_hp[q][lane] = ptr;
+                const uint32_t dm = __ballot_sync(0xFFFFFFFFu, ex);
+                if (lane == 0) s_hdm[q] = dm;
+            }
+        }
         __syncwarp();
-        // ---- K steps: tile cells and the halo slots of layer <= K - j ------------------------
+        uint32_t hw[kSliceLanesSlots];
+#pragma unroll
+        for (int i = 0; i < kSliceLanesSlots; ++i) hw[i] = 0u;
+        long long ring[kSliceLag + 1][kSliceLanesSlots];
+        const int qq = hq < 6 ? hq : 0;
+#pragma unroll
+        for (int t = 0; t < 32 + kSliceLag; ++t) {
+            if (t >= (int)cnt + kSliceLag) break;
+            if (t < 32 && t < (int)cnt) {
+                const unsigned long long P = s_hp[qq][t];
+#pragma unroll
+                for (int i = 0; i < kSliceLanesSlots; ++i) {
+                    long long v = 0;
+                    if (P != 0ull && hslot[i] != 0xFFFFu) {
+                        const long long* q = reinterpret_cast<const long long*>(P + hloc[i]);
+                        if (P2P)
+                            asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(q));
+                        else
+                            v = __ldg(q);
+                    }
+                    ring[t % (kSliceLag + 1)][i] = v;
+                }
+            }
+            if (t >= kSliceLag) {
+                const int tc = t - kSliceLag;
+#pragma unroll
+                for (int i = 0; i < kSliceLanesSlots; ++i) {
+                    const long long v = ring[tc % (kSliceLag + 1)][i];
+                    const uint32_t nz = (uint32_t)v | (uint32_t)((unsigned long long)v >> 32);
+                    hw[i] |= min(nz, 1u) << tc;
+                }
+            }
+        }
+        const uint32_t dm = s_hdm[qq];
+#pragma unroll
+        for (int i = 0; i < kSliceLanesSlots; ++i) {
+            if (hslot[i] != 0xFFFFu) {
+                box[s_bidx[hslot[i]]] = hw[i] & dm;
+                hmask[hslot[i]] = dm;
+            }
+        }
+    };
+    auto step_batch = [&](uint32_t u, uint32_t cnt, uint32_t base0, uint32_t* box, const uint32_t* hmask) {
+        __syncwarp();
+        uint32_t w[8];
         for (int j = 1; j <= K; ++j) {
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                if (k < 7 || k7) w[k] = sliced_cell_step<CONWAY>(box + cb[k], birth, survive);
+                if (k < 7 || k7) w[k] = sliced_cell_step<CONWAY>(box + s_cb[32 * k + lane], birth, survive);
             const int ns = c_sslots.upto[K - j];
             uint32_t hn[kSliceMaxM];
 #pragma unroll
             for (int m = 0; m < kSliceMaxM; ++m) {
                 const int s = lane + 32 * m;
                 hn[m] = 0u;
-                if (s < ns) hn[m] = sliced_cell_step<CONWAY>(box + s_bidx[s], birth, survive) & s_hmask[wib][s];
+                if (s < ns) hn[m] = sliced_cell_step<CONWAY>(box + s_bidx[s], birth, survive) & hmask[s];
             }
             __syncwarp();
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                if (k < 7 || k7) box[cb[k]] = w[k];
+                if (k < 7 || k7) box[s_cb[32 * k + lane]] = w[k];
 #pragma unroll
             for (int m = 0; m < kSliceMaxM; ++m) {
                 const int s = lane + 32 * m;
@@ -257,33 +314,51 @@ __global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB) ca_compact_s
             }
             __syncwarp();
         }
-        // the lane's cells in load order again
 #pragma unroll
         for (int k = 0; k < 8; ++k) w[k] = (k < 7 || k7) ? box[s_tb[32 * k + lane]] : 0u;
-        // ---- store: cell li of tile t = bit t of w[k] --------------------------------------
-        {
-            char* Q0 = reinterpret_cast<char*>(a.dst) + 8ull * base0;
+        // cell li of tile t = bit t of w[k]
+        uint32_t off[8];
+        tile_offsets(off);
+        const uint64_t tbase = (BB && lane < (int)cnt) ? 8ull * tile_base(u) : 0ull;
+        char* Q0 = reinterpret_cast<char*>(a.dst) + 8ull * base0;
 #pragma unroll
-            for (int t = 0; t < 32; ++t) {
-                if (t >= (int)cnt) break;
-                char* Q = Q0 + 216u * t;
-                if constexpr (BB) Q = reinterpret_cast<char*>(a.dst) + __shfl_sync(0xFFFFFFFFu, tbase, t);
+        for (int t = 0; t < 32; ++t) {
+            if (t >= (int)cnt) break;
+            char* Q = Q0 + 216u * t;
+            if constexpr (BB) Q = reinterpret_cast<char*>(a.dst) + __shfl_sync(0xFFFFFFFFu, tbase, t);
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    if (k < 7 || k7) *reinterpret_cast<long long*>(Q + off[k]) = (long long)((w[k] >> t) & 1u);
-            }
+            for (int k = 0; k < 8; ++k)
+                if (k < 7 || k7) *reinterpret_cast<long long*>(Q + off[k]) = (long long)((w[k] >> t) & 1u);
         }
     };
 
+    // ---- the walk: batch i of this CTA uses box i & 1 -----------------------------------------
+    // Both warps enumerate the same batches. The loader waits for EMPTY before refilling a box
+    // (not for its first two batches) and arrives FULL; the stepper writes the halo words of
+    // batch i into box i & 1 before waiting for FULL, and arrives EMPTY only when the loader
+    // will wait for it (batch i + 2 exists).
+    auto run = [&](uint32_t i, bool more2, uint32_t u, uint32_t cnt, uint32_t base0) {
+        const int b = (int)(i & 1u);
+        if (loader) {
+            if (i >= 2) nb_sync_empty(b);
+            load_batch(u, cnt, base0, s_box[b]);
+            __syncwarp();
+            nb_arrive_full(b);
+        } else {
+            halo_batch(u, cnt, s_box[b], s_hmask[b]);
+            nb_sync_full(b);
+            step_batch(u, cnt, base0, s_box[b], s_hmask[b]);
+            if (more2) nb_arrive_empty(b);
+        }
+    };
     if constexpr (!BB) {
-        for (uint32_t b = warp_global; b < sb.total; b += nwarps) {
-            uint32_t row, c0, cnt;
-            if (b < sb.nb0) {
+        auto decode = [&](uint32_t bt, uint32_t& row, uint32_t& c0, uint32_t& cnt) {
+            if (bt < sb.nb0) {
                 row = sb.row0;
-                c0 = sb.col0 + 32u * b;
+                c0 = sb.col0 + 32u * bt;
                 cnt = min(32u, sb.col0 + sb.cols0 - c0);
             } else {
-                const uint32_t b2 = b - sb.nb0, q = fastdiv(b2, sb.div_nb_row);
+                const uint32_t b2 = bt - sb.nb0, q = fastdiv(b2, sb.div_nb_row);
                 if (q < sb.mid_rows) {
                     row = sb.row0 + 1u + q;
                     c0 = 32u * (b2 - q * sb.nb_row);
@@ -294,32 +369,47 @@ __global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB) ca_compact_s
                     cnt = min(32u, sb.last_cols - c0);
                 }
             }
-            batch(row * a.Hb + c0 + (uint32_t)lane, cnt, 9u * row * a.W + 27u * c0);
+        };
+        uint32_t i = 0;
+        for (uint32_t bt = blockIdx.x; bt < sb.total; bt += gridDim.x, ++i) {
+            uint32_t row, c0, cnt;
+            decode(bt, row, c0, cnt);
+            run(i, bt + 2u * gridDim.x < sb.total, row * a.Hb + c0 + (uint32_t)lane, cnt, 9u * row * a.W + 27u * c0);
         }
     } else {
-        // the warps scan the (n/32)^2 box tiles in windows of 32, window i by warp i mod nwarps
+        // both warps scan the (n/32)^2 box tiles in windows of 32, window j by CTA j mod grid
         // (interleaved: box rows hold 2^popc(by) member tiles, so contiguous ranges would not
-        // balance); a box tile holds members iff bx ⊆ by — the reference's threads of the other
-        // tiles all fail their membership test
+        // balance), and batch the member tiles in the same order; a box tile holds members iff
+        // bx ⊆ by — the reference's threads of the other tiles all fail their membership test
         const uint32_t nbox = (uint32_t)(a.n >> 5), lg = 31u - __clz(nbox), boxes = nbox * nbox;
-        uint32_t* list = s_list[wib];
         auto tile_of_box = [&](uint32_t bi) -> uint32_t {  // λ⁻¹ at block level
             const uint32_t bx = bi & (nbox - 1u), by = bi >> lg;
             const uint32_t wx = bits_base3(even_bits(bx)) + bits_base3(even_bits(by));
             const uint32_t wy = bits_base3(even_bits(bx >> 1)) + bits_base3(even_bits(by >> 1));
             return wx * a.Hb + wy;
         };
-        uint32_t filled = 0;
-        for (uint32_t b = 32u * warp_global; b < boxes; b += 32u * nwarps) {
-            const uint32_t bi = b + (uint32_t)lane;
+        // the batches of this CTA: counted first (the stepper must know whether batch i + 2 exists)
+        uint32_t members = 0;
+        for (uint32_t bw = 32u * blockIdx.x; bw < boxes; bw += 32u * gridDim.x) {
+            const uint32_t bi = bw + (uint32_t)lane;
+            members += __popc(__ballot_sync(0xFFFFFFFFu, bi < boxes && ((bi & (nbox - 1u)) & ~(bi >> lg)) == 0u));
+        }
+        const uint32_t nbatch = (members + 31u) / 32u;
+        uint32_t filled = 0, i = 0;
+        uint32_t* list = s_list[wib][0];
+        for (uint32_t bw = 32u * blockIdx.x; bw < boxes; bw += 32u * gridDim.x) {
+            const uint32_t bi = bw + (uint32_t)lane;
             const bool m = bi < boxes && ((bi & (nbox - 1u)) & ~(bi >> lg)) == 0u;
             const uint32_t bal = __ballot_sync(0xFFFFFFFFu, m), nm = __popc(bal);
             const uint32_t rank = __popc(bal & ((1u << lane) - 1u));
+            list = s_list[wib][i & 1u];
             if (m && filled + rank < 32u) list[filled + rank] = tile_of_box(bi);
             if (filled + nm >= 32u) {
                 __syncwarp();
-                batch(list[lane], 32u, 0u);
+                run(i, i + 2u < nbatch, list[lane], 32u, 0u);
+                ++i;
                 __syncwarp();
+                list = s_list[wib][i & 1u];
                 if (m && filled + rank >= 32u) list[filled + rank - 32u] = tile_of_box(bi);
                 filled = filled + nm - 32u;
             } else {
@@ -327,7 +417,7 @@ __global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB) ca_compact_s
             }
         }
         __syncwarp();
-        if (filled) batch(lane < (int)filled ? list[lane] : 0u, filled, 0u);
+        if (filled) run(i, false, lane < (int)filled ? list[lane] : 0u, filled, 0u);
     }
     if (P2P) p2p_arrive(p);
 }

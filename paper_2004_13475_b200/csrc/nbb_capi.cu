@@ -897,12 +897,22 @@ template <bool P2P, bool BB>
 void (*sliced_kernel(bool conway))(CompactCaArgs, SliceBatches, FastDiv, const int32_t*, P2PArgs) {
     return conway ? ca_compact_sliced_kernel<true, P2P, BB> : ca_compact_sliced_kernel<false, P2P, BB>;
 }
-// grid of a tile-sliced launch: one wave (resident CTAs), fewer when the batches are fewer
+// grid of a tile-sliced launch: one wave of CTAs (one loader/stepper pipeline each), fewer when
+// the batches are fewer
 int sliced_grid(DeviceCtx* ctx, const void* kern, uint64_t batches, bool bb, unsigned* grid) {
     int occ;
+    static std::mutex m;
+    static std::vector<const void*> carved;  // the shared-memory carveout raised once per kernel
+    {
+        std::lock_guard<std::mutex> lock(m);
+        if (std::find(carved.begin(), carved.end(), kern) == carved.end()) {
+            NBB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            carved.push_back(kern);
+        }
+    }
     NBB_CHECK(pass_occupancy_threads(kern, 32 * kSliceWarps, &occ));
     const uint64_t wave = (uint64_t)ctx->sms * occ;
-    *grid = (unsigned)std::max<uint64_t>(1, bb ? wave : std::min<uint64_t>(wave, (batches + kSliceWarps - 1) / kSliceWarps));
+    *grid = (unsigned)std::max<uint64_t>(1, bb ? wave : std::min<uint64_t>(wave, batches));  // a batch pipeline per CTA
     return NBB_OK;
 }
 
@@ -1035,6 +1045,71 @@ int p2p_passes(const nbb_config* cfg, int64_t first_pass, int32_t steps, int kma
     }
     ps.result_in_b = (int32_t)(j & 1);
     if (stats) *stats = ps;
+    return NBB_OK;
+}
+}  // namespace
+
+#include "nbb_multi.inc"
+
+namespace {
+
+// nbb_gpu_ca on the compact state: member sectors of the host Grid -> the λ-ordered compact array
+// on devices[0] (2 x 8·3^r bytes, no embedded grid), passes over the orthotope (spread over the
+// worker devices when ndev > 1), compact -> member sectors of out_grid.
+int ca_compact_host(const nbb_config* cfg, Launch& L, const int64_t* initial, int64_t* out_grid, nbb_report* per_step,
+                    int32_t steps, uint16_t birth, uint16_t survive, const long long* h_in, long long* h_out,
+                    const int32_t* devices, int32_t ndev) {
+    NBB_CHECK(compact_workload_check(cfg, ndev == 1));
+    if (cfg->cell_width != 8) return fail(NBB_ERR_INVALID_ARGUMENT, "the compact state holds int64 values: cell_width 8");
+    const size_t b64 = grid_bytes(L, 8);
+    CompactShape cs;
+    NBB_CHECK(compact_shape(cfg, &cs));
+    void *ca, *cb, *stage = nullptr;
+    NBB_CHECK(device_buffer(*L.ctx, 1, cs.total * 8, &ca));
+    NBB_CHECK(device_buffer(*L.ctx, 2, cs.total * 8, &cb));
+    const void* src = h_in;
+    if (!src) {  // pageable input: stage the embedded grid in HBM
+        NBB_CHECK(device_buffer(*L.ctx, 0, b64, &stage));
+        NBB_CUDA(cudaMemcpyAsync(stage, initial, b64, cudaMemcpyHostToDevice, L.stream));
+        src = stage;
+    }
+    // member sectors -> compact in embedded row order (host pages stay sequential)
+    compact_from_rows_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)src, (long long*)ca,
+                                                                    (int64_t)cs.n, (uint32_t)cs.W);
+    NBB_CUDA(cudaGetLastError());
+    if (ndev > 1) {  // the worker split over devices
+        nbb_pass_stats ps;
+        NBB_CHECK(multi_device_passes(cfg, devices, ndev, ca, cb, steps, birth, survive, L.stream, &ps));
+        if (per_step)
+            for (int s = 0; s < steps; ++s) fill_report(cfg, &per_step[s], 0);
+        if (ps.result_in_b) std::swap(ca, cb);
+    } else if (cfg->timing) {  // per-step launch times: one launch per step
+        NBB_CHECK(check_pass_steps(cfg));
+        for (int s = 0; s < steps; ++s) {
+            Timer t(true, L.stream);
+            NBB_CHECK(launch_pass(L.ctx, cfg, ca, cb, 1, birth, survive, L.stream));
+            const uint64_t us = t.stop_micros();
+            if (per_step) fill_report(cfg, &per_step[s], us);
+            std::swap(ca, cb);
+        }
+    } else {  // passes of up to pass_steps steps; the result in whichever buffer the last pass wrote
+        nbb_pass_stats ps;
+        NBB_CHECK(run_ca_compact(L.ctx, cfg, ca, cb, steps, birth, survive, L.stream, false, &ps));
+        if (per_step)
+            for (int s = 0; s < steps; ++s) fill_report(cfg, &per_step[s], 0);
+        if (ps.result_in_b) std::swap(ca, cb);
+    }
+    if (h_out) {  // member sectors straight into the zeroed pinned output, row by row
+        compact_to_rows_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)ca, h_out, (int64_t)cs.n,
+                                                                      (uint32_t)cs.W);
+        NBB_CUDA(cudaGetLastError());
+    } else {
+        if (!stage) NBB_CHECK(device_buffer(*L.ctx, 0, b64, &stage));
+        NBB_CUDA(cudaMemsetAsync(stage, 0, b64, L.stream));
+        NBB_CHECK(compact_to_sectors(L.ctx, cfg, ca, stage, L.stream));
+        NBB_CUDA(cudaMemcpyAsync(out_grid, stage, b64, cudaMemcpyDeviceToHost, L.stream));
+    }
+    NBB_CUDA(cudaStreamSynchronize(L.stream));
     return NBB_OK;
 }
 }  // namespace
@@ -1373,53 +1448,7 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
     const bool compact_ok = gasket && cw == 8 && cfg->r >= 5 && cfg->r <= 18 && cfg->kernel == NBB_KERNEL_AUTO &&
                             cfg->shard_count == 0;
     if ((cfg->flags & NBB_FLAG_COMPACT_STATE) || (compact_ok && !(cfg->flags & NBB_FLAG_EMBEDDED_STATE))) {
-        // compact state: member sectors -> the λ-ordered compact array (2 x 8·3^r bytes on the
-        // device, no embedded grid), passes over the orthotope, compact -> member sectors.
-        NBB_CHECK(compact_workload_check(cfg, true));
-        if (cw != 8) return fail(NBB_ERR_INVALID_ARGUMENT, "the compact state holds int64 values: cell_width 8");
-        CompactShape cs;
-        NBB_CHECK(compact_shape(cfg, &cs));
-        void *ca, *cb, *stage = nullptr;
-        NBB_CHECK(device_buffer(*L.ctx, 1, cs.total * 8, &ca));
-        NBB_CHECK(device_buffer(*L.ctx, 2, cs.total * 8, &cb));
-        const void* src = h_in;
-        if (!src) {  // pageable input: stage the embedded grid in HBM
-            NBB_CHECK(device_buffer(*L.ctx, 0, b64, &stage));
-            NBB_CUDA(cudaMemcpyAsync(stage, initial, b64, cudaMemcpyHostToDevice, L.stream));
-            src = stage;
-        }
-        // member sectors -> compact in embedded row order (host pages stay sequential)
-        compact_from_rows_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)src, (long long*)ca,
-                                                                        (int64_t)cs.n, (uint32_t)cs.W);
-        NBB_CUDA(cudaGetLastError());
-        if (cfg->timing) {  // per-step launch times: one launch per step
-            NBB_CHECK(check_pass_steps(cfg));
-            for (int s = 0; s < steps; ++s) {
-                Timer t(true, L.stream);
-                NBB_CHECK(launch_pass(L.ctx, cfg, ca, cb, 1, birth, survive, L.stream));
-                const uint64_t us = t.stop_micros();
-                if (per_step) fill_report(cfg, &per_step[s], us);
-                std::swap(ca, cb);
-            }
-        } else {  // passes of up to 4 steps; the result in whichever buffer the last pass wrote
-            nbb_pass_stats ps;
-            NBB_CHECK(run_ca_compact(L.ctx, cfg, ca, cb, steps, birth, survive, L.stream, false, &ps));
-            if (per_step)
-                for (int s = 0; s < steps; ++s) fill_report(cfg, &per_step[s], 0);
-            if (ps.result_in_b) std::swap(ca, cb);
-        }
-        if (h_out) {  // member sectors straight into the zeroed pinned output, row by row
-            compact_to_rows_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)ca, h_out,
-                                                                          (int64_t)cs.n, (uint32_t)cs.W);
-            NBB_CUDA(cudaGetLastError());
-        } else {
-            if (!stage) NBB_CHECK(device_buffer(*L.ctx, 0, b64, &stage));
-            NBB_CUDA(cudaMemsetAsync(stage, 0, b64, L.stream));
-            NBB_CHECK(compact_to_sectors(L.ctx, cfg, ca, stage, L.stream));
-            NBB_CUDA(cudaMemcpyAsync(out_grid, stage, b64, cudaMemcpyDeviceToHost, L.stream));
-        }
-        NBB_CUDA(cudaStreamSynchronize(L.stream));
-        return NBB_OK;
+        return ca_compact_host(cfg, L, initial, out_grid, per_step, steps, birth, survive, h_in, h_out, nullptr, 1);
     }
     void *d64 = nullptr, *da, *db;
     if (cw == 8) {
@@ -1482,6 +1511,94 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
     }
     NBB_CUDA(cudaMemcpyAsync(out_grid, da, b64, cudaMemcpyDeviceToHost, L.stream));
     NBB_CUDA(cudaStreamSynchronize(L.stream));
+    return NBB_OK;
+}
+
+int nbb_gpu_ca_multi(const nbb_config* cfg, const int32_t* devices, int32_t ndev, const int64_t* initial,
+                     int32_t initial_level, int32_t steps, uint16_t birth, uint16_t survive, int64_t* out_grid,
+                     nbb_report* per_step) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    NBB_CHECK(check_devices(devices, ndev));
+    nbb_config c = *cfg;
+    c.device = devices[0];
+    if (ndev == 1) return nbb_gpu_ca(&c, initial, initial_level, steps, birth, survive, out_grid, per_step);
+    NBB_TRY(nbbhost::validate(c));
+    if (initial_level != c.r) return fail(NBB_ERR_INVALID_ARGUMENT, "ca: grid level does not match the configured r");
+    if (steps < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "ca: negative step count");
+    if (c.shard_count > 0) return fail(NBB_ERR_INVALID_ARGUMENT, "multi: the devices split the whole tile range");
+    if (c.flags & NBB_FLAG_EMBEDDED_STATE)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "multi: the worker split runs on the compact state");
+    Launch L;
+    NBB_CHECK(prepare(&c, OP_CA, &L, true));
+    L.stream = L.ctx->stream;
+    if (steps == 0) {
+        if (out_grid != initial) std::memmove(out_grid, initial, grid_bytes(L, 8));
+        return NBB_OK;
+    }
+    const long long* h_in = (const long long*)mapped_host_ptr(initial);
+    long long* h_out = (c.flags & NBB_FLAG_OUT_ZEROED) ? (long long*)mapped_host_ptr(out_grid) : nullptr;
+    return ca_compact_host(&c, L, initial, out_grid, per_step, steps, birth, survive, h_in, h_out, devices, ndev);
+}
+
+int nbb_gpu_reduction_multi(const nbb_config* cfg, const int32_t* devices, int32_t ndev, const int64_t* grid,
+                            int32_t grid_level, int64_t* value, nbb_report* report) {
+    if (!cfg || !value) return fail(NBB_ERR_INVALID_ARGUMENT, "null argument");
+    NBB_CHECK(check_devices(devices, ndev));
+    nbb_config c = *cfg;
+    c.device = devices[0];
+    if (ndev == 1) return nbb_gpu_reduction(&c, grid, grid_level, value, report);
+    NBB_TRY(nbbhost::validate(c));
+    if (grid_level != c.r)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "reduction: grid level " + std::to_string(grid_level) +
+                                                  " does not match the configured r = " + std::to_string(c.r));
+    NBB_CHECK(compact_workload_check(&c));
+    Launch L;
+    NBB_CHECK(prepare(&c, OP_RD, &L, false));
+    L.stream = L.ctx->stream;
+    CompactShape cs;
+    NBB_CHECK(compact_shape(&c, &cs));
+    const size_t b64 = grid_bytes(L, 8), bytes = (size_t)cs.total * 8;
+    void *stage, *ca;
+    NBB_CHECK(device_buffer(*L.ctx, 0, b64, &stage));
+    NBB_CHECK(device_buffer(*L.ctx, 1, bytes, &ca));
+    NBB_CUDA(cudaMemcpyAsync(stage, grid, b64, cudaMemcpyHostToDevice, L.stream));
+    compact_from_rows_kernel<<<L.ctx->sms * 8, 256, 0, L.stream>>>((const long long*)stage, (long long*)ca,
+                                                                    (int64_t)cs.n, (uint32_t)cs.W);
+    NBB_CUDA(cudaGetLastError());
+    NBB_CUDA(cudaStreamSynchronize(L.stream));
+    // worker w sums its chunk of tiles on its device; the partial sums add up on the host (int64
+    // addition wraps like the reference's accumulation, so any split gives the same value)
+    FastDiv d;
+    const CompactCaArgs a = compact_args(&c, nullptr, nullptr, 0, 0, &d);
+    const uint32_t chunk = (a.tiles + (uint32_t)ndev - 1) / (uint32_t)ndev;
+    unsigned long long total = 0;
+    for (int w = 0; w < ndev; ++w) {
+        nbb_config wc = c;
+        wc.device = devices[w];
+        wc.shard_begin = std::min<uint64_t>((uint64_t)chunk * (uint64_t)w, a.tiles);
+        wc.shard_count = std::min<uint64_t>((uint64_t)chunk, a.tiles - wc.shard_begin);
+        if (wc.shard_count == 0) continue;
+        DeviceCtx* ctx;
+        NBB_CHECK(ensure_device(devices[w], &ctx));
+        void* mine = ca;
+        if (devices[w] != devices[0]) {
+            NBB_CHECK(device_buffer(*ctx, 1, bytes, &mine));
+            NBB_CUDA(cudaMemcpyPeerAsync(mine, devices[w], ca, devices[0], bytes, ctx->stream));
+        }
+        Segs sg;
+        NBB_CHECK(compact_segments(&wc, &sg));
+        unsigned long long* part = ctx->partials + 4096;
+        NBB_CUDA(cudaMemsetAsync(part, 0, 8, ctx->stream));
+        segment_sum_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>((const long long*)mine, sg, part);
+        NBB_CUDA(cudaGetLastError());
+        unsigned long long v = 0;
+        NBB_CUDA(cudaMemcpyAsync(&v, part, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        NBB_CUDA(cudaStreamSynchronize(ctx->stream));
+        total += v;
+    }
+    NBB_CUDA(cudaSetDevice(devices[0]));
+    *value = (int64_t)total;
+    fill_report(&c, report, 0);
     return NBB_OK;
 }
 
@@ -1816,3 +1933,5 @@ int nbb_gpu_release(void) {
 }
 
 }  // extern "C"
+
+#include "nbb_comm.inc"

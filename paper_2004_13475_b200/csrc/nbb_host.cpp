@@ -656,3 +656,79 @@ Error slice_slots(SliceSlots* out) {
     return {};
 }
 }  // namespace nbbhost
+
+// ---- halo exchange lists of the multi-process compact CA (see nbb_host.hpp) ----------------
+namespace nbbhost {
+namespace {
+uint64_t digits_to_bits(uint64_t v, bool two_only) {  // X(v) (digit 2) / Y(v) (digit >= 1) at even bits
+    uint64_t out = 0;
+    for (int j = 0; v; ++j, v /= 3) {
+        const uint64_t d = v % 3;
+        if (two_only ? d == 2 : d >= 1) out |= 1ull << (2 * j);
+    }
+    return out;
+}
+uint64_t even_bits_base3(uint64_t b) {  // bits 0, 2, 4, ... of b read as base-3 digits in {0, 1}
+    uint64_t v = 0, p = 1;
+    for (int j = 0; j < 64; j += 2, p *= 3) v += ((b >> j) & 1u) * p;
+    return v;
+}
+}  // namespace
+
+Error halo_exchange_lists(int r, int world, int rank, int kmax, std::vector<std::vector<uint32_t>>* send,
+                          std::vector<std::vector<uint32_t>>* recv) {
+    if (r < 5 || r > 18) return err(NBB_ERR_INVALID_ARGUMENT, "halo exchange: 5 <= r <= 18");
+    if (world < 1 || rank < 0 || rank >= world) return err(NBB_ERR_INVALID_ARGUMENT, "halo exchange: 0 <= rank < world");
+    if (kmax < 1 || kmax > kSliceMaxK) return err(NBB_ERR_INVALID_ARGUMENT, "halo exchange: 1 <= kmax <= 8");
+    SliceSlots ss;
+    Error e = slice_slots(&ss);
+    if (!e.ok()) return e;
+    const int rb = r - 5;
+    uint64_t W = 1, Wb = 1, Hb = 1;
+    for (int i = 0; i < (r + 1) / 2; ++i) W *= 3;
+    for (int i = 0; i < (rb + 1) / 2; ++i) Wb *= 3;
+    for (int i = 0; i < rb / 2; ++i) Hb *= 3;
+    const uint64_t tiles = Wb * Hb, nb = uint64_t(1) << rb;
+    const uint64_t chunk = (tiles + (uint64_t)world - 1) / (uint64_t)world;
+    auto owner = [&](uint64_t u) { return (int)(u / chunk); };
+    auto base = [&](uint64_t u) { return 9 * (u / Hb) * W + 27 * (u % Hb); };
+    // slot offsets inside a neighbouring tile, per direction, layers <= kmax
+    std::vector<uint32_t> loc[8];
+    for (int d = 0; d < 8; ++d)
+        for (int j = 0; j < ss.dir_upto[d][kmax]; ++j) {
+            const uint32_t li = ss.li[ss.by_dir[d][j]];
+            loc[d].push_back((uint32_t)((li / 27) * W + li % 27));
+        }
+    auto neighbour = [&](uint64_t u, int d, uint64_t* out) {  // tile ordinal in direction d, if any
+        const int d9 = d < 4 ? d : d + 1;
+        const uint64_t wx = u / Hb, wy = u % Hb;
+        const uint64_t bx = digits_to_bits(wx, true) | digits_to_bits(wy, true) << 1;
+        const uint64_t by = digits_to_bits(wx, false) | digits_to_bits(wy, false) << 1;
+        const int64_t qx = (int64_t)bx + d9 % 3 - 1, qy = (int64_t)by + d9 / 3 - 1;
+        if (qx < 0 || qy < 0 || (uint64_t)qx >= nb || (uint64_t)qy >= nb || ((uint64_t)qx & (uint64_t)qy) != (uint64_t)qx)
+            return false;
+        *out = (even_bits_base3((uint64_t)qx) + even_bits_base3((uint64_t)qy)) * Hb +
+               even_bits_base3((uint64_t)qx >> 1) + even_bits_base3((uint64_t)qy >> 1);
+        return true;
+    };
+    send->assign((size_t)world, {});
+    recv->assign((size_t)world, {});
+    for (uint64_t u = 0; u < tiles; ++u) {  // the halo cells every tile reads from another rank
+        const int need = owner(u);
+        for (int d = 0; d < 8; ++d) {
+            uint64_t v;
+            if (loc[d].empty() || !neighbour(u, d, &v)) continue;
+            const int has = owner(v);
+            if (has == need || (need != rank && has != rank)) continue;
+            auto& lst = need == rank ? (*recv)[(size_t)has] : (*send)[(size_t)need];
+            for (uint32_t o : loc[d]) lst.push_back((uint32_t)(base(v) + o));
+        }
+    }
+    for (auto* side : {send, recv})
+        for (auto& l : *side) {
+            std::sort(l.begin(), l.end());
+            l.erase(std::unique(l.begin(), l.end()), l.end());
+        }
+    return {};
+}
+}  // namespace nbbhost

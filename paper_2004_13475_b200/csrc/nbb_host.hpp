@@ -8,6 +8,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "nbb_gpu.h"
 
@@ -108,6 +109,14 @@ struct SliceSlots {
     int32_t dir_upto[8][kSliceMaxK + 1];  // per neighbouring tile: slots with layer <= d
 };
 Error slice_slots(SliceSlots* out);
+
+// Halo exchange of the multi-process compact CA (NCCL transport): with `world` ranks owning
+// contiguous chunks of ceil(tiles / world) ρ = 32 tiles (dispatch.cpp:419-427), recv[j] = the
+// compact offsets of rank j's cells that lie in a halo slot of layer <= kmax of one of `rank`'s
+// tiles, send[j] = the offsets of `rank`'s cells that rank j needs; sorted, unique. send[j] on
+// rank i equals recv[i] on rank j by construction.
+Error halo_exchange_lists(int r, int world, int rank, int kmax, std::vector<std::vector<uint32_t>>* send,
+                          std::vector<std::vector<uint32_t>>* recv);
 
 // precomputed fast division magic (see common.cuh FastDiv), exact for x < 2^31
 void fastdiv_magic(uint32_t d, uint32_t* m, uint32_t* s);

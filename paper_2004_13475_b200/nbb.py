@@ -420,6 +420,34 @@ def run_ca(config: DispatchConfig, initial: Grid, steps: int, rule: CaRule = CaR
     return CaResult(out, [WorkReport.from_c(reps[i]) for i in range(steps)])
 
 
+def _devices(devices) -> tuple:
+    ds = [int(d) for d in devices]
+    return (ctypes.c_int32 * len(ds))(*ds), len(ds)
+
+
+def run_ca_multi(config: DispatchConfig, devices, initial: Grid, steps: int, rule: CaRule = CaRule()) -> CaResult:
+    """run_ca with the reference's workers mapped to `devices` of this process (nbb_gpu_ca_multi):
+    contiguous chunks of the compact tile range, halos over peer memory; byte-identical for any
+    device list (devices may repeat)."""
+    arr, nd = _devices(devices)
+    out = Grid(initial.spec, initial.level())
+    reps = (_abi.NbbReport * max(steps, 1))()
+    _check(_lib().nbb_gpu_ca_multi(ctypes.byref(config.to_c()), arr, nd, initial._ptr(), initial.level(), steps,
+                                   rule.birth, rule.survive, out._ptr(), reps))
+    out._generation = initial.generation() + steps
+    return CaResult(out, [WorkReport.from_c(reps[i]) for i in range(steps)])
+
+
+def run_reduction_multi(config: DispatchConfig, devices, grid: Grid) -> ReductionResult:
+    """run_reduction with one worker (contiguous tile chunk) per entry of `devices`."""
+    arr, nd = _devices(devices)
+    v = ctypes.c_int64()
+    rep = _abi.NbbReport()
+    _check(_lib().nbb_gpu_reduction_multi(ctypes.byref(config.to_c()), arr, nd, grid._ptr(), grid.level(),
+                                          ctypes.byref(v), ctypes.byref(rep)))
+    return ReductionResult(v.value, WorkReport.from_c(rep))
+
+
 def work_quotient(bounding_box: WorkReport, lam: WorkReport, weighted: bool = False) -> float:
     q = ctypes.c_double()
     _check(_lib().nbb_gpu_work_quotient(ctypes.byref(bounding_box.to_c()), ctypes.byref(lam.to_c()),

@@ -484,3 +484,70 @@ class P2PCompactCA:
 def _check(rc: int) -> None:
     from .nbb import _check as check
     check(rc)
+
+
+class NcclCompactCA:
+    """The multi-process compact CA over the library's own NCCL communicator (nbb_gpu_comm_*,
+    include/nbb_gpu.h): one process per GPU, rank i owning the contiguous tile chunk i of
+    ceil(tiles / world) (dispatch.cpp:419-427); before every pass of up to 8 steps the halo cells
+    its tiles read from other ranks within 8 steps are exchanged by ncclSend / ncclRecv inside the
+    library, then the pass kernel advances the rank's tiles. The communicator's id travels over
+    the caller's process group (`dist`, any backend); dist=None is a single rank."""
+
+    def __init__(self, r: int, dist=None, device: int = 0):
+        import ctypes
+        import torch
+        from . import _abi
+        self.lib = lib = _abi.load()
+        self.r, self.device = r, device
+        self.world = dist.get_world_size() if dist is not None else 1
+        self.rank = dist.get_rank() if dist is not None else 0
+        uid = (ctypes.c_uint8 * 128)()
+        if self.rank == 0:
+            _check(lib.nbb_gpu_comm_unique_id(uid))
+        if dist is not None:
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0)
+            uid = (ctypes.c_uint8 * 128).from_buffer_copy(box[0])
+        self._comm = ctypes.c_void_p()
+        _check(lib.nbb_gpu_comm_init(uid, self.world, self.rank, device, ctypes.byref(self._comm)))
+        dev = torch.device("cuda", device)
+        self.buffers = [torch.zeros(3 ** r, dtype=torch.int64, device=dev) for _ in range(2)]
+        self.cur = 0
+        self.passes = 0
+
+    def load(self, compact_state) -> None:
+        """Set the state (a (3^r,) int64 tensor; this rank's tiles must be current)."""
+        self.buffers[0].copy_(compact_state.to(self.buffers[0].device).view(-1))
+        self.cur = 0
+
+    def state(self):
+        return self.buffers[self.cur]
+
+    def run(self, config, rule, steps: int, stream) -> None:
+        import ctypes
+        from . import _abi
+        st = _abi.NbbPassStats()
+        a, b = self.buffers[self.cur], self.buffers[self.cur ^ 1]
+        _check(self.lib.nbb_gpu_ca_compact_comm_dev(ctypes.byref(config.to_c()), self._comm,
+                                                    ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
+                                                    steps, rule.birth, rule.survive, ctypes.c_void_p(stream),
+                                                    ctypes.byref(st)))
+        self.cur ^= st.result_in_b
+        self.passes += st.passes
+
+    def reduction(self, config, stream) -> int:
+        """run_reduction of the current state: the rank's partial sum + one ncclAllReduce."""
+        import ctypes
+        import torch
+        out = torch.empty(1, dtype=torch.int64, device=self.buffers[0].device)
+        _check(self.lib.nbb_gpu_reduction_compact_comm_dev(ctypes.byref(config.to_c()), self._comm,
+                                                           ctypes.c_void_p(self.state().data_ptr()),
+                                                           ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream)))
+        torch.cuda.synchronize(self.device)
+        return int(out.item())
+
+    def close(self) -> None:
+        if self._comm:
+            _check(self.lib.nbb_gpu_comm_destroy(self._comm))
+            self._comm = None

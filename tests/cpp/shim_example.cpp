@@ -60,5 +60,13 @@ int main(int argc, char** argv) {
     std::printf("ca13 compact3 %016llx\n", (unsigned long long)fnv(g::run_ca(c13, init13, 20).grid.values()));
     c13.state = g::DispatchConfig::State::Embedded;
     std::printf("ca13 embedded %016llx\n", (unsigned long long)fnv(g::run_ca(c13, init13, 20).grid.values()));
+    // the reference's workers as devices: 3 workers (on device 0 when it is the only GPU)
+    c13.state = g::DispatchConfig::State::Auto;
+    c13.pass_steps = 0;
+    int ndev = 0;
+    g::check(nbb_gpu_device_count(&ndev));
+    const std::vector<int> devs = {0, 1 % ndev, 2 % ndev};
+    std::printf("ca13 workers %016llx\n",
+                (unsigned long long)fnv(g::run_ca(c13, init13, 20, g::CaRule{}, devs).grid.values()));
     return (sum == 59049 && pop == 10398) ? 0 : 2;
 }

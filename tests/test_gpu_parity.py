@@ -467,8 +467,8 @@ def test_cpp_shim_on_gpu():
     assert "ca pop 10398" in r.stdout
     # nbb::gpu::run_ca (the reference signature) at n = 2^13, 20 steps: default (compact) state,
     # compact with 3 steps per pass, embedded int64 grid — all equal the C oracle
-    want = f"{fnv1a64(orc_ca(13, orc_random_member_grid(13, 14, 2), 20)):016x}"
-    for tag in ("default", "compact3", "embedded"):
+    want = fnv1a64(orc_ca(13, orc_random_member_grid(13, 14, 2), 20))
+    for tag in ("default", "compact3", "embedded", "workers"):
         assert f"ca13 {tag} {want}" in r.stdout, (tag, want, r.stdout)
 
 
