@@ -237,8 +237,10 @@ __global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB)
                 const bool ex = nbr6[q] >= 0;
                 unsigned long long ptr = 0ull;
                 if (ex) {
-                    const long long* src = P2P ? s_peer[fastdiv((uint32_t)nbr6[q], p.div_chunk)] : a.src;
+                    const uint32_t own = P2P ? fastdiv((uint32_t)nbr6[q], p.div_chunk) : 0u;
+                    const long long* src = P2P ? s_peer[own] : a.src;
                     ptr = reinterpret_cast<unsigned long long>(src) + 8ull * tile_base((uint32_t)nbr6[q]);
+                    if (P2P && own != (uint32_t)p.rank) ptr |= 1ull;  // bit 0: another rank's buffer
                 }
                 s_hp[q][lane] = ptr;
                 const uint32_t dm = __ballot_sync(0xFFFFFFFFu, ex);
@@ -260,8 +262,8 @@ __global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB)
                 for (int i = 0; i < kSliceLanesSlots; ++i) {
                     long long v = 0;
                     if (P != 0ull && hslot[i] != 0xFFFFu) {
-                        const long long* q = reinterpret_cast<const long long*>(P + hloc[i]);
-                        if (P2P)
+                        const long long* q = reinterpret_cast<const long long*>((P & ~1ull) + hloc[i]);
+                        if (P2P && (P & 1ull))  // a cell of another rank's tile: its buffer over NVLink
                             asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(q));
                         else
                             v = __ldg(q);
