@@ -775,11 +775,12 @@ int compact_nbr_table(DeviceCtx* ctx, const nbb_config* cfg, const CompactCaArgs
 // kernel on the stream drains; kernels launched this way call griddepcontrol.wait before
 // touching memory the previous kernel writes (ca_compact_pass_kernel: pdl_wait()).
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args&&... args) {
+cudaError_t launch_pdl_smem(void (*k)(KArgs...), unsigned grid, unsigned block, size_t dyn_smem, cudaStream_t st,
+                            Args&&... args) {
     cudaLaunchConfig_t c = {};
     c.gridDim = dim3(grid);
     c.blockDim = dim3(block);
-    c.dynamicSmemBytes = 0;
+    c.dynamicSmemBytes = dyn_smem;
     c.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -787,6 +788,10 @@ cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaS
     c.attrs = at;
     c.numAttrs = 1;
     return cudaLaunchKernelEx(&c, k, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args&&... args) {
+    return launch_pdl_smem(k, grid, block, 0, st, std::forward<Args>(args)...);
 }
 
 bool is_conway(uint16_t birth, uint16_t survive) {  // CaRule{} (B3/S23): its own instantiation
@@ -897,22 +902,37 @@ template <bool P2P, bool BB>
 void (*sliced_kernel(bool conway))(CompactCaArgs, SliceBatches, FastDiv, const int32_t*, P2PArgs) {
     return conway ? ca_compact_sliced_kernel<true, P2P, BB> : ca_compact_sliced_kernel<false, P2P, BB>;
 }
-// grid of a tile-sliced launch: one wave of CTAs (one loader/stepper pipeline each), fewer when
-// the batches are fewer
+// grid of a tile-sliced launch: one wave of CTAs (kSlicePipes loader/stepper pipelines each),
+// fewer when the batches are fewer
 int sliced_grid(DeviceCtx* ctx, const void* kern, uint64_t batches, bool bb, unsigned* grid) {
     int occ;
     static std::mutex m;
-    static std::vector<const void*> carved;  // the shared-memory carveout raised once per kernel
+    static std::vector<const void*> carved;  // carveout + dynamic smem limit raised once per kernel
+    const size_t dyn = bb ? 0 : kSliceDynSmem;
     {
         std::lock_guard<std::mutex> lock(m);
         if (std::find(carved.begin(), carved.end(), kern) == carved.end()) {
             NBB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            NBB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
             carved.push_back(kern);
         }
     }
-    NBB_CHECK(pass_occupancy_threads(kern, 32 * kSliceWarps, &occ));
+    {
+        static std::mutex mo;
+        static std::vector<std::pair<const void*, int>> cache;
+        std::lock_guard<std::mutex> lock(mo);
+        occ = 0;
+        for (auto& e : cache)
+            if (e.first == kern) occ = e.second;
+        if (!occ) {
+            NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kSliceWarps, dyn));
+            if (occ < 1) occ = 1;
+            cache.push_back({kern, occ});
+        }
+    }
     const uint64_t wave = (uint64_t)ctx->sms * occ;
-    *grid = (unsigned)std::max<uint64_t>(1, bb ? wave : std::min<uint64_t>(wave, batches));  // a batch pipeline per CTA
+    *grid = (unsigned)std::max<uint64_t>(  // kSlicePipes batch pipelines per CTA
+        1, bb ? wave : std::min<uint64_t>(wave, (batches + kSlicePipes - 1) / kSlicePipes));
     return NBB_OK;
 }
 
@@ -944,7 +964,8 @@ int launch_pass(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* ds
                        : sliced_kernel<false, false>(is_conway(birth, survive));
         unsigned grid;
         NBB_CHECK(sliced_grid(ctx, (const void*)kern, sb.total, bb, &grid));
-        NBB_CUDA(launch_pdl(kern, grid, 32 * kSliceWarps, st, a, sb, div_hb, tab, P2PArgs{}));
+        NBB_CUDA(launch_pdl_smem(kern, grid, 32 * kSliceWarps, bb ? 0 : kSliceDynSmem, st, a, sb, div_hb, tab,
+                                 P2PArgs{}));
         return NBB_OK;
     }
     auto kern = bb ? pass_kernel_k<false, true>(k, is_conway(birth, survive))
@@ -1030,7 +1051,7 @@ int p2p_passes(const nbb_config* cfg, int64_t first_pass, int32_t steps, int kma
             auto kern = sliced_kernel<true, false>(conway);
             unsigned grid;
             NBB_CHECK(sliced_grid(ctx, (const void*)kern, std::max<uint64_t>(1, sb.total), false, &grid));
-            NBB_CUDA(launch_pdl(kern, grid, 32 * kSliceWarps, stream, a, sb, div_hb, tab, p));
+            NBB_CUDA(launch_pdl_smem(kern, grid, 32 * kSliceWarps, kSliceDynSmem, stream, a, sb, div_hb, tab, p));
             ++ps.passes;
             ++ps.by_steps[passes[i]];
             continue;
