@@ -395,6 +395,19 @@ def main():
         head_ms, head_all = timed_run(run, K, W, sampler, reps=5)
         k1, np1, by1 = st["stats"][1]  # the first timed run of K steps
         head_stats = {"passes": np1, "by_steps": by1}
+    nccl_line = None
+    if world > 1 and p2p is not None and world <= ndev:  # the other transport: the library's NCCL communicator
+        try:
+            c1.copy_(c0)
+            ca_n = shard.NcclCompactCA(r, dist, local)
+            ca_n.load(c1)
+            n_ms, n_all = timed_run(lambda k: ca_n.run(cfg(), CONWAY, k, s), K, W, None, reps=3)
+            ca_n.close()
+            nccl_line = {"transport": "nbb_gpu_ca_compact_comm_dev: halo cells by ncclSend/ncclRecv before every "
+                                      "pass (gather + group exchange + scatter), same passes",
+                         "ms_per_step": n_ms, "value": members * 1e3 / n_ms, "runs": n_all}
+        except Exception as e:  # noqa: BLE001 - report, keep the p2p line
+            nccl_line = {"error": f"{type(e).__name__}: {e}"}
     value = members * 1e3 / head_ms  # all ranks together update the 3^r cells per step
     results["ca_lambda_compact_i64"] = head_ms
     gpu_launches = head_stats["passes"] * (3 if launches_per_step == 3 else 1)
@@ -482,6 +495,15 @@ def main():
     sweep = None
     if extras:
         results["ca_lambda_tile_rho32_i64"], _ = timed_run(ca_runner(cfg(), a, b), K, W)
+        # the same K steps on the embedded int64 grid, temporally blocked (nbb_gpu_ca_run_dev: member
+        # sectors -> compact state -> passes -> member sectors of the result buffer)
+        eb = {"x": 0}
+
+        def emb_run(k):
+            bufs = (a, b)
+            dev.ca_run_dev(cfg(), bufs[eb["x"]].data_ptr(), bufs[eb["x"] ^ 1].data_ptr(), k, CONWAY, s)
+            eb["x"] ^= k & 1
+        results["ca_lambda_embedded_i64_blocked"], _ = timed_run(emb_run, K, W)
         variants = {
             "ca_bb_tile_rho32_i64": cfg(mode=nbb.MapMode.BoundingBox),
             "ca_bb_percell_rho32_i64": cfg(mode=nbb.MapMode.BoundingBox, kernel=nbb.KernelFamily.PerCell),
@@ -645,7 +667,18 @@ def main():
         "workloads_cells_per_s": {k: cells(k) for k in results},
         "map_sweep_C4": sweep,
         "c5_r17": c5,
+        "nccl_transport": nccl_line,
         "rd_compact": rd_line,
+        "embedded_int64": None if "ca_lambda_tile_rho32_i64" not in results else {
+            "note": "the same K steps on the reference's int64 embedded Grid in HBM: one launch per step "
+                    "(ca_pipe_kernel) and temporally blocked (nbb_gpu_ca_run_dev: the member sectors go once "
+                    "into the compact state, K steps in passes, back into the member sectors)",
+            "one_step_per_launch_ms": results["ca_lambda_tile_rho32_i64"],
+            "blocked_ms_per_step": results.get("ca_lambda_embedded_i64_blocked"),
+            "sector_roofline_ms_per_step": 2 * layout_bytes_per_pass(r, 8) / (peak * 1e9) * 1e3,
+            "blocked_frac_of_sector_roofline_per_step": (2 * layout_bytes_per_pass(r, 8) / (peak * 1e9) * 1e3) /
+                                                        results["ca_lambda_embedded_i64_blocked"]
+                                                        if "ca_lambda_embedded_i64_blocked" in results else None},
         "one_step_per_launch": None if "ca_lambda_compact_i64_single_step" not in results else {
             "ms_per_step": results["ca_lambda_compact_i64_single_step"],
             "value": cells("ca_lambda_compact_i64_single_step"),

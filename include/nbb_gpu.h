@@ -147,6 +147,13 @@ typedef struct nbb_report {
     uint64_t micros;
 } nbb_report;
 
+/* What a pass sequence did: launches, launches per step count, where the result is. */
+typedef struct nbb_pass_stats {
+    int32_t passes;       /* kernel launches (passes over the state)                  */
+    int32_t by_steps[9];  /* by_steps[k]: passes that advanced k steps (k = 1..8)      */
+    int32_t result_in_b;  /* 1: the state after `steps` steps is in d_b; 0: in d_a     */
+} nbb_pass_stats;
+
 /* ---- library / config helpers ------------------------------------------ */
 int nbb_gpu_abi_version(void);
 const char* nbb_gpu_last_error(void);
@@ -218,6 +225,15 @@ int nbb_gpu_reduction_dev(const nbb_config* cfg, const void* d_grid, void* d_val
  * (true after nbb_gpu_sanitize_dev / a zeroed allocation); they stay 0. */
 int nbb_gpu_ca_step_dev(const nbb_config* cfg, const void* d_src, void* d_dst, uint16_t birth,
                         uint16_t survive, void* stream, nbb_report* report);
+/* `steps` CA steps on an embedded device grid (the reference's layout, d_a initial): the result
+ * is where a run of single steps leaves it (d_a when steps is even, else d_b); the other buffer is
+ * scratch. For the gasket's int64 grid (5 <= r <= 18, kernel AUTO, unsharded, untimed, steps >= 2)
+ * the run is temporally blocked: the member sectors go once into the λ-ordered compact state,
+ * the steps run there in passes of up to pass_steps, and the result comes back into the member
+ * sectors — bit-identical to stepping the embedded grid; otherwise one launch per step. Non-member
+ * cells of both buffers must be 0 (they stay 0). stats (optional): the passes issued. */
+int nbb_gpu_ca_run_dev(const nbb_config* cfg, void* d_a, void* d_b, int32_t steps, uint16_t birth,
+                       uint16_t survive, void* stream, nbb_pass_stats* stats);
 /* Zero every non-member cell of a device grid of cfg->cell_width cells. */
 int nbb_gpu_sanitize_dev(const nbb_config* cfg, void* d_grid, void* stream);
 /* int64 grid -> uint8 alive grid (cell != 0) and back (0/1 -> int64). */
@@ -269,12 +285,6 @@ int nbb_gpu_ca_compact_step_dev(const nbb_config* cfg, const void* d_src, void* 
  * the pass count then has the parity of `steps`, which may cost one pass more). */
 int nbb_gpu_ca_compact_run_dev(const nbb_config* cfg, void* d_a, void* d_b, int32_t steps,
                                uint16_t birth, uint16_t survive, void* stream);
-/* What a pass sequence did: launches, launches per step count, where the result is. */
-typedef struct nbb_pass_stats {
-    int32_t passes;       /* kernel launches (passes over the state)                  */
-    int32_t by_steps[9];  /* by_steps[k]: passes that advanced k steps (k = 1..8)      */
-    int32_t result_in_b;  /* 1: the state after `steps` steps is in d_b; 0: in d_a     */
-} nbb_pass_stats;
 /* The same run with parity = 0: the fewest passes (ceil(steps / pass_steps)), the result in
  * whichever buffer stats->result_in_b names; parity != 0 behaves as nbb_gpu_ca_compact_run_dev.
  * stats may be NULL. */

@@ -144,6 +144,8 @@ SIGNATURES = {
     "nbb_gpu_reduction_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p, RP]),
     "nbb_gpu_ca_step_dev": (c_int, [CP, c_void_p, c_void_p, c_uint16, c_uint16, c_void_p, RP]),
     "nbb_gpu_sanitize_dev": (c_int, [CP, c_void_p, c_void_p]),
+    "nbb_gpu_ca_run_dev": (c_int, [CP, c_void_p, c_void_p, c_int32, c_uint16, c_uint16, c_void_p,
+                                   POINTER(NbbPassStats)]),
     "nbb_gpu_pack_alive_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p]),
     "nbb_gpu_unpack_alive_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p]),
     "nbb_gpu_scatter_members_dev": (c_int, [CP, c_void_p, c_void_p, c_void_p]),

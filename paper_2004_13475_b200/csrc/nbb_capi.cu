@@ -1281,6 +1281,48 @@ int nbb_gpu_ca_step_dev(const nbb_config* cfg, const void* d_src, void* d_dst, u
     return NBB_OK;
 }
 
+int nbb_gpu_ca_run_dev(const nbb_config* cfg, void* d_a, void* d_b, int32_t steps, uint16_t birth, uint16_t survive,
+                       void* stream, nbb_pass_stats* stats) {
+    if (!cfg) return fail(NBB_ERR_INVALID_ARGUMENT, "null config");
+    if (steps < 0) return fail(NBB_ERR_INVALID_ARGUMENT, "run_ca: steps must be non-negative");
+    Launch L;
+    NBB_CHECK(prepare(cfg, OP_CA, &L, true));
+    L.stream = (cudaStream_t)stream;
+    void* res = (steps & 1) ? d_b : d_a;  // where a run of single steps leaves the result
+    const bool blocked = nbbhost::is_gasket(cfg->spec) && cfg->cell_width == 8 && cfg->r >= 5 && cfg->r <= 18 &&
+                         cfg->kernel == NBB_KERNEL_AUTO && !cfg->timing && cfg->shard_count == 0 && steps >= 2 &&
+                         !(cfg->flags & NBB_FLAG_SINGLE_STEP);
+    if (!blocked) {  // one launch per step on the embedded grid
+        nbb_pass_stats ps{};
+        void *src = d_a, *dst = d_b;
+        for (int32_t s = 0; s < steps; ++s) {
+            NBB_CHECK(launch_op(L, OP_CA, src, dst, nullptr, birth, survive));
+            std::swap(src, dst);
+            ++ps.passes;
+            ++ps.by_steps[1];
+        }
+        ps.result_in_b = steps & 1;
+        if (stats) *stats = ps;
+        return NBB_OK;
+    }
+    // temporal blocking of the embedded state: its member sectors -> the λ-ordered compact state
+    // (tile codec), passes of up to pass_steps steps there, compact -> the member sectors of the
+    // result buffer (the same cells a run of single steps writes; non-member cells stay 0)
+    NBB_CHECK(compact_workload_check(cfg, true));
+    CompactShape cs;
+    NBB_CHECK(compact_shape(cfg, &cs));
+    void *ca, *cb;
+    NBB_CHECK(device_buffer(*L.ctx, 1, cs.total * 8, &ca));
+    NBB_CHECK(device_buffer(*L.ctx, 2, cs.total * 8, &cb));
+    NBB_CHECK(compact_from_sectors(L.ctx, cfg, d_a, ca, L.stream));
+    nbb_pass_stats ps;
+    NBB_CHECK(run_ca_compact(L.ctx, cfg, ca, cb, steps, birth, survive, L.stream, false, &ps));
+    NBB_CHECK(compact_to_sectors(L.ctx, cfg, ps.result_in_b ? cb : ca, res, L.stream));
+    ps.result_in_b = steps & 1;
+    if (stats) *stats = ps;
+    return NBB_OK;
+}
+
 int nbb_gpu_sanitize_dev(const nbb_config* cfg, void* d_grid, void* stream) {
     Launch L;
     NBB_CHECK(prepare(cfg, OP_CA, &L, false, true));

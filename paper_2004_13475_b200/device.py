@@ -40,6 +40,16 @@ def ca_step_dev(config: DispatchConfig, d_src: int, d_dst: int, rule: CaRule = C
     return WorkReport.from_c(rep)
 
 
+def ca_run_dev(config: DispatchConfig, d_a: int, d_b: int, steps: int, rule: CaRule = CaRule(),
+               stream: int = 0) -> "_abi.NbbPassStats":
+    """`steps` steps on an embedded device grid (result in d_a for even steps, else d_b); the gasket's
+    int64 grid runs temporally blocked through the compact state (nbb_gpu_ca_run_dev)."""
+    st = _abi.NbbPassStats()
+    _check(_lib().nbb_gpu_ca_run_dev(ctypes.byref(config.to_c()), _vp(d_a), _vp(d_b), steps, rule.birth,
+                                     rule.survive, _vp(stream), ctypes.byref(st)))
+    return st
+
+
 def sanitize_dev(config: DispatchConfig, d_grid: int, stream: int = 0) -> None:
     _check(_lib().nbb_gpu_sanitize_dev(ctypes.byref(config.to_c()), _vp(d_grid), _vp(stream)))
 

@@ -655,3 +655,28 @@ def test_host_buffer_compact_ca_pinned_zero_copy(steps):
                                     ctypes.c_void_p(hout.data_ptr()), None)
         assert rc == 0, _abi.load().nbb_gpu_last_error()
         assert np.array_equal(hout.numpy(), want), trial
+
+
+@pytest.mark.parametrize("r", [5, 8, 11])
+def test_ca_run_dev_embedded_temporal_blocking(r):
+    """nbb_gpu_ca_run_dev on embedded int64 device grids: the gasket's run goes through the compact
+    state in passes (temporal blocking of the embedded layout) — every step count equals the oracle,
+    the result lands where single steps leave it, non-member cells stay 0; pass_steps, a generic rule,
+    BB mode and one launch per step agree."""
+    torch = pytest.importorskip("torch")
+    from paper_2004_13475_b200 import device as dev
+    n = 1 << r
+    s = torch.cuda.current_stream().cuda_stream
+    init = orc_random_member_grid(r, 90 + r, 2)
+    for rule in RULES[:2]:
+        for steps in (1, 2, 7, 20):
+            want = orc_ca(r, init, steps, rule.birth, rule.survive)
+            for kw in ({}, {"pass_steps": 3}, {"mode": MapMode.BoundingBox}, {"flags": _abi.FLAG_SINGLE_STEP}):
+                a = torch.from_numpy(init.copy()).cuda()
+                b = torch.zeros_like(a)
+                st = dev.ca_run_dev(cfg(r=r, rho=32, **kw), a.data_ptr(), b.data_ptr(), steps, rule, s)
+                assert st.result_in_b == steps % 2
+                out = (b if steps % 2 else a).cpu().numpy()
+                assert np.array_equal(out, want), (rule, steps, kw)
+                if kw == {} and steps >= 2:
+                    assert st.passes < steps  # blocked: several steps per pass

@@ -74,27 +74,37 @@ cfg = nbb.DispatchConfig(r=r, rho=32)
 dev.ca_compact_run_dev(cfg, ca.data_ptr(), cb.data_ptr(), 3, nbb.CaRule(), s)
 assert np.array_equal(cb.cpu().numpy(), want[cy, cx])
 checks += 1
-# two steps per pass (ca_compact2_kernel, B3/S23 and generic-rule instantiations): 4 steps = 2 pairs
+# passes of 1..8 steps (ca_compact_sliced_kernel: TMA loader, named-barrier hand-off, halo
+# gather), both rule instantiations, the λ and BB walks
 for rule in (nbb.CaRule(), nbb.CaRule(birth=(1 << 3) | (1 << 6), survive=(1 << 2) | (1 << 3))):
-    ca, cb = comp0.clone(), torch.empty_like(comp0)
-    dev.ca_compact_run_dev(cfg, ca.data_ptr(), cb.data_ptr(), 4, rule, s)
-    assert np.array_equal(ca.cpu().numpy(), orc_ca(r, g, 4, rule.birth, rule.survive)[cy, cx])
-    checks += 1
+    for k in (1, 2, 5, 8):
+        for mode in (nbb.MapMode.Lambda, nbb.MapMode.BoundingBox):
+            ca, cb = comp0.clone(), torch.empty_like(comp0)
+            st = dev.ca_compact_passes_dev(nbb.DispatchConfig(r=r, rho=32, pass_steps=k, mode=mode), ca.data_ptr(),
+                                           cb.data_ptr(), 11, rule, s)
+            out = (cb if st.result_in_b else ca).cpu().numpy()
+            assert np.array_equal(out, orc_ca(r, g, 11, rule.birth, rule.survive)[cy, cx]), (k, mode)
+            checks += 1
+# the P2P passes (world 2, rank 0; every peer mapped to this process): 8-step passes
 plan = shard.ShardPlan(r=r, rho=32, world=2, rank=0, state="compact")
 ca, cb = comp0.clone(), torch.zeros_like(comp0)  # rank 0 writes only its tiles
 sync = torch.zeros(4, dtype=torch.int32, device="cuda")
 peers = [torch.tensor([t.data_ptr()] * 2, dtype=torch.int64, device="cuda") for t in (ca, cb)]
 flags = torch.tensor([sync.data_ptr()] * 2, dtype=torch.int64, device="cuda")
-owner = torch.from_numpy(plan.halo_owner_table()).cuda()
 args = _abi.NbbP2P(2, 0, (ctypes.c_void_p * 2)(ca.data_ptr(), cb.data_ptr()),
-                   (ctypes.c_void_p * 2)(peers[0].data_ptr(), peers[1].data_ptr()), owner.data_ptr(),
+                   (ctypes.c_void_p * 2)(peers[0].data_ptr(), peers[1].data_ptr()), None,
                    sync.data_ptr(), flags.data_ptr(), 20000)
 cc = plan.local_config(cfg).to_c()
-assert _abi.load().nbb_gpu_ca_compact_p2p_dev(ctypes.byref(cc), 0, 1, 8, 12, ctypes.byref(args),
-                                              ctypes.c_void_p(s)) == 0
+assert _abi.load().nbb_gpu_ca_compact_p2p_passes_dev(ctypes.byref(cc), 0, 8, 8, 12, ctypes.byref(args),
+                                                     ctypes.c_void_p(s)) == 0
 torch.cuda.synchronize()
 own = plan.owner(plan.tile_of_ordinal(shard.lambda_inverse_blocks(cx >> 5, cy >> 5, plan.r_b, plan.W))) == 0
-assert np.array_equal(cb.cpu().numpy()[own], orc_ca(r, g, 1)[cy, cx][own])
+assert np.array_equal(cb.cpu().numpy()[own], orc_ca(r, g, 8)[cy, cx][own])
 assert int(sync[0].item()) == 2 and int(sync[2].item()) == 0
 checks += 1
+# the worker split over devices (2 and 3 workers on this GPU)
+for devs in ([0, 0], [0, 0, 0]):
+    got = nbb.run_ca_multi(nbb.DispatchConfig(r=r, rho=32), devs, nbb.Grid(G, r, g), 9).grid.values
+    assert np.array_equal(got, orc_ca(r, g, 9)), devs
+    checks += 1
 print(f"sanitize_run ok: r={r}, {checks} checks")
