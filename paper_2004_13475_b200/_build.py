@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["nbb_capi.cu", "nbb_host.cpp"]
 HEADERS = ["common.cuh", "tile_kernels.cuh", "ca_pipe_kernel.cuh", "bits_kernels.cuh",
-           "compact_kernels.cuh", "compact_pass.cuh", "compact_sliced.cuh",
+           "compact_kernels.cuh", "compact_pass.cuh", "compact_sliced.cuh", "compact_cluster.cuh",
            "percell_kernels.cuh",
            "util_kernels.cuh", "nbb_host.hpp", "nbb_multi.inc", "nbb_comm.inc"]
 

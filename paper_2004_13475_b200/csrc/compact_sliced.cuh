@@ -71,6 +71,44 @@ __device__ __forceinline__ uint32_t sliced_cell_step(const uint32_t* c, uint32_t
                      c[0], CONWAY ? (1u << 3) : birth, CONWAY ? (1u << 2) | (1u << 3) : survive);
 }
 
+// K steps of a batch in its box: the tile's member positions (lane: members 32k + lane in
+// row-major order, box index table cb) and the halo slots of layer <= K - j at step j (slot
+// lane + 32m, box index table bidx, existence mask hmask); then the lane's tile words (cells
+// li = 32k + lane, box index table tb) into w.
+template <bool CONWAY>
+__device__ __forceinline__ void sliced_steps(uint32_t* box, const uint32_t* hmask, int K, const uint16_t* cb,
+                                             const uint16_t* bidx, const uint16_t* tb, uint32_t birth,
+                                             uint32_t survive, uint32_t (&w)[8]) {
+    const int lane = threadIdx.x & 31;
+    const bool k7 = lane < 19;  // member / cell 32 * 7 + lane < 243
+    __syncwarp();
+    for (int j = 1; j <= K; ++j) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < 7 || k7) w[k] = sliced_cell_step<CONWAY>(box + cb[32 * k + lane], birth, survive);
+        const int ns = c_sslots.upto[K - j];
+        uint32_t hn[kSliceMaxM];
+#pragma unroll
+        for (int m = 0; m < kSliceMaxM; ++m) {
+            const int s = lane + 32 * m;
+            hn[m] = 0u;
+            if (s < ns) hn[m] = sliced_cell_step<CONWAY>(box + bidx[s], birth, survive) & hmask[s];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < 7 || k7) box[cb[32 * k + lane]] = w[k];
+#pragma unroll
+        for (int m = 0; m < kSliceMaxM; ++m) {
+            const int s = lane + 32 * m;
+            if (s < ns) box[bidx[s]] = hn[m];
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = (k < 7 || k7) ? box[tb[32 * k + lane]] : 0u;
+}
+
 // Named barriers of the loader / stepper hand-off (64 threads: the pipeline's two warps). Stage b
 // (b = batch index & 1) is FULL once the loader stored the batch's tile words, EMPTY once the
 // stepper copied them into its box. Compile-time ids (ptxas then reserves 9 barriers per CTA; a
@@ -330,33 +368,8 @@ __global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB)
         }
     };
     auto step_batch = [&](uint32_t u, uint32_t cnt, uint32_t base0, uint32_t* box, const uint32_t* hmask) {
-        __syncwarp();
         uint32_t w[8];
-        for (int j = 1; j <= K; ++j) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (k < 7 || k7) w[k] = sliced_cell_step<CONWAY>(box + s_cb[32 * k + lane], birth, survive);
-            const int ns = c_sslots.upto[K - j];
-            uint32_t hn[kSliceMaxM];
-#pragma unroll
-            for (int m = 0; m < kSliceMaxM; ++m) {
-                const int s = lane + 32 * m;
-                hn[m] = 0u;
-                if (s < ns) hn[m] = sliced_cell_step<CONWAY>(box + s_bidx[s], birth, survive) & hmask[s];
-            }
-            __syncwarp();
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (k < 7 || k7) box[s_cb[32 * k + lane]] = w[k];
-#pragma unroll
-            for (int m = 0; m < kSliceMaxM; ++m) {
-                const int s = lane + 32 * m;
-                if (s < ns) box[s_bidx[s]] = hn[m];
-            }
-            __syncwarp();
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) w[k] = (k < 7 || k7) ? box[s_tb[32 * k + lane]] : 0u;
+        sliced_steps<CONWAY>(box, hmask, K, s_cb, s_bidx, s_tb, birth, survive, w);
         // cell li of tile t = bit t of w[k]
 #ifdef NBB_EXP_NOSTORE
         if (w[0] != 0x12345u) return;

@@ -30,6 +30,7 @@
 #include "compact_kernels.cuh"
 #include "compact_pass.cuh"
 #include "compact_sliced.cuh"
+#include "compact_cluster.cuh"
 #include "util_kernels.cuh"
 
 using namespace nbbgpu;
@@ -902,6 +903,44 @@ template <bool P2P, bool BB>
 void (*sliced_kernel(bool conway))(CompactCaArgs, SliceBatches, FastDiv, const int32_t*, P2PArgs) {
     return conway ? ca_compact_sliced_kernel<true, P2P, BB> : ca_compact_sliced_kernel<false, P2P, BB>;
 }
+// The cluster walk (compact_cluster.cuh): the single-device λ walk over the whole orthotope at
+// r_b >= 3, unless NBB_PASS_IMPL=sliced keeps the 32-ordinal batches (comparison runs).
+bool cluster_impl() {  // read per launch: comparison runs flip it inside one process
+    const char* e = std::getenv("NBB_PASS_IMPL");
+    return !(e && (std::strcmp(e, "sliced") == 0 || std::strcmp(e, "warp") == 0));
+}
+bool cluster_walk_ok(const CompactCaArgs& a) {
+    return cluster_impl() && a.rb >= 3 && a.tile_begin == 0 && a.tile_end == a.tiles && a.Wb % 9u == 0 &&
+           a.Hb % 3u == 0;
+}
+ClusterWalk cluster_walk(const CompactCaArgs& a, int k) {
+    ClusterWalk c{};
+    c.K = k;
+    c.ncy = a.Hb / 3u;
+    c.div_ncy.d = c.ncy;
+    nbbhost::fastdiv_magic(c.ncy, &c.div_ncy.m, &c.div_ncy.s);
+    c.total = (a.Wb / 9u) * c.ncy;
+    return c;
+}
+int cluster_grid(DeviceCtx* ctx, const void* kern, uint64_t batches, unsigned* grid) {
+    static std::mutex m;
+    static std::vector<std::pair<const void*, int>> cache;  // kernel -> resident CTAs per SM
+    std::lock_guard<std::mutex> lock(m);
+    int occ = 0;
+    for (auto& e : cache)
+        if (e.first == kern) occ = e.second;
+    if (!occ) {
+        NBB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        NBB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kClDynSmem));
+        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kClWarps, kClDynSmem));
+        if (occ < 1) occ = 1;
+        cache.push_back({kern, occ});
+    }
+    const uint64_t wave = (uint64_t)ctx->sms * occ;
+    *grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(wave, (batches + kClPipes - 1) / kClPipes));
+    return NBB_OK;
+}
+
 // grid of a tile-sliced launch: one wave of CTAs (kSlicePipes loader/stepper pipelines each),
 // fewer when the batches are fewer
 int sliced_grid(DeviceCtx* ctx, const void* kern, uint64_t batches, bool bb, unsigned* grid) {
@@ -958,6 +997,14 @@ int launch_pass(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* ds
     const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
     if (want == 0) return NBB_OK;
     const bool bb = cfg->mode == NBB_MODE_BB;
+    if (!bb && sliced_impl() && cluster_walk_ok(a)) {
+        const ClusterWalk cw = cluster_walk(a, k);
+        auto kern = is_conway(birth, survive) ? ca_compact_cluster_kernel<true> : ca_compact_cluster_kernel<false>;
+        unsigned grid;
+        NBB_CHECK(cluster_grid(ctx, (const void*)kern, cw.total, &grid));
+        NBB_CUDA(launch_pdl_smem(kern, grid, 32 * kClWarps, kClDynSmem, st, a, cw, div_hb, tab));
+        return NBB_OK;
+    }
     if (sliced_impl()) {
         const SliceBatches sb = slice_batches(a, k);
         auto kern = bb ? sliced_kernel<false, true>(is_conway(birth, survive))
