@@ -190,7 +190,9 @@ def config_block(r, rho, world=1, transport="p2p"):
     return {"workload": f"C3: gasket n=2^{r} cellular-automaton step (B3/S23), lambda(omega) launch, "
                         f"rho={rho} tiles; device state = the lambda-ordered compact layout "
                         f"(CompactGrid, 8 B per member), host I/O = the reference's int64 Grid; "
-                        + "up to 8 steps per pass over the state (ca_compact_sliced_kernel)",
+                        + "up to 8 steps per pass over the state (" + (
+                            "ca_compact_cluster_kernel: batches of 27 tiles = one level-3 sub-gasket"
+                            if world == 1 else "ca_compact_sliced_kernel<P2P>") + ")",
             "r": r, "n": 1 << r, "rho": rho, "mode": "lambda", "cells_per_step": 3 ** r,
             "cell": "int64", "state": "compact",
             "parallelism": "1 GPU" if world == 1 else
@@ -572,7 +574,8 @@ def main():
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
         with open(tf) as f:
-            traffic = json.load(f).get("ca_compact_sliced_kernel_k8")
+            traffic = json.load(f).get("ca_compact_cluster_kernel_k8" if world == 1 else
+                                       "ca_compact_sliced_kernel_k8")
 
     # ---- e2e through the public C ABI with pinned host buffers -------------------------
     e2e = None
@@ -651,7 +654,8 @@ def main():
                      "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
                      "launches": head_stats,
-                     "kernel": "ca_compact_sliced_kernel<B3/S23, lambda>: one launch = one pass of up to 8 "
+                     "kernel": ("ca_compact_cluster_kernel<B3/S23>" if world == 1 else
+                                "ca_compact_sliced_kernel<B3/S23, P2P>") + ": one launch = one pass of up to 8 "
                                "CA steps over the compact state, 8 B read + 8 B write per member per pass "
                                "(launches.by_steps[k] = passes of k steps); achieved = alg bytes / "
                                "average pass duration (CUDA events over the K timed steps)"},

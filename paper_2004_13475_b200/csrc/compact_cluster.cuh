@@ -28,6 +28,8 @@
 // and the multi-GPU pass keep the 32-ordinal batches of compact_sliced.cuh.
 #pragma once
 
+#include <type_traits>
+
 #include "compact_sliced.cuh"
 
 namespace nbbgpu {
@@ -45,8 +47,50 @@ struct ClusterWalk {
     int K;            // steps per pass, 1..8
 };
 
+// The in-cluster neighbour of tile t = 3 i + j in halo direction q (q = 0..5: directions
+// 0, 1, 3, 4, 6, 7 of compact_nbr_table_kernel, d9 = (dy + 1) * 3 + dx + 1 with the centre
+// skipped), or -1. Cluster-local tile coordinates: bit 0 from digit 0 of ωx (i % 3), bit 1 from
+// digit 0 of ωy (j), bit 2 from digit 1 of ωx (i / 3); digit v -> x bit (v == 2), y bit (v >= 1).
+// The same for every cluster: the halo word of a slot is a FIXED bit permutation of the tile
+// word its cell lies in (plus the few bits from other clusters).
+__host__ __device__ constexpr int cl_src(int q, int t) {
+    const int d = q < 2 ? q : q < 4 ? q + 1 : q + 2, d9 = d < 4 ? d : d + 1;
+    const int dx = d9 % 3 - 1, dy = d9 / 3 - 1;
+    const int i = t / 3, j = t % 3, d0 = i % 3, d1 = i / 3;
+    const int lx = (d0 == 2) | ((j == 2) << 1) | ((d1 == 2) << 2);
+    const int ly = (d0 >= 1) | ((j >= 1) << 1) | ((d1 >= 1) << 2);
+    const int nx = lx + dx, ny = ly + dy;
+    if (nx < 0 || ny < 0 || nx > 7 || ny > 7 || (nx & ~ny) != 0) return -1;
+    auto dig = [](int x, int y, int b) { return ((x >> b) & 1) ? 2 : ((y >> b) & 1); };
+    return (3 * dig(nx, ny, 2) + dig(nx, ny, 0)) * 3 + dig(nx, ny, 1);
+}
+// source bits s whose target bit is s + delta, for direction q
+__host__ __device__ constexpr uint32_t cl_mask(int q, int delta) {
+    uint32_t m = 0;
+    for (int t = 0; t < 27; ++t) {
+        const int s = cl_src(q, t);
+        if (s >= 0 && t - s == delta) m |= 1u << s;
+    }
+    return m;
+}
+// the permutation: bit t of the result = bit cl_src(q, t) of x (0 where there is none), as one
+// masked shift per distinct distance
+template <int Q, int D = -26>
+__device__ __forceinline__ uint32_t cl_perm(uint32_t x) {
+    constexpr uint32_t m = cl_mask(Q, D);
+    uint32_t r = 0u;
+    if constexpr (m != 0u) r = D >= 0 ? (x & m) << (D >= 0 ? D : 0) : (x & m) >> (D < 0 ? -D : 0);
+    if constexpr (D < 26) return r | cl_perm<Q, D + 1>(x);
+    else return r;
+}
+
+#ifndef NBB_CL_LSTORE  // the loader warp stores the stepper's results (1) or the stepper does (0)
+#define NBB_CL_LSTORE 1
+#endif
+constexpr bool kClLoaderStores = NBB_CL_LSTORE != 0;
+
 #ifndef NBB_CLUSTER_MINB  // resident CTAs per SM the register budget is cut for (tuning builds)
-#define NBB_CLUSTER_MINB 4
+#define NBB_CLUSTER_MINB 3
 #endif
 
 template <bool CONWAY>
@@ -57,14 +101,19 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
     __shared__ uint32_t s_stage[kClPipes][2][kStageWords];
     __shared__ uint32_t s_hmask[kClPipes][kSliceSlots];
     __shared__ uint32_t s_dofs[8][kSliceDirMax];           // per direction, slot j: offset in the neighbour tile (B)
-    __shared__ uint32_t s_dslot[8][kSliceDirMax];          // ... slot | box index of its cell in the neighbour << 16
     __shared__ uint16_t s_bidx[kSliceSlots];
     __shared__ uint16_t s_tb[256];
     __shared__ uint16_t s_cb[256];
-    __shared__ uint32_t s_extw[kClPipes][6][32];             // HBM halo bits: [direction q][slot j], bit t
+    __shared__ uint32_t s_hflat[kSliceSlots];                // halo slots of this K, direction-major:
+                                                             // box index of the cell in the neighbour
+                                                             // | slot << 12 | 5 q << 20
+    __shared__ int s_qstart[7];                              // first flat entry of direction q
+    __shared__ uint32_t s_extw[kClPipes][kSliceSlots];       // HBM halo bits of flat entry m, bit t
     __shared__ uint32_t s_exist[kClPipes][6];                // neighbouring tile present: bit t
     __shared__ unsigned long long s_ext[kClPipes][kClExtMax];  // HBM (tile, direction) pairs: ptr | q << 56 | t << 59
     __shared__ __align__(8) uint64_t s_mbar[kClPipes][2];
+    __shared__ uint32_t s_out[kClPipes][kStageWords];         // stepper -> loader: a batch's result words
+    __shared__ __align__(8) uint64_t s_obar[kClPipes][2];     // [0] out full, [1] out empty (32 arrivals)
     extern __shared__ __align__(16) unsigned char s_dyn[];
     auto s_tma = reinterpret_cast<unsigned char (*)[2][9][kClRunBytes]>(s_dyn);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -80,7 +129,10 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         s_tb[i] = (uint16_t)(((pos >> 5) + kSliceMaxK) * kBoxW + (pos & 31u) + kSliceMaxK);
     }
     for (int i = threadIdx.x; i < kClPipes * kBoxWords; i += blockDim.x) (&s_box[0][0])[i] = 0u;
-    if (threadIdx.x < 2 * kClPipes) mbar_init(&s_mbar[threadIdx.x >> 1][threadIdx.x & 1], 1u);
+    if (threadIdx.x < 2 * kClPipes) {
+        mbar_init(&s_mbar[threadIdx.x >> 1][threadIdx.x & 1], 1u);
+        mbar_init(&s_obar[threadIdx.x >> 1][threadIdx.x & 1], 32u);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     {
         uint32_t y = 0, seen = 0;
@@ -89,17 +141,27 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
             s_cb[c] = (uint16_t)((y + kSliceMaxK) * kBoxW + pdep32(c - seen, y) + kSliceMaxK);
         }
     }
-    __syncthreads();  // s_tb before s_dslot
+    __syncthreads();  // s_tb before s_hflat
     for (int i = threadIdx.x; i < 8 * kSliceDirMax; i += blockDim.x) {
         const int d = i / kSliceDirMax, j = i % kSliceDirMax;
-        uint32_t o = 0u, sl = 0u;
+        uint32_t o = 0u;
         if (j < c_sslots.dir_upto[d][kSliceMaxK]) {
-            const uint32_t s = c_sslots.by_dir[d][j], li = c_sslots.li[s];
+            const uint32_t li = c_sslots.li[c_sslots.by_dir[d][j]];
             o = 8u * ((li / 27u) * a.W + li % 27u);
-            sl = s | ((uint32_t)s_tb[li] << 16);
         }
         s_dofs[d][j] = o;
-        s_dslot[d][j] = sl;
+    }
+    if (threadIdx.x == 0) {
+        int m = 0;
+        for (int q = 0; q < 6; ++q) {
+            const int d = q < 2 ? q : q < 4 ? q + 1 : q + 2;
+            s_qstart[q] = m;
+            for (int j = 0; j < c_sslots.dir_upto[d][K]; ++j, ++m) {
+                const uint32_t sl = c_sslots.by_dir[d][j];
+                s_hflat[m] = (uint32_t)s_tb[c_sslots.li[sl]] | (sl << 12) | ((5u * q) << 20);
+            }
+        }
+        s_qstart[6] = m;
     }
     pdl_wait();
     __syncthreads();
@@ -116,64 +178,131 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
 
     if (loader) {
         // ---- loader: group g of a cluster = tiles (g, 0..2) = nine runs of 81 values ------------
+        // A run starts one value early when its first value sits at an odd element (16-byte
+        // aligned bulk copies): 82 values = 656 B, except at the end of the array (the last
+        // cluster: byte counts clamped, its values past the copy read directly).
         unsigned char (*tma)[9][kClRunBytes] = s_tma[pipe];
         uint64_t* mbar = s_mbar[pipe];
-        auto issue = [&](uint32_t base0, uint32_t g, int sbuf) {
+        const uint64_t row_bytes = 8ull * a.W;
+        auto issue = [&](uint32_t base0, uint32_t g, int sbuf, bool last) {
             if (lane == 0) {
-                uint32_t bytes[9], total = 0;
+                const char* p0 = reinterpret_cast<const char*>(a.src) + 8ull * ((uint64_t)base0 + 9ull * g * a.W);
+                if (!last) {
+                    mbar_expect_tx(&mbar[sbuf], 9u * kClRunBytes);
 #pragma unroll
-                for (int r = 0; r < 9; ++r) {
-                    const uint64_t e0 = (uint64_t)base0 + (uint64_t)(9u * g + r) * a.W, sh = e0 & 1u;
-                    const uint64_t nb = (8u * (81u + sh) + 15u) & ~15ull;
-                    const uint64_t room = (8u * (total_elems - (e0 - sh))) & ~15ull;  // never past the array
-                    bytes[r] = (uint32_t)(nb < room ? nb : room);
-                    total += bytes[r];
-                }
-                mbar_expect_tx(&mbar[sbuf], total);
+                    for (int r = 0; r < 9; ++r)
+                        bulk_g2s(tma[sbuf][r], reinterpret_cast<const void*>(
+                                     reinterpret_cast<uintptr_t>(p0 + r * row_bytes) & ~(uintptr_t)15),
+                                 kClRunBytes, &mbar[sbuf]);
+                } else {
+                    uint32_t bytes[9], total = 0;
 #pragma unroll
-                for (int r = 0; r < 9; ++r) {
-                    const uint64_t e0 = (uint64_t)base0 + (uint64_t)(9u * g + r) * a.W, sh = e0 & 1u;
-                    bulk_g2s(tma[sbuf][r], a.src + (e0 - sh), bytes[r], &mbar[sbuf]);
+                    for (int r = 0; r < 9; ++r) {
+                        const uint64_t e0 = (uint64_t)base0 + (uint64_t)(9u * g + r) * a.W, sh = e0 & 1u;
+                        const uint64_t room = (8u * (total_elems - (e0 - sh))) & ~15ull;  // never past the array
+                        bytes[r] = (uint32_t)(kClRunBytes < room ? kClRunBytes : room);
+                        total += bytes[r];
+                    }
+                    mbar_expect_tx(&mbar[sbuf], total);
+#pragma unroll
+                    for (int r = 0; r < 9; ++r) {
+                        const uint64_t e0 = (uint64_t)base0 + (uint64_t)(9u * g + r) * a.W, sh = e0 & 1u;
+                        bulk_g2s(tma[sbuf][r], a.src + (e0 - sh), bytes[r], &mbar[sbuf]);
+                    }
                 }
             }
         };
+        // the lane's cells li = 32 k + lane: compact row and column inside a tile
+        uint32_t rowk[8], colk[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t li = min(32u * k + lane, 242u);
+            rowk[k] = li / 27u;
+            colk[k] = li % 27u;
+        }
+        // the stepper's results: batch bo's words ow (taken from s_out as soon as they are there),
+        // stored group by group while the loader folds a later batch
+        uint32_t ow[8];
+        uint32_t nout = 0;  // results taken so far
+        auto take_out = [&]() {
+            mbar_wait(&s_obar[pipe][0], nout & 1u);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) ow[k] = (k < 7 || k7) ? s_out[pipe][32 * k + lane] : 0u;
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_obar[pipe][1])) : "memory");
+            ++nout;
+        };
+        auto store_group = [&](uint32_t obase, uint32_t g) {  // tiles (g, 0..2) of the taken batch
+            char* Q0 = reinterpret_cast<char*>(a.dst) + 8ull * ((uint64_t)obase + 9ull * g * a.W);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (k < 7 || k7)
+                        *reinterpret_cast<long long*>(Q0 + 216u * j + 8ull * (rowk[k] * a.W + colk[k])) =
+                            (long long)((ow[k] >> (3u * g + j)) & 1u);
+            }
+        };
         uint32_t gc = 0;  // groups consumed (staging buffer gc & 1, use count gc >> 1)
-        if (pipe_global < cw.total) issue(cluster_base(pipe_global), 0u, 0);
+        if (pipe_global < cw.total) issue(cluster_base(pipe_global), 0u, 0, pipe_global + 1 == cw.total);
         uint32_t i = 0;
         for (uint32_t bt = pipe_global; bt < cw.total; bt += npipes, ++i) {
             const int b = (int)(i & 1u);
             if (i >= 2) nb_op<true>(nb_empty(pipe, b));
             const uint32_t base0 = cluster_base(bt);
+            const bool last = bt + 1 == cw.total;
             const uint32_t nbase = bt + npipes < cw.total ? cluster_base(bt + npipes) : 0u;
+            const bool st = kClLoaderStores && i >= 2;  // stores the result of batch i - 2 meanwhile
+            const uint32_t obase = st ? cluster_base(bt - 2u * npipes) : 0u;
             uint32_t w[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) w[k] = 0u;
 #pragma unroll 1
             for (uint32_t g = 0; g < 9u; ++g, ++gc) {
-                if (g + 1 < 9u) issue(base0, g + 1, (int)((gc + 1) & 1u));
-                else if (bt + npipes < cw.total) issue(nbase, 0u, (int)((gc + 1) & 1u));
+                if (g + 1 < 9u) issue(base0, g + 1, (int)((gc + 1) & 1u), last);
+                else if (bt + npipes < cw.total) issue(nbase, 0u, (int)((gc + 1) & 1u), bt + npipes + 1 == cw.total);
                 const int sb_ = (int)(gc & 1u);
                 mbar_wait(&mbar[sb_], (gc >> 1) & 1u);
+                // parity of a run's first element: base0 + (9 g + row) W with W odd
+                const uint32_t par = (base0 ^ g) & 1u;
+                if (!last) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    if (k == 7 && !k7) continue;
-                    const uint32_t li = 32u * k + lane, row = li / 27u, col = li % 27u;
-                    const uint64_t e0 = (uint64_t)base0 + (uint64_t)(9u * g + row) * a.W;
-                    const uint32_t sh = (uint32_t)(e0 & 1u);
-                    const uint64_t want = (uint64_t)(((8u * (81u + sh) + 15u) & ~15u) / 8u);
-                    const uint64_t room = (total_elems - (e0 - sh)) & ~1ull;
-                    const uint32_t copied = (uint32_t)(want < room ? want : room);
-                    const long long* rowp = reinterpret_cast<const long long*>(tma[sb_][row]);
+                    for (int k = 0; k < 8; ++k) {
+                        if (k == 7 && !k7) continue;
+                        const long long* rowp = reinterpret_cast<const long long*>(tma[sb_][rowk[k]]) +
+                                                ((par ^ rowk[k]) & 1u) + colk[k];
 #pragma unroll
-                    for (int t = 0; t < 3; ++t) {
-                        const uint32_t idx = sh + 27u * t + col;
-                        const long long v = idx < copied ? rowp[idx] : __ldg(a.src + e0 + 27u * t + col);
-                        const uint32_t nz = (uint32_t)v | (uint32_t)((unsigned long long)v >> 32);
-                        w[k] |= min(nz, 1u) << (3u * g + t);
+                        for (int t = 0; t < 3; ++t) {
+                            const long long v = rowp[27 * t];
+                            const uint32_t nz = (uint32_t)v | (uint32_t)((unsigned long long)v >> 32);
+                            w[k] |= min(nz, 1u) << (3u * g + t);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        if (k == 7 && !k7) continue;
+                        const uint32_t row = rowk[k], col = colk[k];
+                        const uint64_t e0 = (uint64_t)base0 + (uint64_t)(9u * g + row) * a.W;
+                        const uint32_t sh = (uint32_t)(e0 & 1u);
+                        const uint64_t want = kClRunBytes / 8u;
+                        const uint64_t room = (total_elems - (e0 - sh)) & ~1ull;
+                        const uint32_t copied = (uint32_t)(want < room ? want : room);
+                        const long long* rowp = reinterpret_cast<const long long*>(tma[sb_][row]);
+#pragma unroll
+                        for (int t = 0; t < 3; ++t) {
+                            const uint32_t idx = sh + 27u * t + col;
+                            const long long v = idx < copied ? rowp[idx] : __ldg(a.src + e0 + 27u * t + col);
+                            const uint32_t nz = (uint32_t)v | (uint32_t)((unsigned long long)v >> 32);
+                            w[k] |= min(nz, 1u) << (3u * g + t);
+                        }
                     }
                 }
                 __syncwarp();
                 fence_proxy_async();  // the reads of this buffer before the next bulk copy into it
+                if (st) {
+                    if (g == 0) take_out();
+                    store_group(obase, g);
+                }
             }
             uint32_t* stage = s_stage[pipe][b];
 #pragma unroll
@@ -181,6 +310,15 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
                 if (k < 7 || k7) stage[32 * k + lane] = w[k];
             __syncwarp();
             nb_op<false>(nb_full(pipe, b));
+        }
+        if (kClLoaderStores) {  // the last two results
+            const uint32_t nb = i;  // batches of this pipeline
+            for (uint32_t o = nb >= 2 ? nb - 2 : 0; o < nb; ++o) {
+                const uint32_t obase = cluster_base(pipe_global + o * npipes);
+                take_out();
+#pragma unroll 1
+                for (uint32_t g = 0; g < 9u; ++g) store_group(obase, g);
+            }
         }
         return;
     }
@@ -195,7 +333,7 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         const bool more2 = bt + 2u * npipes < cw.total;
         const uint32_t cx = fastdiv(bt, cw.div_ncy), cy = bt - cx * cw.ncy;
         const uint32_t wx0 = 9u * cx, wy0 = 3u * cy;
-        // the neighbouring tiles of tile t: in the cluster (π_q = its bit) or in HBM (ext pair)
+        // the neighbouring tiles of tile t: in the cluster (cl_src) or in HBM (an ext pair)
         int4 n0 = make_int4(-1, -1, -1, -1), n1 = n0;
         if (tv) {
             const uint32_t u = (wx0 + ti) * a.Hb + wy0 + tj;
@@ -203,26 +341,25 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
             n1 = __ldg(reinterpret_cast<const int4*>(nbr_tab + 8ull * u) + 1);
         }
         const int32_t nbr6[6] = {n0.x, n0.y, n0.w, n1.x, n1.z, n1.w};  // directions 0,1,3,4,6,7
-        uint32_t pi_pack = 0u;
         uint32_t next = 0;  // ext pairs listed
+        for (int m = lane; m < kSliceSlots; m += 32) s_extw[pipe][m] = 0u;
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
-            s_extw[pipe][q][lane] = 0u;
             const int32_t nq = nbr6[q];
-            uint32_t pi = 31u;  // bit 31 of a tile word is 0: no in-cluster neighbour
             bool ext = false;
             unsigned long long ptr = 0ull;
             if (nq >= 0) {
                 const uint32_t wxn = fastdiv((uint32_t)nq, div_hb), wyn = (uint32_t)nq - wxn * a.Hb;
                 const uint32_t di = wxn - wx0, dj = wyn - wy0;
                 if (di < 9u && dj < 3u) {
-                    pi = 3u * di + dj;
+#ifdef NBB_CL_CHECK  // the compile-time permutation agrees with the neighbour table
+                    if ((int)(3u * di + dj) != cl_src(q, lane)) __trap();
+#endif
                 } else {
                     ext = true;
                     ptr = reinterpret_cast<unsigned long long>(a.src) + 8ull * (9ull * wxn * a.W + 27ull * wyn);
                 }
             }
-            pi_pack |= pi << (5 * q);
             const uint32_t ex = __ballot_sync(0xFFFFFFFFu, nq >= 0);
             if (lane == 0) s_exist[pipe][q] = ex;
             const uint32_t em = __ballot_sync(0xFFFFFFFFu, ext);
@@ -246,7 +383,7 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
                     if (lane < c_sslots.dir_upto[d][K]) {
                         const unsigned long long ptr = e & ((1ull << 56) - 1ull);
                         v[p] = __ldg(reinterpret_cast<const long long*>(ptr + s_dofs[d][lane]));
-                        meta[p] = q | (t << 8);
+                        meta[p] = (uint32_t)(s_qstart[q] + lane) | (t << 8);
                     }
                 }
             }
@@ -254,7 +391,7 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
             for (int p = 0; p < 8; ++p)
                 if (meta[p] != 0xFFFFFFFFu) {
                     const uint32_t nz = (uint32_t)v[p] | (uint32_t)((unsigned long long)v[p] >> 32);
-                    s_extw[pipe][meta[p] & 7u][lane] |= min(nz, 1u) << (meta[p] >> 8);
+                    s_extw[pipe][meta[p] & 0xFFu] |= min(nz, 1u) << (meta[p] >> 8);
                 }
         }
         // the batch's tile words into the box
@@ -267,29 +404,34 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         }
         __syncwarp();
         if (more2) nb_op<false>(nb_empty(pipe, b));
-        // halo words: slot j of direction q, bit t = bit π_q(t) of the neighbour cell's tile word
-        // (one broadcast load + one ballot) | its HBM bit
-#pragma unroll 1
-        for (int q = 0; q < 6; ++q) {
-            const int d = q < 2 ? q : q < 4 ? q + 1 : q + 2;
-            const int ns = c_sslots.dir_upto[d][K];
-            if (ns == 0) continue;
-            const uint32_t pi = (pi_pack >> (5 * q)) & 31u;
-            uint32_t mine = 0u;
-            for (int j = 0; j < ns; ++j) {
-                const uint32_t word = box[s_dslot[d][j] >> 16];
-                const uint32_t hw = __ballot_sync(0xFFFFFFFFu, (word >> pi) & 1u);
-                if (lane == j) mine = hw;
-            }
-            if (lane < ns) {
-                const uint32_t slot = s_dslot[d][lane] & 0xFFFFu, ex = s_exist[pipe][q];
-                box[s_bidx[slot]] = (mine | s_extw[pipe][q][lane]) & ex;
+        // halo words: slot j (lane) of direction q = the fixed bit permutation π_q of the word of
+        // its cell's tile position (cl_perm) | its HBM bits
+        auto halo_dir = [&](auto qc) {
+            constexpr int q = decltype(qc)::value;
+            const int m = s_qstart[q] + lane;
+            if (m < s_qstart[q + 1]) {
+                const uint32_t e = s_hflat[m], slot = (e >> 12) & 0xFFu, ex = s_exist[pipe][q];
+                box[s_bidx[slot]] = (cl_perm<q>(box[e & 0xFFFu]) | s_extw[pipe][m]) & ex;
                 hmask[slot] = ex;
             }
-        }
+        };
+        halo_dir(std::integral_constant<int, 0>{});
+        halo_dir(std::integral_constant<int, 1>{});
+        halo_dir(std::integral_constant<int, 2>{});
+        halo_dir(std::integral_constant<int, 3>{});
+        halo_dir(std::integral_constant<int, 4>{});
+        halo_dir(std::integral_constant<int, 5>{});
         // K steps, then the 27 tiles' values out
         uint32_t w[8];
         sliced_steps<CONWAY>(box, hmask, K, s_cb, s_bidx, s_tb, birth, survive, w);
+        if (kClLoaderStores) {  // to the loader: wait until it took the previous result
+            if (i >= 1) mbar_wait(&s_obar[pipe][1], (i - 1u) & 1u);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k < 7 || k7) s_out[pipe][32 * k + lane] = w[k];
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_obar[pipe][0])) : "memory");
+            continue;
+        }
         uint32_t off[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {

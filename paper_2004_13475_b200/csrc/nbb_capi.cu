@@ -816,20 +816,6 @@ void (*pass_kernel_k(int k, bool conway))(CompactCaArgs, FastDiv, const int32_t*
     }
 }
 // resident CTAs per SM of a pass kernel (cached per kernel pointer)
-int pass_occupancy_threads(const void* k, int threads, int* occ) {
-    static std::mutex m;
-    static std::vector<std::pair<const void*, int>> cache;
-    std::lock_guard<std::mutex> lock(m);
-    for (auto& e : cache)
-        if (e.first == k) {
-            *occ = e.second;
-            return NBB_OK;
-        }
-    NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, threads, 0));
-    if (*occ < 1) *occ = 1;
-    cache.push_back({k, *occ});
-    return NBB_OK;
-}
 int pass_occupancy(const void* k, int* occ) {
     static std::mutex m;
     static std::vector<std::pair<const void*, int>> cache;
