@@ -197,7 +197,8 @@ int nbb_gpu_ca(const nbb_config* cfg, const int64_t* initial, int32_t initial_le
                int32_t steps, uint16_t birth, uint16_t survive, int64_t* out_grid,
                nbb_report* per_step);
 /* run_ca / run_reduction with the reference's `workers` mapped to DEVICES of this process
- * (dispatch.cpp:416-432: contiguous ordinal chunks of ceil(total / workers), result independent
+ * (dispatch.cpp:416-432: contiguous ordinal chunks — ceil(total / workers), rounded up to whole
+ * cluster columns as for nbb_gpu_ca_compact_p2p_passes_dev — result independent
  * of the count — byte-identical for any ndev). The compact tiles are split into ndev contiguous
  * chunks; worker w advances chunk w on devices[w] in passes of up to pass_steps steps and reads
  * the halo cells other workers own from their buffers over NVLink (peer access) inside the pass
@@ -325,7 +326,7 @@ typedef struct nbb_p2p {
     void* d_buf[2];              /* this rank's two compact buffers (3^r int64 each)            */
     const void* d_peer_buf[2];   /* [world] const int64_t*: every rank's buffer 0 / buffer 1   */
     const void* reserved;        /* unused (ABI 2: a halo owner table; the owner of a halo cell
-                                  * is now its tile ordinal / ceil(tiles / world))            */
+                                  * is now its tile ordinal / the shard chunk below)          */
     void* d_sync;                /* this rank's uint32[4] {arrivals, done, error, 0}, zeroed    */
     const void* d_peer_flag;     /* [world] uint32*: every rank's d_sync (arrival counter)      */
     uint32_t timeout_ms;         /* bound on each wait; 0 = 20000                               */
@@ -333,13 +334,16 @@ typedef struct nbb_p2p {
 int nbb_gpu_ca_compact_p2p_dev(const nbb_config* cfg, int64_t first_step, int32_t steps,
                                uint16_t birth, uint16_t survive, const nbb_p2p* p2p, void* stream);
 /* The same step sequence in PASSES of up to cfg->pass_steps steps (default 8; the
- * ca_compact_sliced_kernel over peer memory: the radius-K halo read once, the intermediate
+ * ca_compact_cluster_kernel — ca_compact_sliced_kernel for r < 8 — over peer memory: the
+ * radius-K halo read once, the intermediate
  * steps kept on chip): ceil(steps / K) passes, steps spread evenly. Pass j (first_pass <= j)
  * reads d_buf[j & 1], writes d_buf[(j + 1) & 1] and waits for world x j arrivals; first_pass
  * must equal the number of passes (either entry point: a step of nbb_gpu_ca_compact_p2p_dev
  * is one pass) this d_sync has already run. The shard must be the rank's contiguous chunk:
- * shard_begin = rank * ceil(tiles / world), shard_count = ceil(tiles / world) (clipped) —
- * the owner of every halo cell is derived from it (NBB_ERR_INVALID_ARGUMENT otherwise).
+ * shard_begin = rank * chunk, shard_count = chunk (clipped), chunk = ceil(tiles / world)
+ * rounded up to a multiple of 9 * Hb tiles (whole level-3 cluster columns, Hb = 3^floor((r-5)/2))
+ * when r >= 8, plain ceil(tiles / world) below — the owner of every halo cell is derived from it
+ * (NBB_ERR_INVALID_ARGUMENT otherwise). Results are identical for any split.
  * nbb_gpu_pass_plan(cfg, steps, 0, &stats) names the passes. */
 int nbb_gpu_ca_compact_p2p_passes_dev(const nbb_config* cfg, int64_t first_pass, int32_t steps,
                                       uint16_t birth, uint16_t survive, const nbb_p2p* p2p, void* stream);
@@ -358,7 +362,8 @@ int nbb_gpu_ipc_close(int32_t device, void* d_ptr);
  * reduction. A communicator spans `world` processes (ncclCommInitRank; the 128-byte id comes from
  * nbb_gpu_comm_unique_id on one rank and reaches the others through the caller's launcher).
  * Rank i owns the contiguous compact tile chunk [i * chunk, min((i + 1) * chunk, tiles)),
- * chunk = ceil(tiles / world) (dispatch.cpp:419-427; cfg->shard_* are set from it). Before every
+ * chunk as for nbb_gpu_ca_compact_p2p_passes_dev (dispatch.cpp:419-427 rounded up to whole cluster
+ * columns; cfg->shard_* are set from it). Before every
  * pass of up to pass_steps (<= 8) steps the halo cells the rank's tiles read from other ranks
  * within 8 steps are gathered, exchanged with ncclSend / ncclRecv in one group on `stream` and
  * scattered into the pass's source buffer; d_a / d_b are replica-sized (3^r int64) buffers in

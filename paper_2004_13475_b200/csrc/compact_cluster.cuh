@@ -37,14 +37,15 @@ namespace nbbgpu {
 constexpr int kClPipes = 2;                                         // loader/stepper pipelines per CTA
 constexpr int kClWarps = 2 * kClPipes;
 constexpr int kClRunBytes = ((8 * (81 + 1)) + 15) / 16 * 16;        // 656: one 81-value run (+1 for alignment)
-constexpr size_t kClDynSmem = (size_t)kClPipes * 2 * 9 * kClRunBytes;  // staging [pipe][2][9 runs]
-constexpr int kClExtMax = 27 * 6;                                   // (tile, direction) pairs, any cluster
+constexpr size_t kClTmaBytes = (size_t)kClPipes * 2 * 9 * kClRunBytes;  // staging [pipe][2][9 runs]
+constexpr int kClExtMax = 32;  // HBM (tile, direction) pairs per cluster (<= 6 at every level measured)
 
 struct ClusterWalk {
-    uint32_t ncy;     // clusters per orthotope column: Hb / 3
+    uint32_t ncy;         // clusters per orthotope column: Hb / 3
     FastDiv div_ncy;
-    uint32_t total;   // clusters: (Wb / 9) (Hb / 3)
-    int K;            // steps per pass, 1..8
+    uint32_t total;       // clusters: (Wb / 9) (Hb / 3)
+    uint32_t begin, end;  // this launch's clusters (a shard: whole cluster columns)
+    int K;                // steps per pass, 1..8
 };
 
 // The in-cluster neighbour of tile t = 3 i + j in halo direction q (q = 0..5: directions
@@ -89,15 +90,111 @@ __device__ __forceinline__ uint32_t cl_perm(uint32_t x) {
 #endif
 constexpr bool kClLoaderStores = NBB_CL_LSTORE != 0;
 
+// K steps of a batch in its box (sliced_steps with the lane's box indices and halo masks held in
+// registers across the steps: shared memory is written between the steps, so the compiler
+// would reload them every step)
+template <bool CONWAY>
+__device__ __forceinline__ void cluster_steps(uint32_t* box, const uint32_t* hmask, int K, const uint16_t* cb,
+                                              const uint16_t* bidx, const uint16_t* tb, uint32_t birth,
+                                              uint32_t survive, uint32_t (&w)[8]) {
+    const int lane = threadIdx.x & 31;
+    const bool k7 = lane < 19;
+    __syncwarp();
+    uint32_t ci[8], hi[kSliceMaxM], hm[kSliceMaxM];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ci[k] = (k < 7 || k7) ? cb[32 * k + lane] : 0u;
+    const int n0 = c_sslots.upto[K - 1];
+#pragma unroll
+    for (int m = 0; m < kSliceMaxM; ++m) {
+        const int s = lane + 32 * m;
+        hi[m] = s < n0 ? bidx[s] : 0u;
+        hm[m] = s < n0 ? hmask[s] : 0u;
+    }
+    for (int j = 1; j <= K; ++j) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < 7 || k7) w[k] = sliced_cell_step<CONWAY>(box + ci[k], birth, survive);
+        const int ns = c_sslots.upto[K - j];
+        uint32_t hn[kSliceMaxM];
+#pragma unroll
+        for (int m = 0; m < kSliceMaxM; ++m) {
+            hn[m] = 0u;
+            if (lane + 32 * m < ns) hn[m] = sliced_cell_step<CONWAY>(box + hi[m], birth, survive) & hm[m];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < 7 || k7) box[ci[k]] = w[k];
+#pragma unroll
+        for (int m = 0; m < kSliceMaxM; ++m)
+            if (lane + 32 * m < ns) box[hi[m]] = hn[m];
+        __syncwarp();
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = (k < 7 || k7) ? box[tb[32 * k + lane]] : 0u;
+}
+
+// The same with two boxes: step j reads box[(j - 1) & 1] and writes box[j & 1], so each step
+// needs one warp barrier and no result is held across it. A halo slot not advanced at step j
+// (layer > K - j) keeps a stale value in the written box, read only by cells that are not needed
+// either; the non-member frame is zero in both boxes.
+template <bool CONWAY>
+__device__ __forceinline__ void cluster_steps2(uint32_t* box0, uint32_t* box1, const uint32_t* hmask, int K,
+                                               const uint16_t* cb, const uint16_t* bidx, const uint16_t* tb,
+                                               uint32_t birth, uint32_t survive, uint32_t (&w)[8]) {
+    const int lane = threadIdx.x & 31;
+    const bool k7 = lane < 19;
+    __syncwarp();
+    uint32_t ci[8], hi[kSliceMaxM], hm[kSliceMaxM];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ci[k] = (k < 7 || k7) ? cb[32 * k + lane] : 0u;
+    const int n0 = c_sslots.upto[K - 1];
+#pragma unroll
+    for (int m = 0; m < kSliceMaxM; ++m) {
+        const int s = lane + 32 * m;
+        hi[m] = s < n0 ? bidx[s] : 0u;
+        hm[m] = s < n0 ? hmask[s] : 0u;
+    }
+    for (int j = 1; j <= K; ++j) {
+        const uint32_t* src = (j & 1) ? box0 : box1;
+        uint32_t* dst = (j & 1) ? box1 : box0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < 7 || k7) dst[ci[k]] = sliced_cell_step<CONWAY>(src + ci[k], birth, survive);
+        const int ns = c_sslots.upto[K - j];
+#pragma unroll
+        for (int m = 0; m < kSliceMaxM; ++m)
+            if (lane + 32 * m < ns) dst[hi[m]] = sliced_cell_step<CONWAY>(src + hi[m], birth, survive) & hm[m];
+        __syncwarp();
+    }
+    const uint32_t* fin = (K & 1) ? box1 : box0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k] = (k < 7 || k7) ? fin[tb[32 * k + lane]] : 0u;
+}
+
+#ifndef NBB_CL_DBOX  // two boxes per pipeline (cluster_steps2)
+#define NBB_CL_DBOX 1
+#endif
+constexpr int kClBoxes = NBB_CL_DBOX ? 2 : 1;
+// dynamic shared memory: the loaders' staging, then the steppers' boxes [pipe][box][word]
+constexpr size_t kClDynSmem = kClTmaBytes + (size_t)kClPipes * kClBoxes * kBoxWords * 4;
+
+#ifndef NBB_CL_HOIST  // cluster_steps (1) or sliced_steps (0; tuning builds)
+#define NBB_CL_HOIST 1
+#endif
+
 #ifndef NBB_CLUSTER_MINB  // resident CTAs per SM the register budget is cut for (tuning builds)
 #define NBB_CLUSTER_MINB 3
 #endif
 
-template <bool CONWAY>
+// P2P: one rank's pass of the multi-GPU CA (its shard is whole cluster columns, so every tile of a
+// cluster is its own; the halo cells of neighbouring clusters owned by other ranks are read from
+// their buffers over NVLink; the flag barrier of compact_kernels.cuh orders the passes).
+template <bool CONWAY, bool P2P>
 __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
-    ca_compact_cluster_kernel(CompactCaArgs a, ClusterWalk cw, FastDiv div_hb, const int32_t* __restrict__ nbr_tab) {
+    ca_compact_cluster_kernel(CompactCaArgs a, ClusterWalk cw, FastDiv div_hb, const int32_t* __restrict__ nbr_tab,
+                              P2PArgs p) {
     const uint32_t birth = a.birth, survive = a.survive;
-    __shared__ uint32_t s_box[kClPipes][kBoxWords];
     __shared__ uint32_t s_stage[kClPipes][2][kStageWords];
     __shared__ uint32_t s_hmask[kClPipes][kSliceSlots];
     __shared__ uint32_t s_dofs[8][kSliceDirMax];           // per direction, slot j: offset in the neighbour tile (B)
@@ -110,25 +207,29 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
     __shared__ int s_qstart[7];                              // first flat entry of direction q
     __shared__ uint32_t s_extw[kClPipes][kSliceSlots];       // HBM halo bits of flat entry m, bit t
     __shared__ uint32_t s_exist[kClPipes][6];                // neighbouring tile present: bit t
-    __shared__ unsigned long long s_ext[kClPipes][kClExtMax];  // HBM (tile, direction) pairs: ptr | q << 56 | t << 59
+    __shared__ unsigned long long s_ext[kClPipes][kClExtMax];  // HBM (tile, direction) pairs: ptr | remote << 55
+                                                               // | q << 56 | t << 59
     __shared__ __align__(8) uint64_t s_mbar[kClPipes][2];
     __shared__ uint32_t s_out[kClPipes][kStageWords];         // stepper -> loader: a batch's result words
     __shared__ __align__(8) uint64_t s_obar[kClPipes][2];     // [0] out full, [1] out empty (32 arrivals)
+    __shared__ const long long* s_peer[kMaxP2P];
     extern __shared__ __align__(16) unsigned char s_dyn[];
     auto s_tma = reinterpret_cast<unsigned char (*)[2][9][kClRunBytes]>(s_dyn);
+    auto s_box = reinterpret_cast<uint32_t (*)[kClBoxes][kBoxWords]>(s_dyn + kClTmaBytes);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int pipe = wib >> 1;
     const bool loader = (wib & 1) == 0;
     const int K = cw.K;
     const bool k7 = lane < 19;
     pdl_trigger();
+    if (P2P && threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
     for (int s = threadIdx.x; s < c_sslots.count; s += blockDim.x)
         s_bidx[s] = (uint16_t)((c_sslots.y[s] + kSliceMaxK) * kBoxW + c_sslots.x[s] + kSliceMaxK);
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         const uint32_t pos = i < 243 ? c_local_pos[i] : 0u;
         s_tb[i] = (uint16_t)(((pos >> 5) + kSliceMaxK) * kBoxW + (pos & 31u) + kSliceMaxK);
     }
-    for (int i = threadIdx.x; i < kClPipes * kBoxWords; i += blockDim.x) (&s_box[0][0])[i] = 0u;
+    for (int i = threadIdx.x; i < kClPipes * kClBoxes * kBoxWords; i += blockDim.x) (&s_box[0][0][0])[i] = 0u;
     if (threadIdx.x < 2 * kClPipes) {
         mbar_init(&s_mbar[threadIdx.x >> 1][threadIdx.x & 1], 1u);
         mbar_init(&s_obar[threadIdx.x >> 1][threadIdx.x & 1], 32u);
@@ -163,10 +264,19 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         }
         s_qstart[6] = m;
     }
-    pdl_wait();
+    if (P2P && p.wait_target != 0u) {
+        // the arrival wait (this rank's own previous pass is among the arrivals); the first pass
+        // of every call also waits for its predecessor grid (whatever last wrote the state)
+        if (threadIdx.x == 0) p2p_wait(p);
+        if (p.first_pass) pdl_wait();
+    } else {
+        pdl_wait();
+    }
     __syncthreads();
+    // every thread orders its peer reads after the arrivals waited for
+    if (P2P && p.wait_target != 0u) asm volatile("fence.acq_rel.sys;" ::: "memory");
 
-    uint32_t* box = s_box[pipe];
+    uint32_t* box = s_box[pipe][0];
     uint32_t* hmask = s_hmask[pipe];
     const uint32_t pipe_global = blockIdx.x * kClPipes + (uint32_t)pipe;
     const uint32_t npipes = gridDim.x * kClPipes;
@@ -243,14 +353,15 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
             }
         };
         uint32_t gc = 0;  // groups consumed (staging buffer gc & 1, use count gc >> 1)
-        if (pipe_global < cw.total) issue(cluster_base(pipe_global), 0u, 0, pipe_global + 1 == cw.total);
+        if (cw.begin + pipe_global < cw.end)
+            issue(cluster_base(cw.begin + pipe_global), 0u, 0, cw.begin + pipe_global + 1 == cw.total);
         uint32_t i = 0;
-        for (uint32_t bt = pipe_global; bt < cw.total; bt += npipes, ++i) {
+        for (uint32_t bt = cw.begin + pipe_global; bt < cw.end; bt += npipes, ++i) {
             const int b = (int)(i & 1u);
             if (i >= 2) nb_op<true>(nb_empty(pipe, b));
             const uint32_t base0 = cluster_base(bt);
             const bool last = bt + 1 == cw.total;
-            const uint32_t nbase = bt + npipes < cw.total ? cluster_base(bt + npipes) : 0u;
+            const uint32_t nbase = bt + npipes < cw.end ? cluster_base(bt + npipes) : 0u;
             const bool st = kClLoaderStores && i >= 2;  // stores the result of batch i - 2 meanwhile
             const uint32_t obase = st ? cluster_base(bt - 2u * npipes) : 0u;
             uint32_t w[8];
@@ -259,7 +370,7 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
 #pragma unroll 1
             for (uint32_t g = 0; g < 9u; ++g, ++gc) {
                 if (g + 1 < 9u) issue(base0, g + 1, (int)((gc + 1) & 1u), last);
-                else if (bt + npipes < cw.total) issue(nbase, 0u, (int)((gc + 1) & 1u), bt + npipes + 1 == cw.total);
+                else if (bt + npipes < cw.end) issue(nbase, 0u, (int)((gc + 1) & 1u), bt + npipes + 1 == cw.total);
                 const int sb_ = (int)(gc & 1u);
                 mbar_wait(&mbar[sb_], (gc >> 1) & 1u);
                 // parity of a run's first element: base0 + (9 g + row) W with W odd
@@ -314,23 +425,21 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         if (kClLoaderStores) {  // the last two results
             const uint32_t nb = i;  // batches of this pipeline
             for (uint32_t o = nb >= 2 ? nb - 2 : 0; o < nb; ++o) {
-                const uint32_t obase = cluster_base(pipe_global + o * npipes);
+                const uint32_t obase = cluster_base(cw.begin + pipe_global + o * npipes);
                 take_out();
 #pragma unroll 1
                 for (uint32_t g = 0; g < 9u; ++g) store_group(obase, g);
             }
         }
-        return;
-    }
-
+    } else {
     // ---- stepper --------------------------------------------------------------------------------
     // lane t < 27 is tile (i, j) = (t / 3, t % 3) of the cluster
     const uint32_t ti = (uint32_t)lane / 3u, tj = (uint32_t)lane % 3u;
     const bool tv = lane < 27;
     uint32_t i = 0;
-    for (uint32_t bt = pipe_global; bt < cw.total; bt += npipes, ++i) {
+    for (uint32_t bt = cw.begin + pipe_global; bt < cw.end; bt += npipes, ++i) {
         const int b = (int)(i & 1u);
-        const bool more2 = bt + 2u * npipes < cw.total;
+        const bool more2 = bt + 2u * npipes < cw.end;
         const uint32_t cx = fastdiv(bt, cw.div_ncy), cy = bt - cx * cw.ncy;
         const uint32_t wx0 = 9u * cx, wy0 = 3u * cy;
         // the neighbouring tiles of tile t: in the cluster (cl_src) or in HBM (an ext pair)
@@ -357,12 +466,16 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
 #endif
                 } else {
                     ext = true;
-                    ptr = reinterpret_cast<unsigned long long>(a.src) + 8ull * (9ull * wxn * a.W + 27ull * wyn);
+                    const uint32_t own = P2P ? fastdiv((uint32_t)nq, p.div_chunk) : 0u;
+                    const long long* src = P2P ? s_peer[own] : a.src;
+                    ptr = reinterpret_cast<unsigned long long>(src) + 8ull * (9ull * wxn * a.W + 27ull * wyn);
+                    if (P2P && own != (uint32_t)p.rank) ptr |= 1ull << 55;  // another rank's buffer
                 }
             }
             const uint32_t ex = __ballot_sync(0xFFFFFFFFu, nq >= 0);
             if (lane == 0) s_exist[pipe][q] = ex;
             const uint32_t em = __ballot_sync(0xFFFFFFFFu, ext);
+            if (next + __popc(em) > (uint32_t)kClExtMax) __trap();  // fail loudly, never overrun s_ext
             if (ext) s_ext[pipe][next + __popc(em & ((1u << lane) - 1u))] = ptr | ((unsigned long long)q << 56) |
                                                                          ((unsigned long long)lane << 59);
             next += __popc(em);
@@ -373,25 +486,29 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
             long long v[8];
             uint32_t meta[8];
 #pragma unroll
-            for (int p = 0; p < 8; ++p) {
-                v[p] = 0;
-                meta[p] = 0xFFFFFFFFu;
-                if (p0 + p < next) {
-                    const unsigned long long e = s_ext[pipe][p0 + p];
+            for (int pp = 0; pp < 8; ++pp) {
+                v[pp] = 0;
+                meta[pp] = 0xFFFFFFFFu;
+                if (p0 + pp < next) {
+                    const unsigned long long e = s_ext[pipe][p0 + pp];
                     const uint32_t q = (uint32_t)(e >> 56) & 7u, t = (uint32_t)(e >> 59);
                     const int d = q < 2 ? (int)q : q < 4 ? (int)q + 1 : (int)q + 2;
                     if (lane < c_sslots.dir_upto[d][K]) {
-                        const unsigned long long ptr = e & ((1ull << 56) - 1ull);
-                        v[p] = __ldg(reinterpret_cast<const long long*>(ptr + s_dofs[d][lane]));
-                        meta[p] = (uint32_t)(s_qstart[q] + lane) | (t << 8);
+                        const unsigned long long ptr = e & ((1ull << 55) - 1ull);
+                        const long long* qp = reinterpret_cast<const long long*>(ptr + s_dofs[d][lane]);
+                        if (P2P && ((e >> 55) & 1ull))  // a cell of another rank's tile: over NVLink
+                            asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v[pp]) : "l"(qp));
+                        else
+                            v[pp] = __ldg(qp);
+                        meta[pp] = (uint32_t)(s_qstart[q] + lane) | (t << 8);
                     }
                 }
             }
 #pragma unroll
-            for (int p = 0; p < 8; ++p)
-                if (meta[p] != 0xFFFFFFFFu) {
-                    const uint32_t nz = (uint32_t)v[p] | (uint32_t)((unsigned long long)v[p] >> 32);
-                    s_extw[pipe][meta[p] & 0xFFu] |= min(nz, 1u) << (meta[p] >> 8);
+            for (int pp = 0; pp < 8; ++pp)
+                if (meta[pp] != 0xFFFFFFFFu) {
+                    const uint32_t nz = (uint32_t)v[pp] | (uint32_t)((unsigned long long)v[pp] >> 32);
+                    s_extw[pipe][meta[pp] & 0xFFu] |= min(nz, 1u) << (meta[pp] >> 8);
                 }
         }
         // the batch's tile words into the box
@@ -423,7 +540,9 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         halo_dir(std::integral_constant<int, 5>{});
         // K steps, then the 27 tiles' values out
         uint32_t w[8];
-        sliced_steps<CONWAY>(box, hmask, K, s_cb, s_bidx, s_tb, birth, survive, w);
+        if (NBB_CL_DBOX) cluster_steps2<CONWAY>(box, s_box[pipe][kClBoxes - 1], hmask, K, s_cb, s_bidx, s_tb, birth, survive, w);
+        else if (NBB_CL_HOIST) cluster_steps<CONWAY>(box, hmask, K, s_cb, s_bidx, s_tb, birth, survive, w);
+        else sliced_steps<CONWAY>(box, hmask, K, s_cb, s_bidx, s_tb, birth, survive, w);
         if (kClLoaderStores) {  // to the loader: wait until it took the previous result
             if (i >= 1) mbar_wait(&s_obar[pipe][1], (i - 1u) & 1u);
 #pragma unroll
@@ -448,6 +567,8 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
                 if (k < 7 || k7) *reinterpret_cast<long long*>(Q + off[k]) = (long long)((w[k] >> t) & 1u);
         }
     }
+    }  // stepper
+    if (P2P) p2p_arrive(p);  // after the CTA's last store (the loader's)
 }
 
 }  // namespace nbbgpu

@@ -895,9 +895,12 @@ bool cluster_impl() {  // read per launch: comparison runs flip it inside one pr
     const char* e = std::getenv("NBB_PASS_IMPL");
     return !(e && (std::strcmp(e, "sliced") == 0 || std::strcmp(e, "warp") == 0));
 }
+// ... over a shard of whole cluster columns (9 Hb tiles: the whole orthotope, or a multi-GPU
+// chunk of nbbhost::compact_shard_chunk; an empty shard at the end also qualifies)
 bool cluster_walk_ok(const CompactCaArgs& a) {
-    return cluster_impl() && a.rb >= 3 && a.tile_begin == 0 && a.tile_end == a.tiles && a.Wb % 9u == 0 &&
-           a.Hb % 3u == 0;
+    if (!cluster_impl() || a.rb < 3 || a.Wb % 9u != 0 || a.Hb % 3u != 0) return false;
+    const uint32_t col = 9u * a.Hb;
+    return a.tile_begin % col == 0 && (a.tile_end % col == 0 || a.tile_end == a.tiles) && a.tile_begin <= a.tile_end;
 }
 ClusterWalk cluster_walk(const CompactCaArgs& a, int k) {
     ClusterWalk c{};
@@ -906,6 +909,9 @@ ClusterWalk cluster_walk(const CompactCaArgs& a, int k) {
     c.div_ncy.d = c.ncy;
     nbbhost::fastdiv_magic(c.ncy, &c.div_ncy.m, &c.div_ncy.s);
     c.total = (a.Wb / 9u) * c.ncy;
+    const uint32_t col = 9u * a.Hb;
+    c.begin = a.tile_begin / col * c.ncy;
+    c.end = std::min(c.total, (a.tile_end + col - 1) / col * c.ncy);
     return c;
 }
 int cluster_grid(DeviceCtx* ctx, const void* kern, uint64_t batches, unsigned* grid) {
@@ -924,6 +930,25 @@ int cluster_grid(DeviceCtx* ctx, const void* kern, uint64_t batches, unsigned* g
     }
     const uint64_t wave = (uint64_t)ctx->sms * occ;
     *grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(wave, (batches + kClPipes - 1) / kClPipes));
+    return NBB_OK;
+}
+
+// One pass of the cluster walk (P2P: a rank's pass of the multi-GPU step); `sharing` workers
+// co-resident on the device get a share of one wave each and no PDL (they wait on each other)
+template <bool P2P>
+int launch_cluster_pass(DeviceCtx* ctx, const CompactCaArgs& a, int k, bool conway, const FastDiv& div_hb,
+                        const int32_t* tab, const P2PArgs& p, cudaStream_t st, int sharing = 1) {
+    const ClusterWalk cw = cluster_walk(a, k);
+    auto kern = conway ? ca_compact_cluster_kernel<true, P2P> : ca_compact_cluster_kernel<false, P2P>;
+    unsigned grid;
+    NBB_CHECK(cluster_grid(ctx, (const void*)kern, std::max<uint64_t>(1, cw.end - cw.begin), &grid));
+    if (sharing > 1) {
+        grid = std::max(1u, grid / (unsigned)sharing);
+        kern<<<grid, 32 * kClWarps, kClDynSmem, st>>>(a, cw, div_hb, tab, p);
+        NBB_CUDA(cudaGetLastError());
+        return NBB_OK;
+    }
+    NBB_CUDA(launch_pdl_smem(kern, grid, 32 * kClWarps, kClDynSmem, st, a, cw, div_hb, tab, p));
     return NBB_OK;
 }
 
@@ -983,14 +1008,8 @@ int launch_pass(DeviceCtx* ctx, const nbb_config* cfg, const void* src, void* ds
     const uint64_t want = (a.tile_end - a.tile_begin + 7) / 8;
     if (want == 0) return NBB_OK;
     const bool bb = cfg->mode == NBB_MODE_BB;
-    if (!bb && sliced_impl() && cluster_walk_ok(a)) {
-        const ClusterWalk cw = cluster_walk(a, k);
-        auto kern = is_conway(birth, survive) ? ca_compact_cluster_kernel<true> : ca_compact_cluster_kernel<false>;
-        unsigned grid;
-        NBB_CHECK(cluster_grid(ctx, (const void*)kern, cw.total, &grid));
-        NBB_CUDA(launch_pdl_smem(kern, grid, 32 * kClWarps, kClDynSmem, st, a, cw, div_hb, tab));
-        return NBB_OK;
-    }
+    if (!bb && sliced_impl() && cluster_walk_ok(a))
+        return launch_cluster_pass<false>(ctx, a, k, is_conway(birth, survive), div_hb, tab, P2PArgs{}, st);
     if (sliced_impl()) {
         const SliceBatches sb = slice_batches(a, k);
         auto kern = bb ? sliced_kernel<false, true>(is_conway(birth, survive))
@@ -1048,12 +1067,13 @@ int p2p_passes(const nbb_config* cfg, int64_t first_pass, int32_t steps, int kma
     CompactCaArgs a = compact_args(cfg, p2p->d_buf[0], p2p->d_buf[1], birth, survive, &div_hb);
     // the owner of a halo cell is its tile's ordinal / chunk: the shard must be the reference's
     // contiguous worker chunk (dispatch.cpp:419-427) of this rank, as every peer assumes
-    const uint32_t chunk = (a.tiles + (uint32_t)p2p->world - 1) / (uint32_t)p2p->world;
+    const uint32_t chunk = (uint32_t)nbbhost::compact_shard_chunk(a.rb, a.tiles, a.Hb, p2p->world);
     const uint64_t want_b = std::min<uint64_t>((uint64_t)chunk * (uint64_t)p2p->rank, a.tiles);
     const uint64_t want_e = std::min<uint64_t>(want_b + chunk, a.tiles);
     if (cfg->shard_count == 0 || a.tile_begin != want_b || a.tile_end != want_e)
         return fail(NBB_ERR_INVALID_ARGUMENT,
-                    "p2p: the shard must be the rank's contiguous chunk of ceil(tiles / world) tiles: [" +
+                    "p2p: the shard must be the rank's contiguous chunk of tiles (nbb_gpu.h: ceil(tiles / world) "
+                    "rounded up to whole 9 Hb-tile cluster columns when r >= 8): [" +
                         std::to_string(want_b) + ", " + std::to_string(want_e) + ")");
     const int32_t* tab;
     NBB_CHECK(compact_nbr_table(ctx, cfg, a, div_hb, &tab));
@@ -1079,6 +1099,12 @@ int p2p_passes(const nbb_config* cfg, int64_t first_pass, int32_t steps, int kma
         p.peer_src = (const long long* const*)p2p->d_peer_buf[par];
         p.wait_target = (unsigned int)((uint64_t)p2p->world * (uint64_t)j);
         p.first_pass = i == 0 ? 1u : 0u;
+        if (sliced_impl() && cluster_walk_ok(a)) {
+            NBB_CHECK(launch_cluster_pass<true>(ctx, a, passes[i], conway, div_hb, tab, p, stream));
+            ++ps.passes;
+            ++ps.by_steps[passes[i]];
+            continue;
+        }
         if (sliced_impl()) {
             const SliceBatches sb = slice_batches(a, passes[i]);
             auto kern = sliced_kernel<true, false>(conway);
@@ -1666,7 +1692,7 @@ int nbb_gpu_reduction_multi(const nbb_config* cfg, const int32_t* devices, int32
     // addition wraps like the reference's accumulation, so any split gives the same value)
     FastDiv d;
     const CompactCaArgs a = compact_args(&c, nullptr, nullptr, 0, 0, &d);
-    const uint32_t chunk = (a.tiles + (uint32_t)ndev - 1) / (uint32_t)ndev;
+    const uint32_t chunk = (uint32_t)nbbhost::compact_shard_chunk(a.rb, a.tiles, a.Hb, ndev);
     unsigned long long total = 0;
     for (int w = 0; w < ndev; ++w) {
         nbb_config wc = c;

@@ -689,7 +689,7 @@ Error halo_exchange_lists(int r, int world, int rank, int kmax, std::vector<std:
     for (int i = 0; i < (rb + 1) / 2; ++i) Wb *= 3;
     for (int i = 0; i < rb / 2; ++i) Hb *= 3;
     const uint64_t tiles = Wb * Hb, nb = uint64_t(1) << rb;
-    const uint64_t chunk = (tiles + (uint64_t)world - 1) / (uint64_t)world;
+    const uint64_t chunk = compact_shard_chunk(rb, tiles, Hb, world);
     auto owner = [&](uint64_t u) { return (int)(u / chunk); };
     auto base = [&](uint64_t u) { return 9 * (u / Hb) * W + 27 * (u % Hb); };
     // slot offsets inside a neighbouring tile, per direction, layers <= kmax

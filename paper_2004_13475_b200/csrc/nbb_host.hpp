@@ -115,6 +115,19 @@ Error slice_slots(SliceSlots* out);
 // compact offsets of rank j's cells that lie in a halo slot of layer <= kmax of one of `rank`'s
 // tiles, send[j] = the offsets of `rank`'s cells that rank j needs; sorted, unique. send[j] on
 // rank i equals recv[i] on rank j by construction.
+// Tiles per rank of the multi-GPU compact CA (the reference's contiguous worker chunks,
+// dispatch.cpp:419-427, in the tile order u = ωx_b·Hb + ωy_b): ceil(tiles / world), rounded up to
+// whole cluster columns (9·Hb tiles: every rank then owns whole level-3 clusters, the batches of
+// compact_cluster.cuh) when r_b >= 3. Results are identical for any split; this one is shared by
+// every multi-GPU entry point (peer passes, workers as devices, the NCCL communicator's lists).
+inline uint64_t compact_shard_chunk(int rb, uint64_t tiles, uint64_t Hb, int world) {
+    if (world < 1) world = 1;
+    if (rb >= 3 && Hb % 3 == 0 && tiles % (9 * Hb) == 0) {
+        const uint64_t col = 9 * Hb, ncol = tiles / col;
+        return ((ncol + (uint64_t)world - 1) / (uint64_t)world) * col;
+    }
+    return (tiles + (uint64_t)world - 1) / (uint64_t)world;
+}
 Error halo_exchange_lists(int r, int world, int rank, int kmax, std::vector<std::vector<uint32_t>>* send,
                           std::vector<std::vector<uint32_t>>* recv);
 

@@ -30,6 +30,18 @@ HALO = np.array([(-1, -1), (0, -1), (1, -1), (-1, -2), (-2, -3), (-2, -2), (-2, 
                 dtype=np.int64)
 
 
+def compact_shard_chunk(r_b: int, tiles: int, Hb: int, world: int) -> int:
+    """Tiles per rank of the compact-state CA (nbbhost::compact_shard_chunk): ceil(tiles / world)
+    — the reference's contiguous worker chunks (dispatch.cpp:419-427) — rounded up to whole
+    cluster columns of 9·Hb tiles when r_b >= 3, so every rank owns whole level-3 clusters (the
+    batches of the library's cluster pass). Results are identical for any split."""
+    world = max(1, world)
+    if r_b >= 3 and Hb % 3 == 0 and tiles % (9 * Hb) == 0:
+        col = 9 * Hb
+        return -(-(tiles // col) // world) * col
+    return -(-tiles // world)
+
+
 def _halo_offsets(rho: int) -> np.ndarray:
     """The 8 candidate halo cells of a member tile, tile-local (x, y)."""
     return np.array([(-1, -1), (0, -1), (1, -1), (-1, rho - 1), (rho, rho - 2), (rho, rho - 1),
@@ -102,7 +114,8 @@ class ShardPlan:
         self.W = 3 ** ((self.r_b + 1) // 2)
         self.Hb = 3 ** (self.r_b // 2)
         self.total = 3 ** self.r_b
-        self.chunk = -(-self.total // self.world)
+        self.chunk = (compact_shard_chunk(self.r_b, self.total, self.Hb, self.world)
+                      if self.state == "compact" else -(-self.total // self.world))
         self.begin = min(self.rank * self.chunk, self.total)
         self.count = max(0, min(self.chunk, self.total - self.begin))
         if self.world > 1:

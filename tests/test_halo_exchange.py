@@ -1,7 +1,7 @@
 """Host logic of the multi-process compact CA over NCCL (nbb_gpu_ca_compact_comm_dev): the halo
 exchange lists (nbb_gpu_halo_exchange_counts / _lists, nbbhost::halo_exchange_lists).
 
-Each rank owns the contiguous chunk of ceil(tiles / world) compact tiles (dispatch.cpp:419-427).
+Each rank owns the contiguous chunk of compact tiles of shard.compact_shard_chunk (ceil(tiles / world) rounded up to whole cluster columns; dispatch.cpp:419-427).
 Before a pass of K steps it must hold every cell of another rank that can reach one of its
 members within K steps. Checked here without a GPU:
   * K = 1 equals the one-step exchange of the Python shard plan (shard.ShardPlan, state="compact"),
@@ -56,11 +56,11 @@ def test_one_step_lists_equal_shard_plan(r, world):
             assert np.array_equal(np.sort(plan.send_idx[so[p]:so[p + 1]]), send[p]), (rank, p)
 
 
-@pytest.mark.parametrize("r,world", [(7, 2), (9, 3), (10, 8)])
+@pytest.mark.parametrize("r,world", [(7, 2), (11, 3), (10, 8), (12, 4)])
 def test_lists_symmetric_and_owned(r, world):
     W, Hb = 3 ** ((r + 1) // 2), 3 ** ((r - 5) // 2)
     tiles = 3 ** (r - 5)
-    chunk = -(-tiles // world)
+    chunk = shard.compact_shard_chunk(r - 5, tiles, Hb, world)
     for k in (2, 5, 8):
         al = [lists(r, world, q, k) for q in range(world)]
         for i in range(world):
@@ -75,14 +75,14 @@ def test_lists_symmetric_and_owned(r, world):
                 assert np.isin(small[i][1][j], al[i][1][j]).all()  # grows with K
 
 
-@pytest.mark.parametrize("r,world,k", [(8, 3, 3), (9, 2, 6), (9, 4, 8)])
+@pytest.mark.parametrize("r,world,k", [(7, 3, 3), (10, 3, 3), (10, 2, 6), (11, 4, 8)])
 def test_lists_cover_the_k_step_neighbourhood(r, world, k):
     """Brute force: BFS over member cells from every member of the rank's tiles, k layers; every
     reached cell owned by another rank is in the receive list from that rank."""
     n = 1 << r
     W = 3 ** ((r + 1) // 2)
     tiles = 3 ** (r - 5)
-    chunk = -(-tiles // world)
+    chunk = shard.compact_shard_chunk(r - 5, tiles, 3 ** ((r - 5) // 2), world)
     ys, xs = np.nonzero(((np.arange(n)[None, :] & ~np.arange(n)[:, None]) == 0))  # x ⊆ y
     member = np.zeros((n, n), dtype=bool)
     member[ys, xs] = True

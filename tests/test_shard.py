@@ -116,7 +116,7 @@ def _compact_worker(rank, world, port, r, steps, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,r", [(2, 8), (3, 9)])
+@pytest.mark.parametrize("world,r", [(2, 7), (2, 10), (3, 10)])
 def test_sharded_compact_ca_matches_single_domain(world, r):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
