@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define NBB_GPU_ABI_VERSION 3
+#define NBB_GPU_ABI_VERSION 4  /* 4: nbb_pass_stats.by_steps[13], passes of up to 12 steps */
 #define NBB_MAX_REPLICAS 9
 
 /* Status codes; the C++ shim (nbb_gpu.hpp) rethrows the matching std:: type. */
@@ -101,7 +101,9 @@ typedef struct nbb_config {
     uint64_t shard_count;
     uint32_t flags;     /* NBB_FLAG_* */
     uint32_t pass_steps; /* compact-state CA: at most this many steps per pass over the
-                          * state (1..8; 0 = 8). See nbb_gpu_ca_compact_passes_dev. */
+                          * state (1..12; 0 = 8; above 8 only the cluster walk — gasket,
+                          * lambda, r >= 8 — the others cap at 8). See
+                          * nbb_gpu_ca_compact_passes_dev. */
 } nbb_config;
 
 /* nbb_config.flags
@@ -126,7 +128,8 @@ typedef struct nbb_config {
 /* NBB_FLAG_SINGLE_STEP: compact-state CA runs (nbb_gpu_ca with NBB_FLAG_COMPACT_STATE,
  *   nbb_gpu_ca_compact_*_dev) launch one kernel per step (= pass_steps 1). Without it,
  *   untimed runs advance up to pass_steps (default 8) steps per pass over the state
- *   (ca_compact_sliced_kernel: the tile and its radius-K halo are read once, the intermediate
+ *   (ca_compact_cluster_kernel / ca_compact_sliced_kernel: the tile and its radius-K halo are
+ *   read once, the intermediate
  *   steps stay on chip) — the same result. */
 #define NBB_FLAG_SINGLE_STEP 4u
 
@@ -150,7 +153,7 @@ typedef struct nbb_report {
 /* What a pass sequence did: launches, launches per step count, where the result is. */
 typedef struct nbb_pass_stats {
     int32_t passes;       /* kernel launches (passes over the state)                  */
-    int32_t by_steps[9];  /* by_steps[k]: passes that advanced k steps (k = 1..8)      */
+    int32_t by_steps[13]; /* by_steps[k]: passes that advanced k steps (k = 1..12)     */
     int32_t result_in_b;  /* 1: the state after `steps` steps is in d_b; 0: in d_a     */
 } nbb_pass_stats;
 

@@ -92,7 +92,7 @@ class NbbPassStats(Structure):
     """nbb_pass_stats (nbb_gpu.h): the passes a compact CA run issued."""
     _fields_ = [
         ("passes", c_int32),
-        ("by_steps", c_int32 * 9),
+        ("by_steps", c_int32 * 13),
         ("result_in_b", c_int32),
     ]
 

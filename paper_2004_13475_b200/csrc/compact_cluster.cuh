@@ -23,7 +23,7 @@
 // cluster is 9 groups (one per i) of three consecutive tiles = nine 81-value (648 B) runs of
 // compact rows per group; the loader fetches a group with nine bulk (TMA) copies into a
 // double-buffered staging area and folds it into the stage words, as in the sliced λ loader.
-// The steps and stores are the sliced pass's (sliced_steps). Needs r_b >= 3 (ωx has two digits,
+// The steps are the sliced pass's cell update with radius up to 12 (cluster_steps). Needs r_b >= 3 (ωx has two digits,
 // ωy one) and the whole orthotope in one launch (the single-device λ walk); shards, the BB walk
 // and the multi-GPU pass keep the 32-ordinal batches of compact_sliced.cuh.
 #pragma once
@@ -33,6 +33,21 @@
 #include "compact_sliced.cuh"
 
 namespace nbbgpu {
+
+using nbbhost::ClusterSlots;
+using nbbhost::kClDirSlots;
+using nbbhost::kClMaxK;
+using nbbhost::kClSlots;
+__constant__ ClusterSlots c_cslots;  // the radius-12 halo slots (nbbhost::cluster_slots)
+// The box of a pass of up to F steps: the tile and an F-cell frame (odd row pitch). Two
+// instantiations: F = 8 with two boxes per stepper (cluster_steps2), F = 12 with one.
+template <int F>
+struct ClBox {
+    static constexpr int kH = 32 + 2 * F, kW = kH + 1, kWords = kW * kH;
+    static constexpr int kBoxes = F <= 8 ? 2 : 1;
+    static constexpr int kM = F <= 8 ? 4 : 8;  // halo slots a lane advances per step: upto[F - 1] <= 32 kM
+    static_assert(F <= kClMaxK && kWords <= 4096, "box index: 12 bits");
+};
 
 constexpr int kClPipes = 2;                                         // loader/stepper pipelines per CTA
 constexpr int kClWarps = 2 * kClPipes;
@@ -93,40 +108,41 @@ constexpr bool kClLoaderStores = NBB_CL_LSTORE != 0;
 // K steps of a batch in its box (sliced_steps with the lane's box indices and halo masks held in
 // registers across the steps: shared memory is written between the steps, so the compiler
 // would reload them every step)
-template <bool CONWAY>
-__device__ __forceinline__ void cluster_steps(uint32_t* box, const uint32_t* hmask, int K, const uint16_t* cb,
+template <bool CONWAY, int BW, int M>
+__device__ __forceinline__ void cluster_steps(uint32_t* box, const uint32_t* exist, const uint8_t* sq, int K,
+                                              const uint16_t* cb,
                                               const uint16_t* bidx, const uint16_t* tb, uint32_t birth,
                                               uint32_t survive, uint32_t (&w)[8]) {
     const int lane = threadIdx.x & 31;
     const bool k7 = lane < 19;
     __syncwarp();
-    uint32_t ci[8], hi[kSliceMaxM], hm[kSliceMaxM];
+    uint32_t ci[8], hi[M], hm[M];
 #pragma unroll
     for (int k = 0; k < 8; ++k) ci[k] = (k < 7 || k7) ? cb[32 * k + lane] : 0u;
-    const int n0 = c_sslots.upto[K - 1];
+    const int n0 = c_cslots.upto[K - 1];
 #pragma unroll
-    for (int m = 0; m < kSliceMaxM; ++m) {
+    for (int m = 0; m < M; ++m) {
         const int s = lane + 32 * m;
         hi[m] = s < n0 ? bidx[s] : 0u;
-        hm[m] = s < n0 ? hmask[s] : 0u;
+        hm[m] = s < n0 ? exist[sq[s]] : 0u;  // the slot's neighbouring tile is present: bit t
     }
     for (int j = 1; j <= K; ++j) {
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (k < 7 || k7) w[k] = sliced_cell_step<CONWAY>(box + ci[k], birth, survive);
-        const int ns = c_sslots.upto[K - j];
-        uint32_t hn[kSliceMaxM];
+            if (k < 7 || k7) w[k] = sliced_cell_step<CONWAY, BW>(box + ci[k], birth, survive);
+        const int ns = c_cslots.upto[K - j];
+        uint32_t hn[M];
 #pragma unroll
-        for (int m = 0; m < kSliceMaxM; ++m) {
+        for (int m = 0; m < M; ++m) {
             hn[m] = 0u;
-            if (lane + 32 * m < ns) hn[m] = sliced_cell_step<CONWAY>(box + hi[m], birth, survive) & hm[m];
+            if (lane + 32 * m < ns) hn[m] = sliced_cell_step<CONWAY, BW>(box + hi[m], birth, survive) & hm[m];
         }
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             if (k < 7 || k7) box[ci[k]] = w[k];
 #pragma unroll
-        for (int m = 0; m < kSliceMaxM; ++m)
+        for (int m = 0; m < M; ++m)
             if (lane + 32 * m < ns) box[hi[m]] = hn[m];
         __syncwarp();
     }
@@ -138,33 +154,34 @@ __device__ __forceinline__ void cluster_steps(uint32_t* box, const uint32_t* hma
 // needs one warp barrier and no result is held across it. A halo slot not advanced at step j
 // (layer > K - j) keeps a stale value in the written box, read only by cells that are not needed
 // either; the non-member frame is zero in both boxes.
-template <bool CONWAY>
-__device__ __forceinline__ void cluster_steps2(uint32_t* box0, uint32_t* box1, const uint32_t* hmask, int K,
+template <bool CONWAY, int BW, int M>
+__device__ __forceinline__ void cluster_steps2(uint32_t* box0, uint32_t* box1, const uint32_t* exist,
+                                               const uint8_t* sq, int K,
                                                const uint16_t* cb, const uint16_t* bidx, const uint16_t* tb,
                                                uint32_t birth, uint32_t survive, uint32_t (&w)[8]) {
     const int lane = threadIdx.x & 31;
     const bool k7 = lane < 19;
     __syncwarp();
-    uint32_t ci[8], hi[kSliceMaxM], hm[kSliceMaxM];
+    uint32_t ci[8], hi[M], hm[M];
 #pragma unroll
     for (int k = 0; k < 8; ++k) ci[k] = (k < 7 || k7) ? cb[32 * k + lane] : 0u;
-    const int n0 = c_sslots.upto[K - 1];
+    const int n0 = c_cslots.upto[K - 1];
 #pragma unroll
-    for (int m = 0; m < kSliceMaxM; ++m) {
+    for (int m = 0; m < M; ++m) {
         const int s = lane + 32 * m;
         hi[m] = s < n0 ? bidx[s] : 0u;
-        hm[m] = s < n0 ? hmask[s] : 0u;
+        hm[m] = s < n0 ? exist[sq[s]] : 0u;  // the slot's neighbouring tile is present: bit t
     }
     for (int j = 1; j <= K; ++j) {
         const uint32_t* src = (j & 1) ? box0 : box1;
         uint32_t* dst = (j & 1) ? box1 : box0;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (k < 7 || k7) dst[ci[k]] = sliced_cell_step<CONWAY>(src + ci[k], birth, survive);
-        const int ns = c_sslots.upto[K - j];
+            if (k < 7 || k7) dst[ci[k]] = sliced_cell_step<CONWAY, BW>(src + ci[k], birth, survive);
+        const int ns = c_cslots.upto[K - j];
 #pragma unroll
-        for (int m = 0; m < kSliceMaxM; ++m)
-            if (lane + 32 * m < ns) dst[hi[m]] = sliced_cell_step<CONWAY>(src + hi[m], birth, survive) & hm[m];
+        for (int m = 0; m < M; ++m)
+            if (lane + 32 * m < ns) dst[hi[m]] = sliced_cell_step<CONWAY, BW>(src + hi[m], birth, survive) & hm[m];
         __syncwarp();
     }
     const uint32_t* fin = (K & 1) ? box1 : box0;
@@ -172,16 +189,9 @@ __device__ __forceinline__ void cluster_steps2(uint32_t* box0, uint32_t* box1, c
     for (int k = 0; k < 8; ++k) w[k] = (k < 7 || k7) ? fin[tb[32 * k + lane]] : 0u;
 }
 
-#ifndef NBB_CL_DBOX  // two boxes per pipeline (cluster_steps2)
-#define NBB_CL_DBOX 1
-#endif
-constexpr int kClBoxes = NBB_CL_DBOX ? 2 : 1;
-// dynamic shared memory: the loaders' staging, then the steppers' boxes [pipe][box][word]
-constexpr size_t kClDynSmem = kClTmaBytes + (size_t)kClPipes * kClBoxes * kBoxWords * 4;
+template <int F>
+constexpr size_t cl_dyn_smem() { return kClTmaBytes + (size_t)kClPipes * ClBox<F>::kBoxes * ClBox<F>::kWords * 4; }
 
-#ifndef NBB_CL_HOIST  // cluster_steps (1) or sliced_steps (0; tuning builds)
-#define NBB_CL_HOIST 1
-#endif
 
 #ifndef NBB_CLUSTER_MINB  // resident CTAs per SM the register budget is cut for (tuning builds)
 #define NBB_CLUSTER_MINB 3
@@ -190,22 +200,23 @@ constexpr size_t kClDynSmem = kClTmaBytes + (size_t)kClPipes * kClBoxes * kBoxWo
 // P2P: one rank's pass of the multi-GPU CA (its shard is whole cluster columns, so every tile of a
 // cluster is its own; the halo cells of neighbouring clusters owned by other ranks are read from
 // their buffers over NVLink; the flag barrier of compact_kernels.cuh orders the passes).
-template <bool CONWAY, bool P2P>
+template <bool CONWAY, bool P2P, int F>
 __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
     ca_compact_cluster_kernel(CompactCaArgs a, ClusterWalk cw, FastDiv div_hb, const int32_t* __restrict__ nbr_tab,
                               P2PArgs p) {
+    constexpr int kClBoxW = ClBox<F>::kW, kClBoxWords = ClBox<F>::kWords, kClBoxes = ClBox<F>::kBoxes;
     const uint32_t birth = a.birth, survive = a.survive;
     __shared__ uint32_t s_stage[kClPipes][2][kStageWords];
-    __shared__ uint32_t s_hmask[kClPipes][kSliceSlots];
-    __shared__ uint32_t s_dofs[8][kSliceDirMax];           // per direction, slot j: offset in the neighbour tile (B)
-    __shared__ uint16_t s_bidx[kSliceSlots];
+    __shared__ uint8_t s_sq[kClSlots];                     // halo direction q of every slot
+    __shared__ uint32_t s_dofs[8][kClDirSlots];           // per direction, slot j: offset in the neighbour tile (B)
+    __shared__ uint16_t s_bidx[kClSlots];
     __shared__ uint16_t s_tb[256];
     __shared__ uint16_t s_cb[256];
-    __shared__ uint32_t s_hflat[kSliceSlots];                // halo slots of this K, direction-major:
+    __shared__ uint32_t s_hflat[kClSlots];                // halo slots of this K, direction-major:
                                                              // box index of the cell in the neighbour
-                                                             // | slot << 12 | 5 q << 20
+                                                             // | slot << 12
     __shared__ int s_qstart[7];                              // first flat entry of direction q
-    __shared__ uint32_t s_extw[kClPipes][kSliceSlots];       // HBM halo bits of flat entry m, bit t
+    __shared__ uint32_t s_extw[kClPipes][kClSlots];       // HBM halo bits of flat entry m, bit t
     __shared__ uint32_t s_exist[kClPipes][6];                // neighbouring tile present: bit t
     __shared__ unsigned long long s_ext[kClPipes][kClExtMax];  // HBM (tile, direction) pairs: ptr | remote << 55
                                                                // | q << 56 | t << 59
@@ -215,7 +226,7 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
     __shared__ const long long* s_peer[kMaxP2P];
     extern __shared__ __align__(16) unsigned char s_dyn[];
     auto s_tma = reinterpret_cast<unsigned char (*)[2][9][kClRunBytes]>(s_dyn);
-    auto s_box = reinterpret_cast<uint32_t (*)[kClBoxes][kBoxWords]>(s_dyn + kClTmaBytes);
+    auto s_box = reinterpret_cast<uint32_t (*)[kClBoxes][kClBoxWords]>(s_dyn + kClTmaBytes);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int pipe = wib >> 1;
     const bool loader = (wib & 1) == 0;
@@ -223,13 +234,13 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
     const bool k7 = lane < 19;
     pdl_trigger();
     if (P2P && threadIdx.x < (unsigned)p.world) s_peer[threadIdx.x] = p.peer_src[threadIdx.x];
-    for (int s = threadIdx.x; s < c_sslots.count; s += blockDim.x)
-        s_bidx[s] = (uint16_t)((c_sslots.y[s] + kSliceMaxK) * kBoxW + c_sslots.x[s] + kSliceMaxK);
+    for (int s = threadIdx.x; s < c_cslots.count; s += blockDim.x)
+        s_bidx[s] = (uint16_t)((c_cslots.y[s] + F) * kClBoxW + c_cslots.x[s] + F);
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         const uint32_t pos = i < 243 ? c_local_pos[i] : 0u;
-        s_tb[i] = (uint16_t)(((pos >> 5) + kSliceMaxK) * kBoxW + (pos & 31u) + kSliceMaxK);
+        s_tb[i] = (uint16_t)(((pos >> 5) + F) * kClBoxW + (pos & 31u) + F);
     }
-    for (int i = threadIdx.x; i < kClPipes * kClBoxes * kBoxWords; i += blockDim.x) (&s_box[0][0][0])[i] = 0u;
+    for (int i = threadIdx.x; i < kClPipes * kClBoxes * kClBoxWords; i += blockDim.x) (&s_box[0][0][0])[i] = 0u;
     if (threadIdx.x < 2 * kClPipes) {
         mbar_init(&s_mbar[threadIdx.x >> 1][threadIdx.x & 1], 1u);
         mbar_init(&s_obar[threadIdx.x >> 1][threadIdx.x & 1], 32u);
@@ -239,15 +250,15 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         uint32_t y = 0, seen = 0;
         for (uint32_t c = threadIdx.x; c < 243u; c += blockDim.x) {
             while (seen + (1u << __popc(y)) <= c) seen += 1u << __popc(y++);
-            s_cb[c] = (uint16_t)((y + kSliceMaxK) * kBoxW + pdep32(c - seen, y) + kSliceMaxK);
+            s_cb[c] = (uint16_t)((y + F) * kClBoxW + pdep32(c - seen, y) + F);
         }
     }
     __syncthreads();  // s_tb before s_hflat
-    for (int i = threadIdx.x; i < 8 * kSliceDirMax; i += blockDim.x) {
-        const int d = i / kSliceDirMax, j = i % kSliceDirMax;
+    for (int i = threadIdx.x; i < 8 * kClDirSlots; i += blockDim.x) {
+        const int d = i / kClDirSlots, j = i % kClDirSlots;
         uint32_t o = 0u;
-        if (j < c_sslots.dir_upto[d][kSliceMaxK]) {
-            const uint32_t li = c_sslots.li[c_sslots.by_dir[d][j]];
+        if (j < c_cslots.dir_upto[d][kClMaxK]) {
+            const uint32_t li = c_cslots.li[c_cslots.by_dir[d][j]];
             o = 8u * ((li / 27u) * a.W + li % 27u);
         }
         s_dofs[d][j] = o;
@@ -257,9 +268,10 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         for (int q = 0; q < 6; ++q) {
             const int d = q < 2 ? q : q < 4 ? q + 1 : q + 2;
             s_qstart[q] = m;
-            for (int j = 0; j < c_sslots.dir_upto[d][K]; ++j, ++m) {
-                const uint32_t sl = c_sslots.by_dir[d][j];
-                s_hflat[m] = (uint32_t)s_tb[c_sslots.li[sl]] | (sl << 12) | ((5u * q) << 20);
+            for (int j = 0; j < c_cslots.dir_upto[d][K]; ++j, ++m) {
+                const uint32_t sl = c_cslots.by_dir[d][j];
+                s_sq[sl] = (uint8_t)q;
+                s_hflat[m] = (uint32_t)s_tb[c_cslots.li[sl]] | (sl << 12);
             }
         }
         s_qstart[6] = m;
@@ -277,7 +289,6 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
     if (P2P && p.wait_target != 0u) asm volatile("fence.acq_rel.sys;" ::: "memory");
 
     uint32_t* box = s_box[pipe][0];
-    uint32_t* hmask = s_hmask[pipe];
     const uint32_t pipe_global = blockIdx.x * kClPipes + (uint32_t)pipe;
     const uint32_t npipes = gridDim.x * kClPipes;
     const uint64_t total_elems = (uint64_t)a.W * (uint64_t)(a.tiles / a.Hb) * 9u;  // 3^r
@@ -451,7 +462,7 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         }
         const int32_t nbr6[6] = {n0.x, n0.y, n0.w, n1.x, n1.z, n1.w};  // directions 0,1,3,4,6,7
         uint32_t next = 0;  // ext pairs listed
-        for (int m = lane; m < kSliceSlots; m += 32) s_extw[pipe][m] = 0u;
+        for (int m = lane; m < kClSlots; m += 32) s_extw[pipe][m] = 0u;
 #pragma unroll
         for (int q = 0; q < 6; ++q) {
             const int32_t nq = nbr6[q];
@@ -481,34 +492,37 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
             next += __popc(em);
         }
         __syncwarp();
-        // the HBM halo cells: pair p = (tile t, direction q); lane j loads the pair's slot j
-        for (uint32_t p0 = 0; p0 < next; p0 += 8) {
+        // the HBM halo cells: pair p = (tile t, direction q); load unit (p, h): lane j loads the
+        // pair's slot j = lane + 32 h (a direction holds up to kClDirSlots slots)
+        for (uint32_t u0 = 0; u0 < 2u * next; u0 += 8) {
             long long v[8];
             uint32_t meta[8];
 #pragma unroll
-            for (int pp = 0; pp < 8; ++pp) {
-                v[pp] = 0;
-                meta[pp] = 0xFFFFFFFFu;
-                if (p0 + pp < next) {
-                    const unsigned long long e = s_ext[pipe][p0 + pp];
+            for (int uu = 0; uu < 8; ++uu) {
+                v[uu] = 0;
+                meta[uu] = 0xFFFFFFFFu;
+                const uint32_t u = u0 + uu;
+                if (u < 2u * next) {
+                    const unsigned long long e = s_ext[pipe][u >> 1];
                     const uint32_t q = (uint32_t)(e >> 56) & 7u, t = (uint32_t)(e >> 59);
                     const int d = q < 2 ? (int)q : q < 4 ? (int)q + 1 : (int)q + 2;
-                    if (lane < c_sslots.dir_upto[d][K]) {
+                    const int j = lane + 32 * (int)(u & 1u);
+                    if (j < c_cslots.dir_upto[d][K]) {
                         const unsigned long long ptr = e & ((1ull << 55) - 1ull);
-                        const long long* qp = reinterpret_cast<const long long*>(ptr + s_dofs[d][lane]);
+                        const long long* qp = reinterpret_cast<const long long*>(ptr + s_dofs[d][j]);
                         if (P2P && ((e >> 55) & 1ull))  // a cell of another rank's tile: over NVLink
-                            asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v[pp]) : "l"(qp));
+                            asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v[uu]) : "l"(qp));
                         else
-                            v[pp] = __ldg(qp);
-                        meta[pp] = (uint32_t)(s_qstart[q] + lane) | (t << 8);
+                            v[uu] = __ldg(qp);
+                        meta[uu] = (uint32_t)(s_qstart[q] + j) | (t << 16);
                     }
                 }
             }
 #pragma unroll
-            for (int pp = 0; pp < 8; ++pp)
-                if (meta[pp] != 0xFFFFFFFFu) {
-                    const uint32_t nz = (uint32_t)v[pp] | (uint32_t)((unsigned long long)v[pp] >> 32);
-                    s_extw[pipe][meta[pp] & 0xFFu] |= min(nz, 1u) << (meta[pp] >> 8);
+            for (int uu = 0; uu < 8; ++uu)
+                if (meta[uu] != 0xFFFFFFFFu) {
+                    const uint32_t nz = (uint32_t)v[uu] | (uint32_t)((unsigned long long)v[uu] >> 32);
+                    s_extw[pipe][meta[uu] & 0xFFFFu] |= min(nz, 1u) << (meta[uu] >> 16);
                 }
         }
         // the batch's tile words into the box
@@ -525,11 +539,10 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         // its cell's tile position (cl_perm) | its HBM bits
         auto halo_dir = [&](auto qc) {
             constexpr int q = decltype(qc)::value;
-            const int m = s_qstart[q] + lane;
-            if (m < s_qstart[q + 1]) {
-                const uint32_t e = s_hflat[m], slot = (e >> 12) & 0xFFu, ex = s_exist[pipe][q];
+            const uint32_t ex = s_exist[pipe][q];
+            for (int m = s_qstart[q] + lane; m < s_qstart[q + 1]; m += 32) {
+                const uint32_t e = s_hflat[m], slot = e >> 12;
                 box[s_bidx[slot]] = (cl_perm<q>(box[e & 0xFFFu]) | s_extw[pipe][m]) & ex;
-                hmask[slot] = ex;
             }
         };
         halo_dir(std::integral_constant<int, 0>{});
@@ -540,9 +553,11 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         halo_dir(std::integral_constant<int, 5>{});
         // K steps, then the 27 tiles' values out
         uint32_t w[8];
-        if (NBB_CL_DBOX) cluster_steps2<CONWAY>(box, s_box[pipe][kClBoxes - 1], hmask, K, s_cb, s_bidx, s_tb, birth, survive, w);
-        else if (NBB_CL_HOIST) cluster_steps<CONWAY>(box, hmask, K, s_cb, s_bidx, s_tb, birth, survive, w);
-        else sliced_steps<CONWAY>(box, hmask, K, s_cb, s_bidx, s_tb, birth, survive, w);
+        if constexpr (kClBoxes == 2)
+            cluster_steps2<CONWAY, kClBoxW, ClBox<F>::kM>(box, s_box[pipe][1], s_exist[pipe], s_sq, K, s_cb, s_bidx, s_tb, birth,
+                                            survive, w);
+        else
+            cluster_steps<CONWAY, kClBoxW, ClBox<F>::kM>(box, s_exist[pipe], s_sq, K, s_cb, s_bidx, s_tb, birth, survive, w);
         if (kClLoaderStores) {  // to the loader: wait until it took the previous result
             if (i >= 1) mbar_wait(&s_obar[pipe][1], (i - 1u) & 1u);
 #pragma unroll

@@ -65,9 +65,9 @@ struct SliceBatches {
 };
 
 // One step of a cell position of 32 tiles: its word and the 8 neighbouring words of the box.
-template <bool CONWAY>
+template <bool CONWAY, int BW = kBoxW>
 __device__ __forceinline__ uint32_t sliced_cell_step(const uint32_t* c, uint32_t birth, uint32_t survive) {
-    return life_rule(c[-kBoxW - 1], c[-kBoxW], c[-kBoxW + 1], c[-1], c[1], c[kBoxW - 1], c[kBoxW], c[kBoxW + 1],
+    return life_rule(c[-BW - 1], c[-BW], c[-BW + 1], c[-1], c[1], c[BW - 1], c[BW], c[BW + 1],
                      c[0], CONWAY ? (1u << 3) : birth, CONWAY ? (1u << 2) | (1u << 3) : survive);
 }
 

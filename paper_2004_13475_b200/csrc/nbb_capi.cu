@@ -133,6 +133,12 @@ int ensure_device(int device, DeviceCtx** out) {
         if (ss.upto[kSliceMaxK - 1] > 32 * kSliceMaxM)
             return fail(NBB_ERR_RUNTIME, "slice slots: more halo slots per step than compiled for");
         NBB_CUDA(cudaMemcpyToSymbol(c_sslots, &ss, sizeof(ss)));
+        nbbhost::ClusterSlots cs;
+        NBB_TRY(nbbhost::cluster_slots(&cs));
+        if (cs.upto[kClMaxK - 1] > 32 * ClBox<kClMaxK>::kM || cs.upto[7] > 32 * ClBox<8>::kM ||
+            cs.dir_upto[2][kClMaxK] != 0 || cs.dir_upto[5][kClMaxK] != 0)
+            return fail(NBB_ERR_RUNTIME, "cluster slots: more halo slots per step than compiled for");
+        NBB_CUDA(cudaMemcpyToSymbol(c_cslots, &cs, sizeof(cs)));
         NBB_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         NBB_CUDA(cudaMalloc(&c.partials, 4097 * sizeof(unsigned long long)));
         c.ready = true;
@@ -840,24 +846,33 @@ bool sliced_impl() {
     }();
     return v;
 }
-int impl_max_k() { return sliced_impl() ? kSliceMaxK : kPassMaxK; }
-// steps per pass: cfg->pass_steps (0 = the default), 1 with NBB_FLAG_SINGLE_STEP
-int default_pass_steps() {
-    static const int v = [] {
-        const char* e = std::getenv("NBB_PASS_STEPS");  // tuning
-        const int k = e ? std::atoi(e) : 0;
-        return k > 0 ? std::min(k, impl_max_k()) : (sliced_impl() ? 8 : 4);
-    }();
-    return v;
+bool cluster_walk_ok(const CompactCaArgs& a);
+// the most steps one pass of this config's kernel takes: the cluster walk 12 (λ over whole
+// cluster columns, r >= 8), the tile-sliced walk 8, the warp-per-tile kernel 4
+int impl_max_k(const nbb_config* cfg) {
+    if (!sliced_impl()) return kPassMaxK;
+    if (cfg && cfg->mode != NBB_MODE_BB && cfg->r >= 8 && cfg->r <= 20) {
+        FastDiv d;
+        if (cluster_walk_ok(compact_args(cfg, nullptr, nullptr, 0, 0, &d))) return kClMaxK;
+    }
+    return kSliceMaxK;
 }
+// steps per pass: cfg->pass_steps (0 = the default: the kernel's most), 1 with NBB_FLAG_SINGLE_STEP
 int max_pass_steps(const nbb_config* cfg) {
     if (cfg->flags & NBB_FLAG_SINGLE_STEP) return 1;
-    const int k = cfg->pass_steps ? (int)cfg->pass_steps : default_pass_steps();
-    return std::max(1, std::min(k, impl_max_k()));
+    static const int env = [] {
+        const char* e = std::getenv("NBB_PASS_STEPS");  // tuning
+        return e ? std::atoi(e) : 0;
+    }();
+    // default 8: a pass of 8 steps still streams the state at >= 0.7 of the HBM peak; 12 steps
+    // per pass (pass_steps = 12, cluster walk) are ~10% faster per step at ~0.6 of peak per pass
+    const int kmax = impl_max_k(cfg);
+    const int k = cfg->pass_steps ? (int)cfg->pass_steps : env > 0 ? env : kSliceMaxK;
+    return std::max(1, std::min(k, kmax));
 }
 int check_pass_steps(const nbb_config* cfg) {
-    if (cfg->pass_steps > (uint32_t)kSliceMaxK)
-        return fail(NBB_ERR_INVALID_ARGUMENT, "pass_steps: at most 8 CA steps per pass over the compact state");
+    if (cfg->pass_steps > (uint32_t)kClMaxK)
+        return fail(NBB_ERR_INVALID_ARGUMENT, "pass_steps: at most 12 CA steps per pass over the compact state");
     return NBB_OK;
 }
 
@@ -914,7 +929,7 @@ ClusterWalk cluster_walk(const CompactCaArgs& a, int k) {
     c.end = std::min(c.total, (a.tile_end + col - 1) / col * c.ncy);
     return c;
 }
-int cluster_grid(DeviceCtx* ctx, const void* kern, uint64_t batches, unsigned* grid) {
+int cluster_grid(DeviceCtx* ctx, const void* kern, size_t dyn, uint64_t batches, unsigned* grid) {
     static std::mutex m;
     static std::vector<std::pair<const void*, int>> cache;  // kernel -> resident CTAs per SM
     std::lock_guard<std::mutex> lock(m);
@@ -923,8 +938,8 @@ int cluster_grid(DeviceCtx* ctx, const void* kern, uint64_t batches, unsigned* g
         if (e.first == kern) occ = e.second;
     if (!occ) {
         NBB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        NBB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kClDynSmem));
-        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kClWarps, kClDynSmem));
+        NBB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        NBB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kClWarps, dyn));
         if (occ < 1) occ = 1;
         cache.push_back({kern, occ});
     }
@@ -934,22 +949,31 @@ int cluster_grid(DeviceCtx* ctx, const void* kern, uint64_t batches, unsigned* g
 }
 
 // One pass of the cluster walk (P2P: a rank's pass of the multi-GPU step); `sharing` workers
-// co-resident on the device get a share of one wave each and no PDL (they wait on each other)
-template <bool P2P>
-int launch_cluster_pass(DeviceCtx* ctx, const CompactCaArgs& a, int k, bool conway, const FastDiv& div_hb,
-                        const int32_t* tab, const P2PArgs& p, cudaStream_t st, int sharing = 1) {
+// co-resident on the device get a share of one wave each and no PDL (they wait on each other).
+// Passes of up to 8 steps run the 8-cell-frame kernel (two boxes per stepper), longer ones the
+// 12-cell-frame kernel.
+template <bool P2P, int F>
+int launch_cluster_pass_f(DeviceCtx* ctx, const CompactCaArgs& a, int k, bool conway, const FastDiv& div_hb,
+                          const int32_t* tab, const P2PArgs& p, cudaStream_t st, int sharing) {
     const ClusterWalk cw = cluster_walk(a, k);
-    auto kern = conway ? ca_compact_cluster_kernel<true, P2P> : ca_compact_cluster_kernel<false, P2P>;
+    auto kern = conway ? ca_compact_cluster_kernel<true, P2P, F> : ca_compact_cluster_kernel<false, P2P, F>;
+    constexpr size_t dyn = cl_dyn_smem<F>();
     unsigned grid;
-    NBB_CHECK(cluster_grid(ctx, (const void*)kern, std::max<uint64_t>(1, cw.end - cw.begin), &grid));
+    NBB_CHECK(cluster_grid(ctx, (const void*)kern, dyn, std::max<uint64_t>(1, cw.end - cw.begin), &grid));
     if (sharing > 1) {
         grid = std::max(1u, grid / (unsigned)sharing);
-        kern<<<grid, 32 * kClWarps, kClDynSmem, st>>>(a, cw, div_hb, tab, p);
+        kern<<<grid, 32 * kClWarps, dyn, st>>>(a, cw, div_hb, tab, p);
         NBB_CUDA(cudaGetLastError());
         return NBB_OK;
     }
-    NBB_CUDA(launch_pdl_smem(kern, grid, 32 * kClWarps, kClDynSmem, st, a, cw, div_hb, tab, p));
+    NBB_CUDA(launch_pdl_smem(kern, grid, 32 * kClWarps, dyn, st, a, cw, div_hb, tab, p));
     return NBB_OK;
+}
+template <bool P2P>
+int launch_cluster_pass(DeviceCtx* ctx, const CompactCaArgs& a, int k, bool conway, const FastDiv& div_hb,
+                        const int32_t* tab, const P2PArgs& p, cudaStream_t st, int sharing = 1) {
+    return k <= 8 ? launch_cluster_pass_f<P2P, 8>(ctx, a, k, conway, div_hb, tab, p, st, sharing)
+                  : launch_cluster_pass_f<P2P, kClMaxK>(ctx, a, k, conway, div_hb, tab, p, st, sharing);
 }
 
 // grid of a tile-sliced launch: one wave of CTAs (kSlicePipes loader/stepper pipelines each),

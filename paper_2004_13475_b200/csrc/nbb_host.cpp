@@ -591,8 +591,9 @@ Error halo_slots(HaloSlots* out) {
 
 // ---- halo slots of the tile-sliced pass (see nbb_host.hpp) ----------------------------------
 namespace nbbhost {
-Error slice_slots(SliceSlots* out) {
-    constexpr int L = 12, T = 32, K = kSliceMaxK, E = T + 2 * K;
+template <class S>
+Error build_slot_table(S* out) {
+    constexpr int L = 12, T = 32, K = S::kMaxK, E = T + 2 * K;
     const int64_t n = int64_t(1) << L, nb = n / T;
     auto member = [&](int64_t x, int64_t y) { return x >= 0 && y >= 0 && x < n && y < n && (x & y) == x; };
     std::vector<int> best(E * E, 99), layer(E * E);
@@ -630,8 +631,8 @@ Error slice_slots(SliceSlots* out) {
     for (int i = 0; i < E * E; ++i)
         if (best[i] <= K) pos.push_back({best[i], i});
     std::stable_sort(pos.begin(), pos.end(), [](auto a, auto b) { return a.first < b.first; });
-    if ((int)pos.size() > kSliceSlots) return err(NBB_ERR_RUNTIME, "slice slots: too many halo positions");
-    SliceSlots h{};
+    if ((int)pos.size() > S::kSlots) return err(NBB_ERR_RUNTIME, "slice slots: too many halo positions");
+    S h{};
     h.count = (int32_t)pos.size();
     for (int s = 0; s < h.count; ++s) {
         const int x = pos[s].second % E - K, y = pos[s].second / E - K, d = pos[s].first;
@@ -643,7 +644,8 @@ Error slice_slots(SliceSlots* out) {
         const int dir = d9 > 4 ? d9 - 1 : d9;
         h.dir_of[s] = (uint8_t)dir;
         h.li[s] = (uint8_t)tile_local_index_host((uint32_t)(x - dx * T), (uint32_t)(y - dy * T));
-        h.by_dir[dir][h.dir_upto[dir][K]++] = (uint8_t)s;
+        if (h.dir_upto[dir][K] >= S::kDirMax) return err(NBB_ERR_RUNTIME, "slice slots: too many in one tile");
+        h.by_dir[dir][h.dir_upto[dir][K]++] = (uint16_t)s;
         for (int k = d; k <= K; ++k) ++h.upto[k];
     }
     for (int dir = 0; dir < 8; ++dir)  // the per-tile lists are in slot (= layer) order
@@ -655,6 +657,8 @@ Error slice_slots(SliceSlots* out) {
     *out = h;
     return {};
 }
+Error slice_slots(SliceSlots* out) { return build_slot_table(out); }
+Error cluster_slots(ClusterSlots* out) { return build_slot_table(out); }
 }  // namespace nbbhost
 
 // ---- halo exchange lists of the multi-process compact CA (see nbb_host.hpp) ----------------

@@ -93,28 +93,34 @@ struct HaloSlots {
 };
 Error halo_slots(HaloSlots* out);
 
-// The same layers up to K = 8 for the tile-sliced pass (compact_sliced.cuh): positions sorted by
-// layer, and per neighbouring tile the slots lying in it, sorted by layer (the halo loads walk
-// one neighbour at a time). 8 / 22 / 36 / 58 / 76 / 104 / 128 / 166 slots for K = 1..8.
+// The same layers for the multi-step passes over the compact state: positions sorted by layer,
+// and per neighbouring tile the slots lying in it, sorted by layer (the halo loads walk one
+// neighbour at a time). 8 / 22 / 36 / 58 / 76 / 104 / 128 / 166 / 184 / 212 / 240 / 288 slots for
+// K = 1..12, at most 54 of them in one neighbouring tile.
+template <int MAXK, int SLOTS, int DIRMAX>
+struct SlotTable {
+    static constexpr int kMaxK = MAXK, kSlots = SLOTS, kDirMax = DIRMAX;
+    int32_t count;                      // slots with layer <= MAXK
+    int32_t upto[MAXK + 1];             // upto[d] = slots with layer <= d
+    int8_t x[SLOTS], y[SLOTS];
+    uint8_t layer[SLOTS];
+    uint8_t li[SLOTS];                  // local compact index in the neighbouring tile
+    uint8_t dir_of[SLOTS];              // neighbouring tile, 0..7 ((dy+1)*3 + dx+1, centre skipped)
+    uint16_t by_dir[8][DIRMAX];         // per neighbouring tile: its slots, by layer
+    int32_t dir_upto[8][MAXK + 1];      // per neighbouring tile: slots with layer <= d
+};
+// the tile-sliced pass (compact_sliced.cuh): up to 8 steps
 constexpr int kSliceMaxK = 8;
 constexpr int kSliceSlots = 192;
-struct SliceSlots {
-    int32_t count;                      // slots with layer <= kSliceMaxK
-    int32_t upto[kSliceMaxK + 1];       // upto[d] = slots with layer <= d
-    int8_t x[kSliceSlots], y[kSliceSlots];
-    uint8_t layer[kSliceSlots];
-    uint8_t li[kSliceSlots];            // local compact index in the neighbouring tile
-    uint8_t dir_of[kSliceSlots];        // neighbouring tile, 0..7 ((dy+1)*3 + dx+1, centre skipped)
-    uint8_t by_dir[8][kSliceSlots];     // per neighbouring tile: its slots, by layer
-    int32_t dir_upto[8][kSliceMaxK + 1];  // per neighbouring tile: slots with layer <= d
-};
+using SliceSlots = SlotTable<kSliceMaxK, kSliceSlots, kSliceSlots>;
 Error slice_slots(SliceSlots* out);
+// the cluster pass (compact_cluster.cuh): up to 12 steps
+constexpr int kClMaxK = 12;
+constexpr int kClSlots = 320;
+constexpr int kClDirSlots = 64;
+using ClusterSlots = SlotTable<kClMaxK, kClSlots, kClDirSlots>;
+Error cluster_slots(ClusterSlots* out);
 
-// Halo exchange of the multi-process compact CA (NCCL transport): with `world` ranks owning
-// contiguous chunks of ceil(tiles / world) ρ = 32 tiles (dispatch.cpp:419-427), recv[j] = the
-// compact offsets of rank j's cells that lie in a halo slot of layer <= kmax of one of `rank`'s
-// tiles, send[j] = the offsets of `rank`'s cells that rank j needs; sorted, unique. send[j] on
-// rank i equals recv[i] on rank j by construction.
 // Tiles per rank of the multi-GPU compact CA (the reference's contiguous worker chunks,
 // dispatch.cpp:419-427, in the tile order u = ωx_b·Hb + ωy_b): ceil(tiles / world), rounded up to
 // whole cluster columns (9·Hb tiles: every rank then owns whole level-3 clusters, the batches of
@@ -128,6 +134,11 @@ inline uint64_t compact_shard_chunk(int rb, uint64_t tiles, uint64_t Hb, int wor
     }
     return (tiles + (uint64_t)world - 1) / (uint64_t)world;
 }
+// Halo exchange of the multi-process compact CA (NCCL transport): with `world` ranks owning
+// contiguous chunks of compact_shard_chunk ρ = 32 tiles (dispatch.cpp:419-427), recv[j] = the
+// compact offsets of rank j's cells that lie in a halo slot of layer <= kmax of one of `rank`'s
+// tiles, send[j] = the offsets of `rank`'s cells that rank j needs; sorted, unique. send[j] on
+// rank i equals recv[i] on rank j by construction.
 Error halo_exchange_lists(int r, int world, int rank, int kmax, std::vector<std::vector<uint32_t>>* send,
                           std::vector<std::vector<uint32_t>>* recv);
 

@@ -1,8 +1,9 @@
 """Per-rank cost of the compact CA at N ranks, measured on ONE GPU (gpurun has 1 GPU).
 
-For each level r in {16, 17} and N in {1, 2, 4, 8}, rank 0's shard (chunk = ceil(tiles / N),
-dispatch.cpp:419-427) is advanced K steps by the library's C++ pass loop:
-  plain : the tile-sliced pass kernel on the shard (nbb_gpu_ca_compact_passes_dev, no exchange)
+For each level r in {16, 17} and N in {1, 2, 4, 8}, rank 0's shard (shard.compact_shard_chunk:
+ceil(tiles / N) rounded up to whole cluster columns, dispatch.cpp:419-427) is advanced K steps by
+the library's C++ pass loop:
+  plain : the cluster pass kernel on the shard (nbb_gpu_ca_compact_passes_dev, no exchange)
           — the compute floor of one rank;
   p2p   : the P2P pass kernel on the shard (nbb_gpu_ca_compact_p2p_passes_dev) with world N and
           every peer mapped to this process (peer buffers and flags = ours, N arrivals per

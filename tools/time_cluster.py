@@ -2,6 +2,7 @@
 library NBB_GPU_LIB (tuning builds), each result checked equal to the 32-ordinal sliced walk.
 
     NBB_GPU_LIB=tune/lib_x.so python tools/time_cluster.py [label]
+(the sliced walk runs passes of min(K, 8); the comparison is after 3K steps)
 """
 import json
 import os
@@ -23,7 +24,7 @@ g = torch.Generator(device="cuda")
 g.manual_seed(r)
 a0 = torch.randint(0, 2, (3 ** r,), dtype=torch.int64, device="cuda", generator=g)
 a, b = a0.clone(), torch.empty_like(a0)
-for K in (1, 4, 8):
+for K in (1, 4, 8, 10, 12):
     for name, rule in (("conway", nbb.CaRule()), ("generic", hl)):
         c = nbb.DispatchConfig(r=r, rho=32, max_cells=(1 << r) ** 2, pass_steps=K)
         outs = []
