@@ -42,13 +42,13 @@ def golden():
         return json.load(f)
 
 
-def run_compact(torch, r, c0, steps, rule, flags=0):
+def run_compact(torch, r, c0, steps, rule, flags=0, pass_steps=0):
     """nbb_gpu_ca_compact_run_dev from the initial compact state; the result back on the host."""
     from paper_2004_13475_b200 import device as dev
     s = torch.cuda.current_stream().cuda_stream
     a = torch.from_numpy(c0).cuda()
     b = torch.empty_like(a)
-    dev.ca_compact_run_dev(cfg(r, flags=flags), a.data_ptr(), b.data_ptr(), steps, rule, s)
+    dev.ca_compact_run_dev(cfg(r, flags=flags, pass_steps=pass_steps), a.data_ptr(), b.data_ptr(), steps, rule, s)
     out = (a if steps % 2 == 0 else b).cpu().numpy()
     del a, b
     return out
@@ -103,6 +103,26 @@ def test_c3_compact_trajectory_full_size(rule_name):
         if k in (4, 20):
             single = run_compact(torch, r, c0, k, rule, flags=_abi.FLAG_SINGLE_STEP)
             assert np.array_equal(single, want), (rule_name, k, "single step")
+
+
+def test_c3_passes_of_12_full_size():
+    """C3 at full size in passes of up to 12 steps (pass_steps = 12: the cluster kernel with the
+    radius-12 halo): all 3^16 cells equal the oracle after 9, 12, 20 and 24 steps, and the
+    digests equal the reference's."""
+    import torch
+    r = 16
+    c0 = orc_random_member_compact(r, 17, 2)
+    g = golden()
+    gt = g["trajectories"].get("B3/S23") if g else None
+    want, done = c0, 0
+    for k in (9, 12, 20, 24):
+        want = orc_ca_compact(r, want, k - done, CONWAY.birth, CONWAY.survive)
+        done = k
+        got = run_compact(torch, r, c0, k, CONWAY, pass_steps=12)
+        bad = np.flatnonzero(got != want)
+        assert bad.size == 0, (k, bad.size, bad[:8])
+        if gt is not None and str(k) in gt:
+            assert (int(want.sum()), fnv1a64(want)) == (gt[str(k)]["population"], gt[str(k)]["fnv"]), k
 
 
 def test_c3_embedded_int64_one_step_full_size():

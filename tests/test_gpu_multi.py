@@ -40,7 +40,8 @@ def test_ca_multi_matches_oracle(r, workers):
 
 
 def test_ca_multi_rules_pass_lengths_and_pinned_io():
-    """A generic rule, every pass length (pass_steps 1..8) and the zero-copy pinned host path."""
+    """A generic rule, every pass length (pass_steps 1..12: the cluster walk's F = 8 and F = 12
+    kernels over peer memory) and the zero-copy pinned host path."""
     torch = pytest.importorskip("torch")
     import ctypes
     r = 11
@@ -48,7 +49,7 @@ def test_ca_multi_rules_pass_lengths_and_pinned_io():
     init = orc_random_member_grid(r, 5, 2)
     rule = CaRule(birth=(1 << 3) | (1 << 6), survive=(1 << 2) | (1 << 3))
     want = orc_ca(r, init, 9, rule.birth, rule.survive)
-    for k in (1, 2, 3, 5, 8):
+    for k in (1, 2, 3, 5, 8, 9, 12):
         got = nbb.run_ca_multi(cfg(r, pass_steps=k), devs, Grid(GASKET, r, init), 9, rule)
         assert np.array_equal(got.grid.values, want), k
     lib = _abi.load()
