@@ -12,20 +12,23 @@
 // of ωx (the closed-form λ, at block level). The 27 tiles with
 // ωx = 9 cx + i (i < 9) and ωy = 3 cy + j (j < 3) are therefore the member tiles of one 8 x 8-tile
 // box: a level-3 sub-gasket. Bit t = 3 i + j of the batch's words is tile (i, j). A tile's
-// neighbour in direction d is then, for all but a handful of tiles, ANOTHER TILE OF THE BATCH:
-// its halo word is a bit permutation of the batch's own tile words, built in shared memory with
-// one broadcast load + one ballot per halo slot (lane t picks bit π_d(t)). Sub-gaskets touch their
-// neighbours only at corners, so at most 6 (tile, direction) pairs per cluster reach outside it
-// (measured at r_b = 11: mean 5.0, max 6): those few halo cells come from HBM as before. The halo
-// reads drop from 27 x 166 scattered values per batch to ~150.
+// neighbour in direction q is then, for all but a handful of tiles, ANOTHER TILE OF THE BATCH,
+// and the same one in every cluster: a halo slot's word is a fixed bit permutation of the batch's
+// own word at the slot's cell (cl_perm<q>, masked shifts with compile-time constants). Sub-gaskets
+// touch their neighbours only at corners, so at most 6 (tile, direction) pairs per cluster reach
+// outside it (measured at r_b = 11: mean 5.0, max 6): those few halo cells come from HBM (in a
+// multi-GPU pass from the owning rank's buffer). The halo reads drop from 27 x 166 scattered
+// values per batch to ~150.
 //
 // Memory: tile (i, j) is the 9 x 27 compact sub-block at 9 (9 cx + i) W + 27 (3 cy + j), so a
 // cluster is 9 groups (one per i) of three consecutive tiles = nine 81-value (648 B) runs of
 // compact rows per group; the loader fetches a group with nine bulk (TMA) copies into a
-// double-buffered staging area and folds it into the stage words, as in the sliced λ loader.
-// The steps are the sliced pass's cell update with radius up to 12 (cluster_steps). Needs r_b >= 3 (ωx has two digits,
-// ωy one) and the whole orthotope in one launch (the single-device λ walk); shards, the BB walk
-// and the multi-GPU pass keep the 32-ordinal batches of compact_sliced.cuh.
+// double-buffered staging area, folds it into the stage words and stores the stepper's previous
+// results; the stepper builds the halo words and runs the K steps (cluster_steps / _steps2,
+// radius up to 12). Needs r_b >= 3 (ωx has two digits, ωy one) and a launch range of whole
+// cluster columns (9 Hb tiles: the whole orthotope, or a multi-GPU shard of
+// nbbhost::compact_shard_chunk); the BB walk and r < 8 keep the 32-ordinal batches of
+// compact_sliced.cuh.
 #pragma once
 
 #include <type_traits>
