@@ -288,8 +288,13 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         pdl_wait();
     }
     __syncthreads();
-    // every thread orders its peer reads after the arrivals waited for
-    if (P2P && p.wait_target != 0u) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    // every thread orders its peer reads after the arrivals waited for; the proxy
+    // fence orders the generic-proxy stores it acquired (this rank's previous pass) before the
+    // loader's bulk copies (async proxy) of the same buffer
+    if (P2P && p.wait_target != 0u) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
 
     uint32_t* box = s_box[pipe][0];
     const uint32_t pipe_global = blockIdx.x * kClPipes + (uint32_t)pipe;

@@ -236,7 +236,10 @@ __global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB)
     // the poller's ld.acquire.sys synchronises with the peers' fence.acq_rel.sys + red.relaxed.sys,
     // bar.sync carries that to the CTA, and this fence makes each thread's own later ld.relaxed.sys
     // of peer memory observe it at system scope
-    if (P2P && p.wait_target != 0u) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    if (P2P && p.wait_target != 0u) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // before the λ loader's bulk copies
+    }
     // the lane's tile cells li = 32k + lane (loads, stores): byte offset in a tile's sub-block
     // (recomputed per batch: short register lifetimes); the cells it advances in the steps: the
     // (32k + lane)-th member in row-major order, so the 32 lanes' box words of one access fall on
