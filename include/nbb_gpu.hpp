@@ -104,7 +104,7 @@ struct DispatchConfig {  // dispatch.hpp:25-38
     // serves the call, Compact = require it, Embedded = the reference's n x n layout.
     enum class State { Auto, Compact, Embedded } state = State::Auto;
     std::uint32_t flags = 0;       // further NBB_FLAG_* (e.g. NBB_FLAG_OUT_ZEROED)
-    std::uint32_t pass_steps = 0;  // compact state: steps per pass, 1..8 (0 = 8)
+    std::uint32_t pass_steps = 0;  // compact state: steps per pass, 1..12 (0 = 8; > 8: cluster walk only)
 
     nbb_config c() const {
         nbb_config out;

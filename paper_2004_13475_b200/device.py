@@ -98,7 +98,7 @@ def ca_compact_run_dev(config: DispatchConfig, d_a: int, d_b: int, steps: int, r
 
 def ca_compact_passes_dev(config: DispatchConfig, d_a: int, d_b: int, steps: int, rule: CaRule = CaRule(),
                           stream: int = 0, parity: bool = False) -> "_abi.NbbPassStats":
-    """`steps` steps in passes of up to config.pass_steps steps (default 4); without `parity`
+    """`steps` steps in passes of up to config.pass_steps steps (default 8); without `parity`
     the fewest passes, the result in d_b iff the returned stats.result_in_b."""
     st = _abi.NbbPassStats()
     _check(_lib().nbb_gpu_ca_compact_passes_dev(ctypes.byref(config.to_c()), _vp(d_a), _vp(d_b), steps,

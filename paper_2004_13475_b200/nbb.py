@@ -219,7 +219,7 @@ class DispatchConfig:
     shard_begin: int = 0
     shard_count: int = 0  # 0 = every block ordinal of the plan
     flags: int = 0        # _abi.FLAG_* (e.g. FLAG_OUT_ZEROED)
-    pass_steps: int = 0   # compact CA: at most this many steps per pass (1..8; 0 = 8)
+    pass_steps: int = 0   # compact CA: at most this many steps per pass (1..12; 0 = 8; above 8: r >= 8 only)
 
     def to_c(self) -> _abi.NbbConfig:
         c = _abi.NbbConfig()

@@ -2,7 +2,8 @@
 
 The tile ordinal range o = ωy*W + ωx of the λ orthotope is split into contiguous
 chunks, chunk = ceil(total / world) — the same split the reference applies to its
-worker threads (dispatch.cpp:419-427). SW and RD need no exchange (RD ends in one
+worker threads (dispatch.cpp:419-427); for the compact state rounded up to whole cluster
+columns (compact_shard_chunk), the unit of the library's cluster pass. SW and RD need no exchange (RD ends in one
 all-reduce of an int64). A CA step reads, besides its own tile, at most 8 cells of
 neighbouring tiles (the tile's "halo"):
 
@@ -502,7 +503,7 @@ def _check(rc: int) -> None:
 class NcclCompactCA:
     """The multi-process compact CA over the library's own NCCL communicator (nbb_gpu_comm_*,
     include/nbb_gpu.h): one process per GPU, rank i owning the contiguous tile chunk i of
-    ceil(tiles / world) (dispatch.cpp:419-427); before every pass of up to 8 steps the halo cells
+    compact_shard_chunk (dispatch.cpp:419-427); before every pass of up to 8 steps the halo cells
     its tiles read from other ranks within 8 steps are exchanged by ncclSend / ncclRecv inside the
     library, then the pass kernel advances the rank's tiles. The communicator's id travels over
     the caller's process group (`dist`, any backend); dist=None is a single rank."""
