@@ -63,7 +63,7 @@ struct ClusterWalk {
     FastDiv div_ncy;
     uint32_t total;       // clusters: (Wb / 9) (Hb / 3)
     uint32_t begin, end;  // this launch's clusters (a shard: whole cluster columns)
-    int K;                // steps per pass, 1..8
+    int K;                // steps per pass, 1..12
 };
 
 // The in-cluster neighbour of tile t = 3 i + j in halo direction q (q = 0..5: directions
@@ -108,9 +108,9 @@ __device__ __forceinline__ uint32_t cl_perm(uint32_t x) {
 #endif
 constexpr bool kClLoaderStores = NBB_CL_LSTORE != 0;
 
-// K steps of a batch in its box (sliced_steps with the lane's box indices and halo masks held in
-// registers across the steps: shared memory is written between the steps, so the compiler
-// would reload them every step)
+// K steps of a batch in its box (sliced_steps of compact_sliced.cuh with the box pitch BW, up to
+// 32 M halo slots, and the lane's box indices and halo masks held in registers across the steps:
+// shared memory is written between the steps, so the compiler would reload them every step)
 template <bool CONWAY, int BW, int M>
 __device__ __forceinline__ void cluster_steps(uint32_t* box, const uint32_t* exist, const uint8_t* sq, int K,
                                               const uint16_t* cb,
@@ -194,7 +194,6 @@ __device__ __forceinline__ void cluster_steps2(uint32_t* box0, uint32_t* box1, c
 
 template <int F>
 constexpr size_t cl_dyn_smem() { return kClTmaBytes + (size_t)kClPipes * ClBox<F>::kBoxes * ClBox<F>::kWords * 4; }
-
 
 #ifndef NBB_CLUSTER_MINB  // resident CTAs per SM the register budget is cut for (tuning builds)
 #define NBB_CLUSTER_MINB 3
