@@ -278,4 +278,48 @@ __device__ __forceinline__ uint32_t life_rule(uint32_t n0, uint32_t n1, uint32_t
     return (b3 & leaf[8]) | (~b3 & m07);
 }
 
+// A Life-like rule as the constants of two count-indexed mux trees, S for live centres and B for
+// dead ones (leaf v = 0 or ~0: bit v of survive / birth). Level-0 node k of a tree is
+// leaf[2k] ^ (b0 & (leaf[2k] ^ leaf[2k + 1])): every constant enters one logic op as a
+// constant-bank operand (the table is a kernel parameter), so a runtime rule costs no per-cell
+// materialisation of its 18 leaf masks (life_rule's `bit ? ~0 : 0` per leaf and cell).
+struct RuleTab {
+    uint32_t sd[4], se[4], s8;  // survive tree: leaf[2k] ^ leaf[2k + 1], leaf[2k], leaf[8]
+    uint32_t bd[4], be[4], b8;  // birth tree
+};
+__host__ __device__ inline RuleTab make_rule_tab(uint32_t birth, uint32_t survive) {
+    RuleTab t{};
+    auto leaf = [](uint32_t m, int v) { return ((m >> v) & 1u) ? 0xFFFFFFFFu : 0u; };
+    for (int k = 0; k < 4; ++k) {
+        t.se[k] = leaf(survive, 2 * k);
+        t.sd[k] = leaf(survive, 2 * k) ^ leaf(survive, 2 * k + 1);
+        t.be[k] = leaf(birth, 2 * k);
+        t.bd[k] = leaf(birth, 2 * k) ^ leaf(birth, 2 * k + 1);
+    }
+    t.s8 = leaf(survive, 8);
+    t.b8 = leaf(birth, 8);
+    return t;
+}
+// life_rule with the rule as a RuleTab (same adder tree; bit-identical results)
+__device__ __forceinline__ uint32_t life_rule_tab(uint32_t n0, uint32_t n1, uint32_t n2, uint32_t n3, uint32_t n4,
+                                                  uint32_t n5, uint32_t n6, uint32_t n7, uint32_t centre,
+                                                  const RuleTab& t) {
+    const uint32_t s0 = n0 ^ n1 ^ n2, c0 = (n0 & n1) | (n2 & (n0 ^ n1));
+    const uint32_t s1 = n3 ^ n4 ^ n5, c1 = (n3 & n4) | (n5 & (n3 ^ n4));
+    const uint32_t s2 = n6 ^ n7, c2 = n6 & n7;
+    const uint32_t b0 = s0 ^ s1 ^ s2, k0 = (s0 & s1) | (s2 & (s0 ^ s1));
+    const uint32_t u0 = c0 ^ c1 ^ c2, v0 = (c0 & c1) | (c2 & (c0 ^ c1));
+    const uint32_t b1 = u0 ^ k0, w0 = u0 & k0;
+    const uint32_t b2 = v0 ^ w0, b3 = v0 & w0;
+    auto tree = [&](const uint32_t* d, const uint32_t* e, uint32_t l8) {
+        const uint32_t m0 = e[0] ^ (b0 & d[0]), m1 = e[1] ^ (b0 & d[1]);
+        const uint32_t m2 = e[2] ^ (b0 & d[2]), m3 = e[3] ^ (b0 & d[3]);
+        const uint32_t q0 = (b1 & m1) | (~b1 & m0), q1 = (b1 & m3) | (~b1 & m2);
+        const uint32_t o = (b2 & q1) | (~b2 & q0);
+        return (b3 & l8) | (~b3 & o);  // count 8: b0 = b1 = b2 = 0
+    };
+    const uint32_t sv = tree(t.sd, t.se, t.s8), bv = tree(t.bd, t.be, t.b8);
+    return (centre & sv) | (~centre & bv);
+}
+
 }  // namespace nbbgpu

@@ -64,6 +64,7 @@ struct ClusterWalk {
     uint32_t total;       // clusters: (Wb / 9) (Hb / 3)
     uint32_t begin, end;  // this launch's clusters (a shard: whole cluster columns)
     int K;                // steps per pass, 1..12
+    RuleTab rule;         // the rule's mux-tree constants (the generic-rule instantiation)
 };
 
 // The in-cluster neighbour of tile t = 3 i + j in halo direction q (q = 0..5: directions
@@ -114,8 +115,8 @@ constexpr bool kClLoaderStores = NBB_CL_LSTORE != 0;
 template <bool CONWAY, int BW, int M>
 __device__ __forceinline__ void cluster_steps(uint32_t* box, const uint32_t* exist, const uint8_t* sq, int K,
                                               const uint16_t* cb,
-                                              const uint16_t* bidx, const uint16_t* tb, uint32_t birth,
-                                              uint32_t survive, uint32_t (&w)[8]) {
+                                              const uint16_t* bidx, const uint16_t* tb, const RuleTab& rt,
+                                              uint32_t (&w)[8]) {
     const int lane = threadIdx.x & 31;
     const bool k7 = lane < 19;
     __syncwarp();
@@ -132,13 +133,13 @@ __device__ __forceinline__ void cluster_steps(uint32_t* box, const uint32_t* exi
     for (int j = 1; j <= K; ++j) {
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (k < 7 || k7) w[k] = sliced_cell_step<CONWAY, BW>(box + ci[k], birth, survive);
+            if (k < 7 || k7) w[k] = sliced_cell_step<CONWAY, BW>(box + ci[k], rt);
         const int ns = c_cslots.upto[K - j];
         uint32_t hn[M];
 #pragma unroll
         for (int m = 0; m < M; ++m) {
             hn[m] = 0u;
-            if (lane + 32 * m < ns) hn[m] = sliced_cell_step<CONWAY, BW>(box + hi[m], birth, survive) & hm[m];
+            if (lane + 32 * m < ns) hn[m] = sliced_cell_step<CONWAY, BW>(box + hi[m], rt) & hm[m];
         }
         __syncwarp();
 #pragma unroll
@@ -161,7 +162,7 @@ template <bool CONWAY, int BW, int M>
 __device__ __forceinline__ void cluster_steps2(uint32_t* box0, uint32_t* box1, const uint32_t* exist,
                                                const uint8_t* sq, int K,
                                                const uint16_t* cb, const uint16_t* bidx, const uint16_t* tb,
-                                               uint32_t birth, uint32_t survive, uint32_t (&w)[8]) {
+                                               const RuleTab& rt, uint32_t (&w)[8]) {
     const int lane = threadIdx.x & 31;
     const bool k7 = lane < 19;
     __syncwarp();
@@ -180,11 +181,11 @@ __device__ __forceinline__ void cluster_steps2(uint32_t* box0, uint32_t* box1, c
         uint32_t* dst = (j & 1) ? box1 : box0;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (k < 7 || k7) dst[ci[k]] = sliced_cell_step<CONWAY, BW>(src + ci[k], birth, survive);
+            if (k < 7 || k7) dst[ci[k]] = sliced_cell_step<CONWAY, BW>(src + ci[k], rt);
         const int ns = c_cslots.upto[K - j];
 #pragma unroll
         for (int m = 0; m < M; ++m)
-            if (lane + 32 * m < ns) dst[hi[m]] = sliced_cell_step<CONWAY, BW>(src + hi[m], birth, survive) & hm[m];
+            if (lane + 32 * m < ns) dst[hi[m]] = sliced_cell_step<CONWAY, BW>(src + hi[m], rt) & hm[m];
         __syncwarp();
     }
     const uint32_t* fin = (K & 1) ? box1 : box0;
@@ -207,7 +208,6 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
     ca_compact_cluster_kernel(CompactCaArgs a, ClusterWalk cw, FastDiv div_hb, const int32_t* __restrict__ nbr_tab,
                               P2PArgs p) {
     constexpr int kClBoxW = ClBox<F>::kW, kClBoxWords = ClBox<F>::kWords, kClBoxes = ClBox<F>::kBoxes;
-    const uint32_t birth = a.birth, survive = a.survive;
     __shared__ uint32_t s_stage[kClPipes][2][kStageWords];
     __shared__ uint8_t s_sq[kClSlots];                     // halo direction q of every slot
     __shared__ uint32_t s_dofs[8][kClDirSlots];           // per direction, slot j: offset in the neighbour tile (B)
@@ -561,10 +561,10 @@ __global__ void __launch_bounds__(32 * kClWarps, NBB_CLUSTER_MINB)
         // K steps, then the 27 tiles' values out
         uint32_t w[8];
         if constexpr (kClBoxes == 2)
-            cluster_steps2<CONWAY, kClBoxW, ClBox<F>::kM>(box, s_box[pipe][1], s_exist[pipe], s_sq, K, s_cb, s_bidx, s_tb, birth,
-                                            survive, w);
+            cluster_steps2<CONWAY, kClBoxW, ClBox<F>::kM>(box, s_box[pipe][1], s_exist[pipe], s_sq, K, s_cb, s_bidx, s_tb,
+                                                          cw.rule, w);
         else
-            cluster_steps<CONWAY, kClBoxW, ClBox<F>::kM>(box, s_exist[pipe], s_sq, K, s_cb, s_bidx, s_tb, birth, survive, w);
+            cluster_steps<CONWAY, kClBoxW, ClBox<F>::kM>(box, s_exist[pipe], s_sq, K, s_cb, s_bidx, s_tb, cw.rule, w);
         if (kClLoaderStores) {  // to the loader: wait until it took the previous result
             if (i >= 1) mbar_wait(&s_obar[pipe][1], (i - 1u) & 1u);
 #pragma unroll

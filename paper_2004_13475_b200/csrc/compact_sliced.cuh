@@ -62,13 +62,18 @@ struct SliceBatches {
     uint32_t last_cols;               // then columns [0, last_cols) of one more row
     uint32_t total;                   // batches
     int K;                            // steps per pass, 1..8
+    RuleTab rule;                     // the rule's mux-tree constants (generic-rule instantiation)
 };
 
-// One step of a cell position of 32 tiles: its word and the 8 neighbouring words of the box.
+// One step of a cell position of 32 tiles: its word and the 8 neighbouring words of the box
+// (B3/S23 constant-folded; any other rule through its RuleTab, a kernel parameter).
 template <bool CONWAY, int BW = kBoxW>
-__device__ __forceinline__ uint32_t sliced_cell_step(const uint32_t* c, uint32_t birth, uint32_t survive) {
-    return life_rule(c[-BW - 1], c[-BW], c[-BW + 1], c[-1], c[1], c[BW - 1], c[BW], c[BW + 1],
-                     c[0], CONWAY ? (1u << 3) : birth, CONWAY ? (1u << 2) | (1u << 3) : survive);
+__device__ __forceinline__ uint32_t sliced_cell_step(const uint32_t* c, const RuleTab& rt) {
+    if constexpr (CONWAY)
+        return life_rule(c[-BW - 1], c[-BW], c[-BW + 1], c[-1], c[1], c[BW - 1], c[BW], c[BW + 1], c[0], 1u << 3,
+                         (1u << 2) | (1u << 3));
+    else
+        return life_rule_tab(c[-BW - 1], c[-BW], c[-BW + 1], c[-1], c[1], c[BW - 1], c[BW], c[BW + 1], c[0], rt);
 }
 
 // K steps of a batch in its box: the tile's member positions (lane: members 32k + lane in
@@ -77,22 +82,22 @@ __device__ __forceinline__ uint32_t sliced_cell_step(const uint32_t* c, uint32_t
 // li = 32k + lane, box index table tb) into w.
 template <bool CONWAY>
 __device__ __forceinline__ void sliced_steps(uint32_t* box, const uint32_t* hmask, int K, const uint16_t* cb,
-                                             const uint16_t* bidx, const uint16_t* tb, uint32_t birth,
-                                             uint32_t survive, uint32_t (&w)[8]) {
+                                             const uint16_t* bidx, const uint16_t* tb, const RuleTab& rt,
+                                             uint32_t (&w)[8]) {
     const int lane = threadIdx.x & 31;
     const bool k7 = lane < 19;  // member / cell 32 * 7 + lane < 243
     __syncwarp();
     for (int j = 1; j <= K; ++j) {
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-            if (k < 7 || k7) w[k] = sliced_cell_step<CONWAY>(box + cb[32 * k + lane], birth, survive);
+            if (k < 7 || k7) w[k] = sliced_cell_step<CONWAY>(box + cb[32 * k + lane], rt);
         const int ns = c_sslots.upto[K - j];
         uint32_t hn[kSliceMaxM];
 #pragma unroll
         for (int m = 0; m < kSliceMaxM; ++m) {
             const int s = lane + 32 * m;
             hn[m] = 0u;
-            if (s < ns) hn[m] = sliced_cell_step<CONWAY>(box + bidx[s], birth, survive) & hmask[s];
+            if (s < ns) hn[m] = sliced_cell_step<CONWAY>(box + bidx[s], rt) & hmask[s];
         }
         __syncwarp();
 #pragma unroll
@@ -184,7 +189,6 @@ __global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB)
     ca_compact_sliced_kernel(CompactCaArgs a, SliceBatches sb, FastDiv div_hb, const int32_t* __restrict__ nbr_tab,
                              P2PArgs p) {
     static_assert(!(P2P && BB), "the multi-GPU pass walks the λ orthotope");
-    const uint32_t birth = a.birth, survive = a.survive;
     __shared__ uint32_t s_box[kSlicePipes][kBoxWords];
     __shared__ uint32_t s_stage[kSlicePipes][2][kStageWords]; // loader -> stepper tile words
     __shared__ uint32_t s_hmask[kSlicePipes][kSliceSlots];   // slot s exists in tile t: bit t
@@ -372,7 +376,7 @@ __global__ void __launch_bounds__(32 * kSliceWarps, NBB_SLICE_MINB)
     };
     auto step_batch = [&](uint32_t u, uint32_t cnt, uint32_t base0, uint32_t* box, const uint32_t* hmask) {
         uint32_t w[8];
-        sliced_steps<CONWAY>(box, hmask, K, s_cb, s_bidx, s_tb, birth, survive, w);
+        sliced_steps<CONWAY>(box, hmask, K, s_cb, s_bidx, s_tb, sb.rule, w);
         // cell li of tile t = bit t of w[k]
 #ifdef NBB_EXP_NOSTORE
         if (w[0] != 0x12345u) return;

@@ -880,6 +880,7 @@ int check_pass_steps(const nbb_config* cfg) {
 SliceBatches slice_batches(const CompactCaArgs& a, int k) {
     SliceBatches b{};
     b.K = k;
+    b.rule = make_rule_tab(a.birth, a.survive);
     const uint32_t Hb = a.Hb;
     b.nb_row = (Hb + 31u) / 32u;
     b.div_nb_row.d = b.nb_row;
@@ -955,7 +956,8 @@ int cluster_grid(DeviceCtx* ctx, const void* kern, size_t dyn, uint64_t batches,
 template <bool P2P, int F>
 int launch_cluster_pass_f(DeviceCtx* ctx, const CompactCaArgs& a, int k, bool conway, const FastDiv& div_hb,
                           const int32_t* tab, const P2PArgs& p, cudaStream_t st, int sharing) {
-    const ClusterWalk cw = cluster_walk(a, k);
+    ClusterWalk cw = cluster_walk(a, k);
+    cw.rule = make_rule_tab(a.birth, a.survive);
     auto kern = conway ? ca_compact_cluster_kernel<true, P2P, F> : ca_compact_cluster_kernel<false, P2P, F>;
     constexpr size_t dyn = cl_dyn_smem<F>();
     unsigned grid;
