@@ -60,3 +60,21 @@ def test_cluster_walk_arbitrary_int64_values():
     want = orc_ca_compact(r, c0, 12, CaRule().birth, CaRule().survive)
     for k in (1, 8, 12):
         assert np.array_equal(run(torch, r, raw, 12, CaRule(), k, "cluster"), want), k
+
+
+def test_cluster_walk_random_rules():
+    """Runtime rules (RuleTab: the rule as mux-tree constants in the kernel parameters) for 40
+    random birth / survive masks over counts 0..8, including count-0 births and count-8 survival,
+    in passes of 8 and 12 steps, against the oracle."""
+    torch = pytest.importorskip("torch")
+    r = 10
+    rng = np.random.default_rng(2026)
+    c0 = orc_random_member_compact(r, 77, 2)
+    rules = [CaRule(birth=int(b), survive=int(s)) for b, s in rng.integers(0, 1 << 9, size=(38, 2))]
+    rules += [CaRule(birth=1 | (1 << 8), survive=1 << 8), CaRule(birth=0x1FF, survive=0)]
+    for rule in rules:
+        want = orc_ca_compact(r, c0, 13, rule.birth, rule.survive)
+        for k in (8, 12):
+            got = run(torch, r, c0, 13, rule, k, "cluster")
+            assert np.array_equal(got, want), (rule.birth, rule.survive, k)
+        assert np.array_equal(run(torch, r, c0, 13, rule, 8, "sliced"), want), (rule.birth, rule.survive)
